@@ -1,0 +1,214 @@
+/*
+ * zdc.h — C ABI of the B200-native ZDC hot path (zero-delay QKV compression,
+ * arxiv 2408.04107).  "P:<n>" cites /root/reference/PAPER.md line n (section / equation
+ * given alongside); DESIGN.md §3 lists every reading of a silent or ambiguous passage.
+ *
+ * Library: libzdc.so (built in-tree for sm_100a).  Every entry point is extern "C",
+ * takes plain pointers and sizes, and never takes ownership of a caller buffer.
+ *
+ * Conventions
+ *   - Status: ZDC_OK (0) or a negative zdc_status.  zdc_last_error() returns the
+ *     message of the last failing call on the calling thread.
+ *   - Device calls are asynchronous on `stream` (a cudaStream_t passed as void*; NULL =
+ *     legacy default stream).  Argument and shape errors are detected synchronously,
+ *     before anything is enqueued; asynchronous CUDA / NCCL faults surface on the next
+ *     call as ZDC_ERR_CUDA / ZDC_ERR_NCCL.
+ *   - Element types: "bf16" = IEEE bfloat16 bit patterns (uint16_t), "f32" = float,
+ *     "f64" = double.  Matrices are dense row-major unless stated.
+ *   - Ownership: the caller owns every buffer (host and device).  The library owns the
+ *     zdc_ctx host metadata and, after zdc_comm_init, the NCCL communicator; both are
+ *     released by zdc_ctx_destroy.
+ *   - There is no CPU fallback: a call that needs the GPU fails with ZDC_ERR_CUDA when
+ *     no sm_100 device is present.
+ */
+#ifndef ZDC_H
+#define ZDC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ZDC_OK = 0,
+  ZDC_ERR_INVALID_ARG = -1,     /* null pointer, non-finite input, aliasing, bad enum */
+  ZDC_ERR_SHAPE = -2,           /* dimension mismatch; the message names both shapes  */
+  ZDC_ERR_NOT_ORTHONORMAL = -3, /* fold produced R with |R^T R - I| > 1e-10            */
+  ZDC_ERR_NO_CONVERGENCE = -4,  /* one-sided Jacobi did not converge in 60 sweeps      */
+  ZDC_ERR_CAPACITY = -5,        /* len + S > max_seq, B > max_batch                    */
+  ZDC_ERR_CUDA = -6,
+  ZDC_ERR_NCCL = -7,
+  ZDC_ERR_UNSUPPORTED = -8,     /* shape the kernels do not implement (see zdc_ctx_create) */
+  ZDC_ERR_STATE = -9            /* call order: unbound ctx, prefill on a non-empty cache,
+                                   representative layer has not classified a position  */
+} zdc_status;
+
+const char* zdc_last_error(void);
+const char* zdc_version(void);
+
+/* Model dimensions (Table tab:symbols): d = d_model, N_h = n_heads,
+ * d_h = d_head = d / N_h in the paper; GQA (n_kv_heads < n_heads) is reading c4. */
+typedef struct {
+  int32_t n_layers, d_model, n_heads, n_kv_heads, d_head;
+} zdc_dims;
+
+/* Compression plan {g^l, p_QK^i, p_QK^u, p_VL^i, p_VL^u} (§5.2 Eqs. 5-6),
+ * expressed as integer kept ranks (reading c6: r = ceil((1-p) d_h)) and g in basis
+ * points (reading c11).  Every array has n_layers entries.
+ *   1 <= r_*_unimp[l] <= r_*_imp[l] <= d_head.
+ *   g_bp[l] in [0, 10000]; 10000 = no token split at layer l (all tokens important).
+ *   group_rep[l] <= l and group_rep[group_rep[l]] == group_rep[l]; g_bp and the four
+ *     ranks are equal within a group (reading c15).  The representative classifies the
+ *     tokens; the other layers of the group reuse its classes.
+ *   importance_mode 0 = raw sum_h sum_{k<=t} exp(s) (default);
+ *                   1 = per-key mean (minus log(t+1) per head, reading c10). */
+typedef struct {
+  const int32_t *r_qk_imp, *r_qk_unimp, *r_vl_imp, *r_vl_unimp;
+  const int32_t *g_bp;
+  const int32_t *group_rep;
+  int32_t importance_mode;
+} zdc_plan;
+
+/* ------------------------------------------------------------------------------------
+ * (1) Offline fold of ONE layer — host, fp64, NOT part of the timed hot path.
+ *
+ * P:977 and P:989-990 (§4.3, "Finding common rotation matrix offline"): per head
+ * (here per KV group g, reading c4) stack [Q^h for h in group; K^g] ("concatenate
+ * them into a 2 Sigma_S x d_h matrix") and [V^g; (W_O^h)^T for h in group] ((Sigma_S + d) x d_h),
+ * with Q^h = X_c W_Q^h etc. (Eq. 1); R = right singular vectors (A = U Sigma R^T,
+ * P:300 §2.2), sorted by non-increasing sigma, canonical signs (reading c5: the entry of
+ * largest |.| of each column is positive, ties to the lowest row).  Fold (P:1204,
+ * P:1218-1219, Lemma 1): W_Q^{R,h} = W_Q^h R_qk, W_K^{R,g} = W_K^g R_qk,
+ * W_V^{R,g} = W_V^g R_vl, W_O^{R,h} = R_vl^T W_O^h (reading c1).
+ * Algorithm: Householder QR of each stacked block (TSQR), then one-sided Jacobi SVD of
+ * the d_h x d_h triangular factor (no Gram matrix, so tiny singular values keep their
+ * relative accuracy).
+ *
+ *   wq [d][N_h d_h], wk [d][N_kv d_h], wv [d][N_kv d_h], wo [N_h d_h][d]: unfolded, f64.
+ *   calib_x [n_calib][d]: this layer's inputs (stands in for the pruned, k-meaned history
+ *     of P:1154-1167, reading c8).  n_calib (G+1) >= d_h else ZDC_ERR_SHAPE.
+ *   r_qk, r_vl [N_kv][d_h][d_h] (column j = j-th right singular vector);
+ *   sigma_qk, sigma_vl [N_kv][d_h] non-increasing;
+ *   wq_f, wk_f, wv_f, wo_f: full-rank folded weights, same shapes as the inputs.
+ * All outputs are caller-owned host buffers.  Non-finite input -> ZDC_ERR_INVALID_ARG.
+ * ---------------------------------------------------------------------------------- */
+zdc_status zdc_fold_weights(const zdc_dims* dims,
+                            const double* wq, const double* wk, const double* wv, const double* wo,
+                            const double* calib_x, int64_t n_calib,
+                            double* r_qk, double* r_vl, double* sigma_qk, double* sigma_vl,
+                            double* wq_f, double* wk_f, double* wv_f, double* wo_f);
+
+/* ------------------------------------------------------------------------------------
+ * Context: host metadata only.  Device memory is caller-owned: query the three sizes,
+ * allocate (any allocator; 256-byte aligned), bind.  The cache region is zeroed by
+ * zdc_ctx_bind / zdc_cache_reset.
+ *
+ * Supported shapes (else ZDC_ERR_UNSUPPORTED): d_model % 64 == 0; d_head <= 128;
+ * n_heads % n_kv_heads == 0; every kept rank is stored zero-padded to a multiple of 16
+ * (zero columns are exact: they add 0 to every dot product); padded ranks in
+ * {16, 32, 64, 128} for the tcgen05 attention tiles.
+ * ---------------------------------------------------------------------------------- */
+typedef struct zdc_ctx zdc_ctx;
+
+zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan,
+                          int32_t max_batch, int32_t max_seq, zdc_ctx** out);
+zdc_status zdc_ctx_sizes(const zdc_ctx* ctx, int64_t* weight_bytes, int64_t* cache_bytes,
+                         int64_t* scratch_bytes);
+zdc_status zdc_ctx_bind(zdc_ctx* ctx, void* d_weights, void* d_cache, void* d_scratch);
+void zdc_ctx_destroy(zdc_ctx* ctx);
+
+/* Load ONE layer's full-rank folded weights (from zdc_fold_weights, or any fold):
+ * truncate to the plan's important ranks ("drop the right p fraction of
+ * columns of W_Q^R"; "discard p x d_h dimensions from each W_L^{R,h} and
+ * concatenate"), zero-pad ranks to a multiple of 16, round to bf16 (RNE), and pack into
+ * the bound weight region (layout: DESIGN.md §5).  Host f64 inputs; synchronous w.r.t.
+ * the host buffers (they may be freed on return).  No compress op ever runs online. */
+zdc_status zdc_load_folded(zdc_ctx* ctx, int32_t layer, const double* wq_f, const double* wk_f,
+                           const double* wv_f, const double* wo_f, void* stream);
+/* Same, from DEVICE bf16 full-rank folded weights (same shapes); asynchronous on stream.
+ * Used by the benchmark for layers whose fp64 fold is never computed. */
+zdc_status zdc_load_folded_device(zdc_ctx* ctx, int32_t layer, const uint16_t* wq_f,
+                                  const uint16_t* wk_f, const uint16_t* wv_f,
+                                  const uint16_t* wo_f, void* stream);
+
+/* ------------------------------------------------------------------------------------
+ * (2) Prefill (prompt processing) on an EMPTY cache, layers [l0, l1) chained:
+ * y of layer l feeds x of layer l+1.  Per layer (§5.1, fig:overview P:938):
+ *   a1  [Q'|K'|V'] = x W_QKV^R           (Eq. 1 with folded, truncated weights)
+ *   a2  append K'/V' to the compressed KV cache (P:774-776 DEL, P:813 DEL)
+ *   a3  O'^h = softmax(Q'^h K'^T / sqrt(d_h)) V'  causal (Eqs. 2-3; scale: reading c2)
+ *   a4  (representative layers with g_bp < 10000) importance + top-g selection
+ *   a5  y = O' W_O^R                       (Eq. 4 with the folded W_O)
+ *   x, y: device bf16 [B][S][d]; must not alias.  B <= max_batch, S <= max_seq.
+ *   importance: optional device f32 [n_layers][B][max_seq]; row (l, b) receives the
+ *     representative layer l's token scores (log of sum_h sum_{k<=t} exp(s), reading c9).
+ * Every sequence of the batch has length S.  Rejects a non-empty cache (ZDC_ERR_STATE).
+ * ---------------------------------------------------------------------------------- */
+zdc_status zdc_prefill(zdc_ctx* ctx, int32_t l0, int32_t l1, const uint16_t* x, uint16_t* y,
+                       int32_t B, int32_t S, float* importance, void* stream);
+
+/* (3) Decode (token generation): one new token per sequence, appended at position
+ * len[l] of each layer l in [l0, l1) (each layer tracks its own length; all B sequences
+ * share it).  The new token's K'/V' are appended before it attends, so it attends to
+ * itself.  With a token split, a representative layer classifies the token as important
+ * iff its score > tau (the k-th prompt score, reading c12); a non-representative layer
+ * requires its representative to have processed this position (else ZDC_ERR_STATE).
+ *   x, y: device bf16 [B][d]; must not alias.  B must equal the prefill batch. */
+zdc_status zdc_decode(zdc_ctx* ctx, int32_t l0, int32_t l1, const uint16_t* x, uint16_t* y,
+                      int32_t B, void* stream);
+
+/* ------------------------------------------------------------------------------------
+ * (4) Sequence-parallel prefill (§5.3 motivates exchanging compressed data;
+ * the exchange here is an all-gather of compressed K'/V', reading c17).  Rank p of P
+ * holds S_total/P tokens of every sequence:
+ *   layout 0 = contiguous (rank p holds [p S/P, (p+1) S/P)),
+ *   layout 1 = zigzag (2P chunks of S/(2P); rank p holds chunks p and 2P-1-p).
+ * Per layer: a1 on local tokens -> all-gather of K'/V' over NCCL (the only data moved;
+ * bytes = (P-1)/P * B S N_kv (r_k + r_v) * 2) -> a3 for local queries against all keys at
+ * or before their global position -> a5 on local rows.  The result rows equal the
+ * zdc_prefill rows of the same tokens.  Token split under SP is not supported
+ * (ZDC_ERR_UNSUPPORTED).  zdc_comm_init takes a 128-byte ncclUniqueId.
+ *   stats (optional, host): bytes exchanged per rank and the exchange time on the device.
+ * ---------------------------------------------------------------------------------- */
+zdc_status zdc_comm_init(zdc_ctx* ctx, const void* nccl_unique_id, int32_t rank, int32_t world);
+typedef struct {
+  int64_t bytes_sent, bytes_recv, bytes_recv_uncompressed;
+  float exchange_ms, total_ms;
+} zdc_sp_stats;
+zdc_status zdc_sp_prefill(zdc_ctx* ctx, int32_t l0, int32_t l1, const uint16_t* x_local,
+                          uint16_t* y_local, int32_t B, int32_t S_total, int32_t layout,
+                          zdc_sp_stats* stats, void* stream);
+/* Host helper: the global token positions rank `rank` holds (n = S_total / world). */
+zdc_status zdc_sp_positions(int32_t S_total, int32_t world, int32_t rank, int32_t layout,
+                            int32_t* positions);
+
+/* ------------------------------------------------------------------------------------
+ * Inspection (tests): export one layer's cache as zero-filled f32 at the important
+ * widths, in position order: k [B][len][N_kv][r_qk_imp], v [B][len][N_kv][r_vl_imp],
+ * is_important u8 [B][len] (all 1 without a split), tau f32 [B] (+inf without a split).
+ * Host output buffers; synchronises `stream`.  Any pointer may be NULL to skip it.
+ * ---------------------------------------------------------------------------------- */
+zdc_status zdc_cache_export(const zdc_ctx* ctx, int32_t layer, float* k, float* v,
+                            uint8_t* is_important, float* tau, void* stream);
+zdc_status zdc_cache_length(const zdc_ctx* ctx, int32_t layer, int32_t* len);
+zdc_status zdc_cache_reset(zdc_ctx* ctx, void* stream);
+
+/* Device LSE of the last prefill/decode call of a layer: f32 [B][N_h][T] (T = S for a
+ * prefill, 1 for a decode step), log of the Eq. 3 denominator of each query row. */
+zdc_status zdc_last_lse(const zdc_ctx* ctx, int32_t layer, float* lse_host, void* stream);
+
+/* ------------------------------------------------------------------------------------
+ * Kernel-level entry (tests and roofline measurements): the tcgen05 projection GEMM of
+ * a1/a5, D[M][N] = A[M][K] * B[N][K]^T, bf16 in, f32 accumulate, bf16 out (RNE).
+ * a, b, d: device; K % 64 == 0; rows 16-byte aligned. */
+zdc_status zdc_gemm_bf16(const uint16_t* a, const uint16_t* b, uint16_t* d,
+                         int32_t M, int32_t N, int32_t K, void* stream);
+
+/* Number of kernels the last prefill / decode call enqueued (for bench.py's gpu_launches). */
+int64_t zdc_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZDC_H */

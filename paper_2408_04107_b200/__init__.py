@@ -1,0 +1,257 @@
+"""Python binding of libzdc.so (include/zdc.h) — argument marshalling only.
+
+Every step of the ZDC hot path runs in the library's sm_100a kernels; this module only
+converts arguments (torch device tensors / numpy host arrays -> pointers) and raises
+ZdcError on a non-zero status.  There is no CPU fallback: importing works without a GPU,
+but any call that needs the device fails loudly if libzdc.so or the GPU is missing.
+PyTorch is used for device memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+__all__ = ["ZdcError", "lib", "lib_path", "Dims", "Plan", "Context", "fold_weights", "gemm_bf16",
+           "sp_positions", "EXPORTED_SYMBOLS", "last_launch_count"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libzdc.so")
+_lib = None
+
+ZDC_STATUS = {0: "ZDC_OK", -1: "ZDC_ERR_INVALID_ARG", -2: "ZDC_ERR_SHAPE", -3: "ZDC_ERR_NOT_ORTHONORMAL",
+              -4: "ZDC_ERR_NO_CONVERGENCE", -5: "ZDC_ERR_CAPACITY", -6: "ZDC_ERR_CUDA", -7: "ZDC_ERR_NCCL",
+              -8: "ZDC_ERR_UNSUPPORTED", -9: "ZDC_ERR_STATE"}
+
+EXPORTED_SYMBOLS = ["zdc_last_error", "zdc_version", "zdc_fold_weights", "zdc_ctx_create", "zdc_ctx_sizes",
+                    "zdc_ctx_bind", "zdc_ctx_destroy", "zdc_load_folded", "zdc_load_folded_device",
+                    "zdc_prefill", "zdc_decode", "zdc_comm_init", "zdc_sp_prefill", "zdc_sp_positions",
+                    "zdc_cache_export", "zdc_cache_length", "zdc_cache_reset", "zdc_last_lse",
+                    "zdc_gemm_bf16", "zdc_kernel_launch_count"]
+
+
+class ZdcError(RuntimeError):
+    def __init__(self, status: int, fn: str, msg: str):
+        self.status = status
+        super().__init__("%s -> %s: %s" % (fn, ZDC_STATUS.get(status, status), msg))
+
+
+class Dims(ctypes.Structure):
+    _fields_ = [("n_layers", ctypes.c_int32), ("d_model", ctypes.c_int32), ("n_heads", ctypes.c_int32),
+                ("n_kv_heads", ctypes.c_int32), ("d_head", ctypes.c_int32)]
+
+
+class Plan(ctypes.Structure):
+    _fields_ = [("r_qk_imp", ctypes.POINTER(ctypes.c_int32)), ("r_qk_unimp", ctypes.POINTER(ctypes.c_int32)),
+                ("r_vl_imp", ctypes.POINTER(ctypes.c_int32)), ("r_vl_unimp", ctypes.POINTER(ctypes.c_int32)),
+                ("g_bp", ctypes.POINTER(ctypes.c_int32)), ("group_rep", ctypes.POINTER(ctypes.c_int32)),
+                ("importance_mode", ctypes.c_int32)]
+
+
+class SpStats(ctypes.Structure):
+    _fields_ = [("bytes_sent", ctypes.c_int64), ("bytes_recv", ctypes.c_int64),
+                ("bytes_recv_uncompressed", ctypes.c_int64), ("exchange_ms", ctypes.c_float),
+                ("total_ms", ctypes.c_float)]
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def lib():
+    """Load libzdc.so (built in-tree by paper_2408_04107_b200.build).  Raises if missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError("libzdc.so not built: run `python -m paper_2408_04107_b200.build` "
+                              "(no CPU fallback exists)")
+        L = ctypes.CDLL(_LIB_PATH)
+        P, I32, I64, F = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float
+        dp = ctypes.POINTER(ctypes.c_double)
+        sig = {
+            "zdc_last_error": ([], ctypes.c_char_p), "zdc_version": ([], ctypes.c_char_p),
+            "zdc_fold_weights": ([ctypes.POINTER(Dims), dp, dp, dp, dp, dp, I64, dp, dp, dp, dp, dp, dp, dp, dp], I32),
+            "zdc_ctx_create": ([ctypes.POINTER(Dims), ctypes.POINTER(Plan), I32, I32, ctypes.POINTER(P)], I32),
+            "zdc_ctx_sizes": ([P, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)], I32),
+            "zdc_ctx_bind": ([P, P, P, P], I32), "zdc_ctx_destroy": ([P], None),
+            "zdc_load_folded": ([P, I32, dp, dp, dp, dp, P], I32),
+            "zdc_load_folded_device": ([P, I32, P, P, P, P, P], I32),
+            "zdc_prefill": ([P, I32, I32, P, P, I32, I32, P, P], I32),
+            "zdc_decode": ([P, I32, I32, P, P, I32, P], I32),
+            "zdc_comm_init": ([P, P, I32, I32], I32),
+            "zdc_sp_prefill": ([P, I32, I32, P, P, I32, I32, I32, ctypes.POINTER(SpStats), P], I32),
+            "zdc_sp_positions": ([I32, I32, I32, I32, ctypes.POINTER(I32)], I32),
+            "zdc_cache_export": ([P, I32, P, P, P, P, P], I32),
+            "zdc_cache_length": ([P, I32, ctypes.POINTER(I32)], I32),
+            "zdc_cache_reset": ([P, P], I32),
+            "zdc_last_lse": ([P, I32, P, P], I32),
+            "zdc_gemm_bf16": ([P, P, P, I32, I32, I32, P], I32),
+            "zdc_kernel_launch_count": ([], I64),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _ = F
+        _lib = L
+    return _lib
+
+
+def _check(status: int, fn: str):
+    if status != 0:
+        raise ZdcError(status, fn, lib().zdc_last_error().decode())
+
+
+def last_launch_count() -> int:
+    return int(lib().zdc_kernel_launch_count())
+
+
+def _dptr(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _i32arr(v: Sequence[int]):
+    arr = (ctypes.c_int32 * len(v))(*[int(x) for x in v])
+    return arr
+
+
+def _stream(stream=None) -> int:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream)
+
+
+def _tptr(t, dtype_name: str):
+    """Device pointer of a contiguous torch tensor of the expected dtype."""
+    import torch
+    want = {"bf16": torch.bfloat16, "f32": torch.float32, "u16": torch.int16}[dtype_name]
+    if t.dtype != want and not (dtype_name == "bf16" and t.dtype == torch.int16):
+        raise TypeError("expected %s tensor, got %s" % (dtype_name, t.dtype))
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValueError("expected a contiguous CUDA tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def make_dims(d) -> Dims:
+    return Dims(d.n_layers, d.d_model, d.n_heads, d.n_kv_heads, d.d_head)
+
+
+def fold_weights(dims, wq, wk, wv, wo, xc):
+    """zdc_fold_weights (host fp64, one layer).  Returns dict like the oracle's fold."""
+    nkv, dh = dims.n_kv_heads, dims.d_head
+    c = lambda a: np.ascontiguousarray(a, dtype=np.float64)  # noqa: E731
+    wq, wk, wv, wo, xc = c(wq), c(wk), c(wv), c(wo), c(xc)
+    out = dict(r_qk=np.zeros((nkv, dh, dh)), r_vl=np.zeros((nkv, dh, dh)), sigma_qk=np.zeros((nkv, dh)),
+               sigma_vl=np.zeros((nkv, dh)), wq_f=np.zeros_like(wq), wk_f=np.zeros_like(wk),
+               wv_f=np.zeros_like(wv), wo_f=np.zeros_like(wo))
+    D = make_dims(dims)
+    st = lib().zdc_fold_weights(ctypes.byref(D), _dptr(wq), _dptr(wk), _dptr(wv), _dptr(wo), _dptr(xc),
+                                xc.shape[0], _dptr(out["r_qk"]), _dptr(out["r_vl"]), _dptr(out["sigma_qk"]),
+                                _dptr(out["sigma_vl"]), _dptr(out["wq_f"]), _dptr(out["wk_f"]),
+                                _dptr(out["wv_f"]), _dptr(out["wo_f"]))
+    _check(st, "zdc_fold_weights")
+    return out
+
+
+def sp_positions(S_total: int, world: int, rank: int, layout: int) -> np.ndarray:
+    n = S_total // world
+    buf = (ctypes.c_int32 * max(n, 1))()
+    _check(lib().zdc_sp_positions(S_total, world, rank, layout, buf), "zdc_sp_positions")
+    return np.array(buf[:n], dtype=np.int64)
+
+
+def gemm_bf16(a, b, d, stream=None):
+    """D[M][N] = A[M][K] B[N][K]^T through zdc_gemm_bf16 (tcgen05)."""
+    M, K = a.shape
+    N = b.shape[0]
+    _check(lib().zdc_gemm_bf16(_tptr(a, "bf16"), _tptr(b, "bf16"), _tptr(d, "bf16"), M, N, K, _stream(stream)),
+           "zdc_gemm_bf16")
+
+
+class Context:
+    """zdc_ctx plus its three caller-owned device regions (allocated with torch)."""
+
+    def __init__(self, dims, plan, max_batch: int, max_seq: int, device="cuda"):
+        import torch
+        self.dims, self.plan = dims, plan
+        self._keep = [_i32arr(plan.r_qk_imp), _i32arr(plan.r_qk_unimp), _i32arr(plan.r_vl_imp),
+                      _i32arr(plan.r_vl_unimp), _i32arr(plan.g_bp), _i32arr(plan.group_rep)]
+        P = Plan(*[ctypes.cast(a, ctypes.POINTER(ctypes.c_int32)) for a in self._keep], int(plan.importance_mode))
+        D = make_dims(dims)
+        h = ctypes.c_void_p()
+        _check(lib().zdc_ctx_create(ctypes.byref(D), ctypes.byref(P), max_batch, max_seq, ctypes.byref(h)),
+               "zdc_ctx_create")
+        self.h = h
+        wb, cb, sb = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().zdc_ctx_sizes(h, ctypes.byref(wb), ctypes.byref(cb), ctypes.byref(sb)), "zdc_ctx_sizes")
+        self.sizes = (wb.value, cb.value, sb.value)
+        self.weights = torch.empty(max(wb.value, 256), dtype=torch.uint8, device=device)
+        self.cache = torch.empty(max(cb.value, 256), dtype=torch.uint8, device=device)
+        self.scratch = torch.empty(max(sb.value, 256), dtype=torch.uint8, device=device)
+        _check(lib().zdc_ctx_bind(h, ctypes.c_void_p(self.weights.data_ptr()), ctypes.c_void_p(self.cache.data_ptr()),
+                                  ctypes.c_void_p(self.scratch.data_ptr())), "zdc_ctx_bind")
+        self.max_batch, self.max_seq = max_batch, max_seq
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().zdc_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def load_folded(self, layer: int, wq_f, wk_f, wv_f, wo_f, stream=None):
+        c = lambda a: np.ascontiguousarray(a, dtype=np.float64)  # noqa: E731
+        arrs = [c(wq_f), c(wk_f), c(wv_f), c(wo_f)]
+        _check(lib().zdc_load_folded(self.h, layer, *[_dptr(a) for a in arrs], ctypes.c_void_p(_stream(stream))),
+               "zdc_load_folded")
+
+    def load_folded_device(self, layer: int, wq_f, wk_f, wv_f, wo_f, stream=None):
+        _check(lib().zdc_load_folded_device(self.h, layer, *[_tptr(t, "bf16") for t in (wq_f, wk_f, wv_f, wo_f)],
+                                            ctypes.c_void_p(_stream(stream))), "zdc_load_folded_device")
+
+    def prefill(self, x, y, l0: int = 0, l1: Optional[int] = None, importance=None, stream=None):
+        l1 = self.dims.n_layers if l1 is None else l1
+        B, S, _ = x.shape
+        imp = _tptr(importance, "f32") if importance is not None else None
+        _check(lib().zdc_prefill(self.h, l0, l1, _tptr(x, "bf16"), _tptr(y, "bf16"), B, S, imp,
+                                 ctypes.c_void_p(_stream(stream))), "zdc_prefill")
+
+    def decode(self, x, y, l0: int = 0, l1: Optional[int] = None, stream=None):
+        l1 = self.dims.n_layers if l1 is None else l1
+        _check(lib().zdc_decode(self.h, l0, l1, _tptr(x, "bf16"), _tptr(y, "bf16"), x.shape[0],
+                                ctypes.c_void_p(_stream(stream))), "zdc_decode")
+
+    def cache_length(self, layer: int) -> int:
+        n = ctypes.c_int32()
+        _check(lib().zdc_cache_length(self.h, layer, ctypes.byref(n)), "zdc_cache_length")
+        return n.value
+
+    def cache_export(self, layer: int, B: int, stream=None):
+        length = self.cache_length(layer)
+        nkv = self.dims.n_kv_heads
+        rk, rv = self.plan.r_qk_imp[layer], self.plan.r_vl_imp[layer]
+        k = np.zeros((B, length, nkv, rk), dtype=np.float32)
+        v = np.zeros((B, length, nkv, rv), dtype=np.float32)
+        imp = np.zeros((B, length), dtype=np.uint8)
+        tau = np.zeros(B, dtype=np.float32)
+        ptr = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+        _check(lib().zdc_cache_export(self.h, layer, ptr(k), ptr(v), ptr(imp), ptr(tau),
+                                      ctypes.c_void_p(_stream(stream))), "zdc_cache_export")
+        return k, v, imp.astype(bool), tau
+
+    def last_lse(self, layer: int, B: int, T: int, stream=None) -> np.ndarray:
+        out = np.zeros((B, self.dims.n_heads, T), dtype=np.float32)
+        _check(lib().zdc_last_lse(self.h, layer, ctypes.c_void_p(out.ctypes.data), ctypes.c_void_p(_stream(stream))),
+               "zdc_last_lse")
+        return out
+
+    def reset(self, stream=None):
+        _check(lib().zdc_cache_reset(self.h, ctypes.c_void_p(_stream(stream))), "zdc_cache_reset")

@@ -1,0 +1,527 @@
+// api.cpp — the C ABI of include/zdc.h: context, weight loading, and the per-layer
+// orchestration of the hot path (a1 projection -> a2 append -> a3 attention -> a4 selection
+// -> a5 output projection).  Host code only; every step of the path runs in the kernels of
+// gemm.cu / attn_prefill.cu / decode.cu / select.cu.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "api_util.h"
+#include "ctx.h"
+#include "kernels.h"
+#include "zdc.h"
+
+namespace zdc {
+
+static thread_local std::string t_err;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  t_err = buf;
+}
+
+zdc_status fail(zdc_status s, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  t_err = buf;
+  return s;
+}
+
+static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+static inline int pad16(int r) { return (r + 15) / 16 * 16; }
+
+// bf16 round-to-nearest-even of an f64 through f32 (the same two steps the GPU epilogues take
+// from their f32 accumulators).
+static inline uint16_t f64_to_bf16(double v) {
+  float f = static_cast<float>(v);
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7F800000u) == 0x7F800000u) return static_cast<uint16_t>(u >> 16);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+
+static zdc_status check_sticky() {
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(ZDC_ERR_CUDA, "asynchronous CUDA error from an earlier call: %s", cudaGetErrorString(e));
+  }
+  return ZDC_OK;
+}
+
+}  // namespace zdc
+
+using namespace zdc;
+
+extern "C" {
+
+const char* zdc_last_error(void) { return t_err.c_str(); }
+const char* zdc_version(void) { return "zdc-b200 0.1 (sm_100a tcgen05)"; }
+int64_t zdc_kernel_launch_count(void) { return g_launches; }
+
+// ------------------------------------------------------------------ context
+zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t max_batch, int32_t max_seq,
+                          zdc_ctx** out) {
+  if (!dims || !plan || !out) return fail(ZDC_ERR_INVALID_ARG, "zdc_ctx_create: null argument");
+  *out = nullptr;
+  const zdc_dims& d = *dims;
+  if (d.n_layers <= 0 || d.d_model <= 0 || d.n_heads <= 0 || d.n_kv_heads <= 0 || d.d_head <= 0)
+    return fail(ZDC_ERR_SHAPE, "zdc_ctx_create: non-positive dims (L=%d d=%d Nh=%d Nkv=%d dh=%d)", d.n_layers,
+                d.d_model, d.n_heads, d.n_kv_heads, d.d_head);
+  if (d.n_heads % d.n_kv_heads != 0)
+    return fail(ZDC_ERR_SHAPE, "zdc_ctx_create: n_heads %d not a multiple of n_kv_heads %d", d.n_heads,
+                d.n_kv_heads);
+  if (d.d_model % 64 != 0) return fail(ZDC_ERR_UNSUPPORTED, "zdc_ctx_create: d_model %d %% 64 != 0", d.d_model);
+  if (d.d_head > 128) return fail(ZDC_ERR_UNSUPPORTED, "zdc_ctx_create: d_head %d > 128", d.d_head);
+  const int G = d.n_heads / d.n_kv_heads;
+  if (G != 1 && G != 2 && G != 4 && G != 8)
+    return fail(ZDC_ERR_UNSUPPORTED, "zdc_ctx_create: group size %d not in {1,2,4,8}", G);
+  if (max_batch <= 0 || max_seq <= 0)
+    return fail(ZDC_ERR_SHAPE, "zdc_ctx_create: max_batch %d / max_seq %d", max_batch, max_seq);
+  if (!plan->r_qk_imp || !plan->r_qk_unimp || !plan->r_vl_imp || !plan->r_vl_unimp || !plan->g_bp ||
+      !plan->group_rep)
+    return fail(ZDC_ERR_INVALID_ARG, "zdc_ctx_create: null plan array");
+  if (plan->importance_mode != 0 && plan->importance_mode != 1)
+    return fail(ZDC_ERR_INVALID_ARG, "zdc_ctx_create: importance_mode %d", plan->importance_mode);
+
+  zdc_ctx* c = new zdc_ctx();
+  c->dims = d;
+  c->G = G;
+  c->max_batch = max_batch;
+  c->max_seq = max_seq;
+  c->importance_mode = plan->importance_mode;
+  c->layers.resize(d.n_layers);
+  c->len.assign(d.n_layers, 0);
+  int64_t woff = 0, coff = 0;
+  int max_nq = 0, max_ko = 0, max_rv = 0;
+  bool any_split = false;
+  for (int l = 0; l < d.n_layers; ++l) {
+    LayerInfo& L = c->layers[l];
+    L.rk = plan->r_qk_imp[l];
+    L.rku = plan->r_qk_unimp[l];
+    L.rv = plan->r_vl_imp[l];
+    L.rvu = plan->r_vl_unimp[l];
+    L.g_bp = plan->g_bp[l];
+    L.rep = plan->group_rep[l];
+    if (L.rku < 1 || L.rku > L.rk || L.rk > d.d_head || L.rvu < 1 || L.rvu > L.rv || L.rv > d.d_head) {
+      delete c;
+      return fail(ZDC_ERR_SHAPE, "layer %d: ranks must satisfy 1 <= r_unimp <= r_imp <= d_head (qk %d/%d vl %d/%d)",
+                  l, L.rk, L.rku, L.rv, L.rvu);
+    }
+    if (L.g_bp < 0 || L.g_bp > 10000 || L.rep < 0 || L.rep > l || plan->group_rep[L.rep] != L.rep) {
+      delete c;
+      return fail(ZDC_ERR_INVALID_ARG, "layer %d: g_bp %d / group_rep %d invalid", l, L.g_bp, L.rep);
+    }
+    L.split = L.g_bp < 10000;
+    if (L.split) {
+      const int r = L.rep;
+      if (plan->g_bp[r] != L.g_bp || plan->r_qk_imp[r] != L.rk || plan->r_qk_unimp[r] != L.rku ||
+          plan->r_vl_imp[r] != L.rv || plan->r_vl_unimp[r] != L.rvu) {
+        delete c;
+        return fail(ZDC_ERR_INVALID_ARG, "layer %d: g and ranks must equal those of its representative %d", l, r);
+      }
+      any_split = true;
+    }
+    L.rk_p = pad16(L.rk);
+    L.rv_p = pad16(L.rv);
+    L.rku_p = pad16(L.rku);
+    L.rvu_p = pad16(L.rvu);
+    auto ok_w = [](int r) { return r == 16 || r == 32 || r == 64 || r == 128; };
+    if (!ok_w(L.rk_p) || L.rk_p != L.rv_p) {
+      delete c;
+      return fail(ZDC_ERR_UNSUPPORTED, "layer %d: padded ranks r_k=%d r_v=%d must be equal and in {16,32,64,128}", l,
+                  L.rk_p, L.rv_p);
+    }
+    L.nq = d.n_heads * L.rk_p;
+    L.nk = d.n_kv_heads * L.rk_p;
+    L.nv = d.n_kv_heads * L.rv_p;
+    L.n_qkv = L.nq + L.nk + L.nv;
+    L.ko_p = static_cast<int>(align_up(static_cast<int64_t>(d.n_heads) * L.rv_p, 64));
+    L.w_qkv = woff;
+    woff = align_up(woff + static_cast<int64_t>(L.n_qkv) * d.d_model * 2, 256);
+    L.w_o = woff;
+    woff = align_up(woff + static_cast<int64_t>(d.d_model) * L.ko_p * 2, 256);
+    const int64_t kv_rows = static_cast<int64_t>(max_batch) * d.n_kv_heads * max_seq;
+    L.k_off = coff;
+    coff = align_up(coff + kv_rows * L.rk_p * 2, 256);
+    L.v_off = coff;
+    coff = align_up(coff + kv_rows * L.rv_p * 2, 256);
+    if (L.split && L.rep == l) {
+      L.cls_off = coff;
+      coff = align_up(coff + static_cast<int64_t>(max_batch) * max_seq, 256);
+      L.tau_off = coff;
+      coff = align_up(coff + static_cast<int64_t>(max_batch) * 4, 256);
+      L.score_off = coff;
+      coff = align_up(coff + static_cast<int64_t>(max_batch) * max_seq * 4, 256);
+    }
+    if (L.nq > max_nq) max_nq = L.nq;
+    if (L.ko_p > max_ko) max_ko = L.ko_p;
+    if (L.rv_p > max_rv) max_rv = L.rv_p;
+  }
+  if (any_split) {
+    delete c;
+    return fail(ZDC_ERR_UNSUPPORTED, "token-level split (g_bp < 10000) is not implemented in this build");
+  }
+  c->weight_bytes = woff;
+  c->cache_bytes = coff;
+  const int64_t rows = static_cast<int64_t>(max_batch) * max_seq;
+  int64_t s = 0;
+  c->s_q = s;
+  s = align_up(s + rows * max_nq * 2, 256);
+  c->s_o = s;
+  s = align_up(s + rows * max_ko * 2, 256);
+  c->s_lse = s;
+  s = align_up(s + rows * d.n_heads * 4, 256);
+  c->s_part = s;
+  s = align_up(s + static_cast<int64_t>(max_batch) * d.n_heads * 64 * (max_rv + 2) * 4, 256);
+  c->ldq = max_nq;
+  c->ldo = max_ko;
+  c->scratch_bytes = s;
+  *out = c;
+  return ZDC_OK;
+}
+
+zdc_status zdc_ctx_sizes(const zdc_ctx* c, int64_t* wb, int64_t* cb, int64_t* sb) {
+  if (!c) return fail(ZDC_ERR_INVALID_ARG, "zdc_ctx_sizes: null ctx");
+  if (wb) *wb = c->weight_bytes;
+  if (cb) *cb = c->cache_bytes;
+  if (sb) *sb = c->scratch_bytes;
+  return ZDC_OK;
+}
+
+zdc_status zdc_ctx_bind(zdc_ctx* c, void* w, void* cache, void* scratch) {
+  if (!c || !w || !cache || !scratch) return fail(ZDC_ERR_INVALID_ARG, "zdc_ctx_bind: null argument");
+  if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(cache) | reinterpret_cast<uintptr_t>(scratch)) &
+      255)
+    return fail(ZDC_ERR_INVALID_ARG, "zdc_ctx_bind: buffers must be 256-byte aligned");
+  c->w = static_cast<uint8_t*>(w);
+  c->cache = static_cast<uint8_t*>(cache);
+  c->scratch = static_cast<uint8_t*>(scratch);
+  ZDC_CUDA_TRY(cudaMemset(c->cache, 0, c->cache_bytes));
+  ZDC_CUDA_TRY(cudaMemset(c->scratch, 0, c->scratch_bytes));
+  ZDC_CUDA_TRY(cudaMemset(c->w, 0, c->weight_bytes));
+  c->len.assign(c->dims.n_layers, 0);
+  c->batch = 0;
+  return ZDC_OK;
+}
+
+void zdc_ctx_destroy(zdc_ctx* c) {
+  if (!c) return;
+  comm_destroy(c);
+  delete c;
+}
+
+// ------------------------------------------------------------------ weights
+zdc_status zdc_load_folded(zdc_ctx* c, int32_t layer, const double* wq, const double* wk, const double* wv,
+                           const double* wo, void* stream) {
+  if (!c || !wq || !wk || !wv || !wo) return fail(ZDC_ERR_INVALID_ARG, "zdc_load_folded: null argument");
+  if (!c->w) return fail(ZDC_ERR_STATE, "zdc_load_folded: ctx not bound");
+  if (layer < 0 || layer >= c->dims.n_layers) return fail(ZDC_ERR_SHAPE, "zdc_load_folded: layer %d", layer);
+  const LayerInfo& L = c->layers[layer];
+  const int d = c->dims.d_model, Nh = c->dims.n_heads, Nkv = c->dims.n_kv_heads, dh = c->dims.d_head;
+  std::vector<uint16_t> qkv(static_cast<size_t>(L.n_qkv) * d, 0), o(static_cast<size_t>(d) * L.ko_p, 0);
+  auto finite = [](double v) { return std::isfinite(v); };
+  for (int n = 0; n < L.n_qkv; ++n) {
+    const double* src;
+    int64_t ld, col;
+    int c_in;
+    if (n < L.nq) {
+      c_in = n % L.rk_p;
+      if (c_in >= L.rk) continue;
+      src = wq, ld = static_cast<int64_t>(Nh) * dh, col = (n / L.rk_p) * dh + c_in;
+    } else if (n < L.nq + L.nk) {
+      c_in = (n - L.nq) % L.rk_p;
+      if (c_in >= L.rk) continue;
+      src = wk, ld = static_cast<int64_t>(Nkv) * dh, col = ((n - L.nq) / L.rk_p) * dh + c_in;
+    } else {
+      c_in = (n - L.nq - L.nk) % L.rv_p;
+      if (c_in >= L.rv) continue;
+      src = wv, ld = static_cast<int64_t>(Nkv) * dh, col = ((n - L.nq - L.nk) / L.rv_p) * dh + c_in;
+    }
+    for (int k = 0; k < d; ++k) {
+      const double v = src[k * ld + col];
+      if (!finite(v)) return fail(ZDC_ERR_INVALID_ARG, "zdc_load_folded: non-finite weight");
+      qkv[static_cast<size_t>(n) * d + k] = f64_to_bf16(v);
+    }
+  }
+  for (int h = 0; h < Nh; ++h)
+    for (int cc = 0; cc < L.rv; ++cc) {
+      const double* row = wo + static_cast<int64_t>(h * dh + cc) * d;
+      for (int j = 0; j < d; ++j) {
+        if (!finite(row[j])) return fail(ZDC_ERR_INVALID_ARG, "zdc_load_folded: non-finite weight");
+        o[static_cast<size_t>(j) * L.ko_p + h * L.rv_p + cc] = f64_to_bf16(row[j]);
+      }
+    }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ZDC_CUDA_TRY(cudaMemcpyAsync(c->w + L.w_qkv, qkv.data(), qkv.size() * 2, cudaMemcpyHostToDevice, st));
+  ZDC_CUDA_TRY(cudaMemcpyAsync(c->w + L.w_o, o.data(), o.size() * 2, cudaMemcpyHostToDevice, st));
+  ZDC_CUDA_TRY(cudaStreamSynchronize(st));
+  return ZDC_OK;
+}
+
+zdc_status zdc_load_folded_device(zdc_ctx* c, int32_t layer, const uint16_t* wq, const uint16_t* wk,
+                                  const uint16_t* wv, const uint16_t* wo, void* stream) {
+  if (!c || !wq || !wk || !wv || !wo) return fail(ZDC_ERR_INVALID_ARG, "zdc_load_folded_device: null argument");
+  if (!c->w) return fail(ZDC_ERR_STATE, "zdc_load_folded_device: ctx not bound");
+  if (layer < 0 || layer >= c->dims.n_layers) return fail(ZDC_ERR_SHAPE, "zdc_load_folded_device: layer %d", layer);
+  const LayerInfo& L = c->layers[layer];
+  ZDC_CUDA_TRY(launch_pack_weights_bf16(wq, wk, wv, wo, reinterpret_cast<uint16_t*>(c->w + L.w_qkv),
+                                        reinterpret_cast<uint16_t*>(c->w + L.w_o), c->dims.d_model, c->dims.n_heads,
+                                        c->dims.n_kv_heads, c->dims.d_head, L.rk, L.rv, L.rk_p, L.rv_p, L.ko_p,
+                                        static_cast<cudaStream_t>(stream)));
+  return ZDC_OK;
+}
+
+// ------------------------------------------------------------------ hot path
+static zdc_status check_run(zdc_ctx* c, int l0, int l1, const void* x, const void* y, const char* who) {
+  if (!c) return fail(ZDC_ERR_INVALID_ARG, "%s: null ctx", who);
+  if (!c->w) return fail(ZDC_ERR_STATE, "%s: ctx not bound", who);
+  if (!x || !y) return fail(ZDC_ERR_INVALID_ARG, "%s: null x / y", who);
+  if (x == y) return fail(ZDC_ERR_INVALID_ARG, "%s: x and y alias", who);
+  if (l0 < 0 || l1 > c->dims.n_layers || l0 >= l1)
+    return fail(ZDC_ERR_SHAPE, "%s: layer range [%d, %d) outside [0, %d)", who, l0, l1, c->dims.n_layers);
+  return check_sticky();
+}
+
+static QkvDest qkv_dest(zdc_ctx* c, const LayerInfo& L, int S, int pos0, const int* posmap) {
+  QkvDest q;
+  q.q = reinterpret_cast<uint16_t*>(c->scratch + c->s_q);
+  q.ldq = L.nq;
+  q.nq = L.nq;
+  q.nk = L.nk;
+  q.k = reinterpret_cast<uint16_t*>(c->cache + L.k_off);
+  q.v = reinterpret_cast<uint16_t*>(c->cache + L.v_off);
+  q.rk = L.rk_p;
+  q.rv = L.rv_p;
+  q.S = S;
+  q.kg = static_cast<int64_t>(c->max_seq) * L.rk_p;
+  q.kb = q.kg * c->dims.n_kv_heads;
+  q.vg = static_cast<int64_t>(c->max_seq) * L.rv_p;
+  q.vb = q.vg * c->dims.n_kv_heads;
+  q.pos0 = pos0;
+  q.posmap = posmap;
+  return q;
+}
+
+zdc_status zdc_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, uint16_t* y, int32_t B, int32_t S,
+                       float* importance, void* stream) {
+  zdc_status st = check_run(c, l0, l1, x, y, "zdc_prefill");
+  if (st != ZDC_OK) return st;
+  if (B <= 0 || S <= 0) return fail(ZDC_ERR_SHAPE, "zdc_prefill: B=%d S=%d", B, S);
+  if (B > c->max_batch || S > c->max_seq)
+    return fail(ZDC_ERR_CAPACITY, "zdc_prefill: B=%d S=%d exceeds max_batch=%d max_seq=%d", B, S, c->max_batch,
+                c->max_seq);
+  for (int l = l0; l < l1; ++l)
+    if (c->len[l] != 0) return fail(ZDC_ERR_STATE, "zdc_prefill: layer %d cache is not empty (len %d)", l, c->len[l]);
+  if (c->batch != 0 && c->batch != B) {
+    bool all_empty = true;
+    for (int l = 0; l < c->dims.n_layers; ++l) all_empty &= c->len[l] == 0;
+    if (!all_empty) return fail(ZDC_ERR_SHAPE, "zdc_prefill: batch %d differs from the cache batch %d", B, c->batch);
+  }
+  (void)importance;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  g_launches = 0;
+  const int d = c->dims.d_model, Nh = c->dims.n_heads, Nkv = c->dims.n_kv_heads;
+  const int M = B * S;
+  for (int l = l0; l < l1; ++l) {
+    const LayerInfo& L = c->layers[l];
+    const uint16_t* xin = l == l0 ? x : y;
+    // a1 + a2: [Q'|K'|V'] = x W_QKV^R; K'/V' written into the cache at positions [0, S)
+    Epilogue e1;
+    e1.mode = 1;
+    e1.qkv = qkv_dest(c, L, S, 0, nullptr);
+    ZDC_CUDA_TRY(launch_gemm(xin, d, reinterpret_cast<const uint16_t*>(c->w + L.w_qkv), d, M, L.n_qkv, d, e1, s));
+    // a3: causal attention at head dim r, O' and LSE
+    PrefillAttnArgs a;
+    a.q = reinterpret_cast<const uint16_t*>(c->scratch + c->s_q);
+    a.ldq = L.nq;
+    a.k = reinterpret_cast<const uint16_t*>(c->cache + L.k_off);
+    a.v = reinterpret_cast<const uint16_t*>(c->cache + L.v_off);
+    a.S_cap = c->max_seq;
+    a.o = reinterpret_cast<uint16_t*>(c->scratch + c->s_o);
+    a.ldo = L.ko_p;
+    a.lse = reinterpret_cast<float*>(c->scratch + c->s_lse);
+    a.B = B;
+    a.S = S;
+    a.Nh = Nh;
+    a.Nkv = Nkv;
+    a.rk = L.rk_p;
+    a.rv = L.rv_p;
+    a.scale = 1.0f / std::sqrt(static_cast<float>(c->dims.d_head));
+    a.q_pos0 = 0;
+    a.q_row0 = 0;
+    a.n_q = S;
+    ZDC_CUDA_TRY(launch_prefill_attention(a, s));
+    // a5: y = O' W_O^R
+    Epilogue e5;
+    e5.mode = 0;
+    e5.d = y;
+    e5.ldd = d;
+    ZDC_CUDA_TRY(launch_gemm(a.o, L.ko_p, reinterpret_cast<const uint16_t*>(c->w + L.w_o), L.ko_p, M, d, L.ko_p, e5,
+                             s));
+    c->len[l] = S;
+    c->last_layer = l;
+    c->last_T = S;
+  }
+  c->batch = B;
+  return ZDC_OK;
+}
+
+zdc_status zdc_decode(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, uint16_t* y, int32_t B, void* stream) {
+  zdc_status st = check_run(c, l0, l1, x, y, "zdc_decode");
+  if (st != ZDC_OK) return st;
+  if (B <= 0 || B > c->max_batch) return fail(ZDC_ERR_CAPACITY, "zdc_decode: B=%d (max_batch %d)", B, c->max_batch);
+  if (c->batch != 0 && B != c->batch) return fail(ZDC_ERR_SHAPE, "zdc_decode: B=%d but cache batch is %d", B, c->batch);
+  for (int l = l0; l < l1; ++l)
+    if (c->len[l] + 1 > c->max_seq)
+      return fail(ZDC_ERR_CAPACITY, "zdc_decode: layer %d len %d + 1 > max_seq %d", l, c->len[l], c->max_seq);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  g_launches = 0;
+  const int d = c->dims.d_model, Nh = c->dims.n_heads, Nkv = c->dims.n_kv_heads;
+  for (int l = l0; l < l1; ++l) {
+    const LayerInfo& L = c->layers[l];
+    const uint16_t* xin = l == l0 ? x : y;
+    const int pos = c->len[l];
+    Epilogue e1;
+    e1.mode = 1;
+    e1.qkv = qkv_dest(c, L, 1, pos, nullptr);
+    const uint16_t* wqkv = reinterpret_cast<const uint16_t*>(c->w + L.w_qkv);
+    const uint16_t* wo = reinterpret_cast<const uint16_t*>(c->w + L.w_o);
+    if (B <= 8)
+      ZDC_CUDA_TRY(launch_gemv(wqkv, xin, d, B, L.n_qkv, d, e1, s));
+    else
+      ZDC_CUDA_TRY(launch_gemm(xin, d, wqkv, d, B, L.n_qkv, d, e1, s));
+    DecodeAttnArgs a;
+    a.q = reinterpret_cast<const uint16_t*>(c->scratch + c->s_q);
+    a.ldq = L.nq;
+    a.k = reinterpret_cast<const uint16_t*>(c->cache + L.k_off);
+    a.v = reinterpret_cast<const uint16_t*>(c->cache + L.v_off);
+    a.S_cap = c->max_seq;
+    a.len = pos + 1;
+    a.o = reinterpret_cast<uint16_t*>(c->scratch + c->s_o);
+    a.ldo = L.ko_p;
+    a.lse = reinterpret_cast<float*>(c->scratch + c->s_lse);
+    a.part = reinterpret_cast<float*>(c->scratch + c->s_part);
+    a.B = B;
+    a.Nh = Nh;
+    a.Nkv = Nkv;
+    a.rk = L.rk_p;
+    a.rv = L.rv_p;
+    a.scale = 1.0f / std::sqrt(static_cast<float>(c->dims.d_head));
+    a.splits = decode_splits(B, Nkv, a.len);
+    ZDC_CUDA_TRY(launch_decode_attention(a, s));
+    Epilogue e5;
+    e5.mode = 0;
+    e5.d = y;
+    e5.ldd = d;
+    if (B <= 8)
+      ZDC_CUDA_TRY(launch_gemv(wo, a.o, L.ko_p, B, d, L.ko_p, e5, s));
+    else
+      ZDC_CUDA_TRY(launch_gemm(a.o, L.ko_p, wo, L.ko_p, B, d, L.ko_p, e5, s));
+    c->len[l] = pos + 1;
+    c->last_layer = l;
+    c->last_T = 1;
+  }
+  c->batch = B;
+  return ZDC_OK;
+}
+
+// ------------------------------------------------------------------ inspection
+zdc_status zdc_cache_length(const zdc_ctx* c, int32_t layer, int32_t* len) {
+  if (!c || !len) return fail(ZDC_ERR_INVALID_ARG, "zdc_cache_length: null argument");
+  if (layer < 0 || layer >= c->dims.n_layers) return fail(ZDC_ERR_SHAPE, "zdc_cache_length: layer %d", layer);
+  *len = c->len[layer];
+  return ZDC_OK;
+}
+
+zdc_status zdc_cache_reset(zdc_ctx* c, void* stream) {
+  if (!c) return fail(ZDC_ERR_INVALID_ARG, "zdc_cache_reset: null ctx");
+  if (!c->cache) return fail(ZDC_ERR_STATE, "zdc_cache_reset: ctx not bound");
+  ZDC_CUDA_TRY(cudaMemsetAsync(c->cache, 0, c->cache_bytes, static_cast<cudaStream_t>(stream)));
+  c->len.assign(c->dims.n_layers, 0);
+  c->batch = 0;
+  return ZDC_OK;
+}
+
+static float bf16_to_f32(uint16_t b) {
+  uint32_t u = static_cast<uint32_t>(b) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+zdc_status zdc_cache_export(const zdc_ctx* c, int32_t layer, float* k, float* v, uint8_t* is_imp, float* tau,
+                            void* stream) {
+  if (!c) return fail(ZDC_ERR_INVALID_ARG, "zdc_cache_export: null ctx");
+  if (!c->cache) return fail(ZDC_ERR_STATE, "zdc_cache_export: ctx not bound");
+  if (layer < 0 || layer >= c->dims.n_layers) return fail(ZDC_ERR_SHAPE, "zdc_cache_export: layer %d", layer);
+  const LayerInfo& L = c->layers[layer];
+  const int B = c->batch, len = c->len[layer], Nkv = c->dims.n_kv_heads;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ZDC_CUDA_TRY(cudaStreamSynchronize(st));
+  const int64_t rows = static_cast<int64_t>(c->max_batch) * Nkv * c->max_seq;
+  std::vector<uint16_t> hk, hv;
+  if (k) {
+    hk.resize(rows * L.rk_p);
+    ZDC_CUDA_TRY(cudaMemcpy(hk.data(), c->cache + L.k_off, hk.size() * 2, cudaMemcpyDeviceToHost));
+  }
+  if (v) {
+    hv.resize(rows * L.rv_p);
+    ZDC_CUDA_TRY(cudaMemcpy(hv.data(), c->cache + L.v_off, hv.size() * 2, cudaMemcpyDeviceToHost));
+  }
+  for (int b = 0; b < B; ++b)
+    for (int t = 0; t < len; ++t)
+      for (int g = 0; g < Nkv; ++g) {
+        const int64_t row = (static_cast<int64_t>(b) * Nkv + g) * c->max_seq + t;
+        if (k)
+          for (int e = 0; e < L.rk; ++e)
+            k[((static_cast<int64_t>(b) * len + t) * Nkv + g) * L.rk + e] = bf16_to_f32(hk[row * L.rk_p + e]);
+        if (v)
+          for (int e = 0; e < L.rv; ++e)
+            v[((static_cast<int64_t>(b) * len + t) * Nkv + g) * L.rv + e] = bf16_to_f32(hv[row * L.rv_p + e]);
+      }
+  if (is_imp) std::memset(is_imp, 1, static_cast<size_t>(B) * len);
+  if (tau)
+    for (int b = 0; b < B; ++b) tau[b] = INFINITY;
+  return ZDC_OK;
+}
+
+zdc_status zdc_last_lse(const zdc_ctx* c, int32_t layer, float* lse_host, void* stream) {
+  if (!c || !lse_host) return fail(ZDC_ERR_INVALID_ARG, "zdc_last_lse: null argument");
+  if (layer != c->last_layer) return fail(ZDC_ERR_STATE, "zdc_last_lse: layer %d is not the last processed (%d)",
+                                          layer, c->last_layer);
+  const int B = c->batch, Nh = c->dims.n_heads, T = c->last_T;
+  ZDC_CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  ZDC_CUDA_TRY(cudaMemcpy(lse_host, c->scratch + c->s_lse, static_cast<size_t>(B) * Nh * T * 4, cudaMemcpyDeviceToHost));
+  return ZDC_OK;
+}
+
+// ------------------------------------------------------------------ kernel-level entry
+zdc_status zdc_gemm_bf16(const uint16_t* a, const uint16_t* b, uint16_t* d, int32_t M, int32_t N, int32_t K,
+                         void* stream) {
+  if (!a || !b || !d) return fail(ZDC_ERR_INVALID_ARG, "zdc_gemm_bf16: null pointer");
+  if (M <= 0 || N <= 0 || K <= 0 || K % 64 != 0 || N % 8 != 0)
+    return fail(ZDC_ERR_SHAPE, "zdc_gemm_bf16: M=%d N=%d K=%d (need K %% 64 == 0, N %% 8 == 0)", M, N, K);
+  zdc_status st = check_sticky();
+  if (st != ZDC_OK) return st;
+  g_launches = 0;
+  Epilogue e;
+  e.mode = 0;
+  e.d = d;
+  e.ldd = N;
+  ZDC_CUDA_TRY(launch_gemm(a, K, b, K, M, N, K, e, static_cast<cudaStream_t>(stream)));
+  return ZDC_OK;
+}
+
+}  // extern "C"

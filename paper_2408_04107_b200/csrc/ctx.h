@@ -1,0 +1,47 @@
+// ctx.h — host-side state behind the opaque zdc_ctx (internal).
+#pragma once
+#include <stdint.h>
+
+#include <vector>
+
+#include "zdc.h"
+
+namespace zdc {
+
+// Per-layer packing / cache layout.  Ranks are the plan's; *_p are padded to 16.
+struct LayerInfo {
+  int rk = 0, rku = 0, rv = 0, rvu = 0;
+  int rk_p = 0, rv_p = 0, rku_p = 0, rvu_p = 0;
+  int g_bp = 10000, rep = 0;
+  bool split = false;
+  int nq = 0, nk = 0, nv = 0, n_qkv = 0, ko_p = 0;
+  int64_t w_qkv = 0, w_o = 0;                      // byte offsets in the weight region
+  int64_t k_off = 0, v_off = 0;                    // byte offsets in the cache region
+  int64_t cls_off = 0, tau_off = 0, score_off = 0;  // representative layers of split groups
+};
+
+struct CommState;
+
+}  // namespace zdc
+
+struct zdc_ctx {
+  zdc_dims dims{};
+  int G = 1;
+  int max_batch = 0, max_seq = 0;
+  int importance_mode = 0;
+  std::vector<zdc::LayerInfo> layers;
+  int64_t weight_bytes = 0, cache_bytes = 0, scratch_bytes = 0;
+  int64_t s_q = 0, s_o = 0, s_lse = 0, s_part = 0;  // scratch offsets
+  int ldq = 0, ldo = 0;
+  uint8_t* w = nullptr;
+  uint8_t* cache = nullptr;
+  uint8_t* scratch = nullptr;
+  std::vector<int> len;  // per-layer cache length
+  int batch = 0;
+  int last_layer = -1, last_T = 0;
+  zdc::CommState* comm = nullptr;
+};
+
+namespace zdc {
+void comm_destroy(zdc_ctx* c);
+}

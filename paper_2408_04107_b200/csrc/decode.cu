@@ -1,0 +1,404 @@
+// decode.cu — token-generation kernels ("Q^h is obtained from the input token, while K^h
+// and V^h of all previous tokens are retrieved from the KVC"), HBM-bound:
+//   gemv_kernel            a1 / a5 for B <= 8 rows: every folded weight byte is read once,
+//                          16-byte non-allocating loads, x staged in shared memory; the a1
+//                          epilogue writes K'/V' of the new token straight into the cache (a2).
+//   decode_attn_partial    a3: split-K over the context ("flash decoding"); one CTA per
+//                          (chunk, KV head, sequence); the G = N_h/N_kv query heads of a KV
+//                          group share each K'/V' row load (GQA, reading c4).
+//   decode_attn_combine    LSE merge of the chunks -> O' (bf16) and the row LSE (f32).
+//   pack_weights_kernel    load-time truncation + zero padding + transposition of the folded
+//                          weights; never on the hot path.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace zdc {
+
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void bf16x8_to_f32(uint4 v, float (&f)[8]) {
+  f[0] = __uint_as_float(v.x << 16);
+  f[1] = __uint_as_float(v.x & 0xFFFF0000u);
+  f[2] = __uint_as_float(v.y << 16);
+  f[3] = __uint_as_float(v.y & 0xFFFF0000u);
+  f[4] = __uint_as_float(v.z << 16);
+  f[5] = __uint_as_float(v.z & 0xFFFF0000u);
+  f[6] = __uint_as_float(v.w << 16);
+  f[7] = __uint_as_float(v.w & 0xFFFF0000u);
+}
+
+__device__ __forceinline__ float dot8(uint4 w, uint4 x) {
+  float a[8], b[8];
+  bf16x8_to_f32(w, a);
+  bf16x8_to_f32(x, b);
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s = fmaf(a[i], b[i], s);
+  return s;
+}
+
+// one bf16 output element (m, n) through the same destination map as the GEMM epilogue
+__device__ __forceinline__ void store_scalar(const Epilogue& e, int m, int n, uint16_t val) {
+  uint16_t* dst;
+  if (e.mode == 0) {
+    dst = e.d + static_cast<int64_t>(m) * e.ldd + n;
+  } else {
+    const QkvDest& q = e.qkv;
+    if (n < q.nq) {
+      dst = q.q + static_cast<int64_t>(m) * q.ldq + n;
+    } else {
+      const int b = m / q.S, t = m - b * q.S;
+      const int pos = q.posmap ? q.posmap[t] : q.pos0 + t;
+      if (n < q.nq + q.nk) {
+        const int nn = n - q.nq, g = nn / q.rk, c = nn - g * q.rk;
+        dst = q.k + b * q.kb + g * q.kg + static_cast<int64_t>(pos) * q.rk + c;
+      } else {
+        const int nn = n - q.nq - q.nk, g = nn / q.rv, c = nn - g * q.rv;
+        dst = q.v + b * q.vb + g * q.vg + static_cast<int64_t>(pos) * q.rv + c;
+      }
+    }
+  }
+  *dst = val;
+}
+
+__device__ __forceinline__ uint16_t f32_to_bf16_bits(float f) {
+  __nv_bfloat16 h = __float2bfloat16_rn(f);
+  return *reinterpret_cast<uint16_t*>(&h);
+}
+
+// ------------------------------------------------------------------ skinny projection
+template <int NB>
+__global__ void __launch_bounds__(256) gemv_kernel(const uint16_t* __restrict__ W, const uint16_t* __restrict__ x,
+                                                   int64_t ldx, int N, int K, const Epilogue epi) {
+  extern __shared__ uint4 xs[];  // [NB][K/8] bf16 units
+  const int kc = K >> 3;
+  for (int i = threadIdx.x; i < NB * kc; i += blockDim.x) {
+    const int b = i / kc, c = i - b * kc;
+    xs[i] = *reinterpret_cast<const uint4*>(x + b * ldx + c * 8);
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int U = 8;
+  for (int n = blockIdx.x * 8 + warp; n < N; n += gridDim.x * 8) {
+    const uint4* w = reinterpret_cast<const uint4*>(W + static_cast<int64_t>(n) * K);
+    float acc[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc[b] = 0.f;
+    for (int c0 = lane; c0 < kc; c0 += 32 * U) {
+      uint4 wv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + 32 * u;
+        wv[u] = c < kc ? ldg_stream(w + c) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + 32 * u;
+        if (c < kc) {
+#pragma unroll
+          for (int b = 0; b < NB; ++b) acc[b] += dot8(wv[u], xs[b * kc + c]);
+        }
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], off);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b) store_scalar(epi, b, n, f32_to_bf16_bits(acc[b]));
+    }
+  }
+}
+
+template <int NB>
+static cudaError_t launch_gemv_nb(const uint16_t* W, const uint16_t* x, int64_t ldx, int N, int K, const Epilogue& epi,
+                                  cudaStream_t stream) {
+  const size_t smem = static_cast<size_t>(NB) * K * 2;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemv_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int blocks = (N + 7) / 8;
+  const int cap = num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  gemv_kernel<NB><<<blocks, 256, smem, stream>>>(W, x, ldx, N, K, epi);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemv(const uint16_t* W, const uint16_t* x, int64_t ldx, int B, int N, int K, const Epilogue& epi,
+                        cudaStream_t stream) {
+  if (K % 8 != 0) return cudaErrorInvalidValue;
+  switch (B) {
+    case 1: return launch_gemv_nb<1>(W, x, ldx, N, K, epi, stream);
+    case 2: return launch_gemv_nb<2>(W, x, ldx, N, K, epi, stream);
+    case 3: return launch_gemv_nb<3>(W, x, ldx, N, K, epi, stream);
+    case 4: return launch_gemv_nb<4>(W, x, ldx, N, K, epi, stream);
+    case 5: return launch_gemv_nb<5>(W, x, ldx, N, K, epi, stream);
+    case 6: return launch_gemv_nb<6>(W, x, ldx, N, K, epi, stream);
+    case 7: return launch_gemv_nb<7>(W, x, ldx, N, K, epi, stream);
+    case 8: return launch_gemv_nb<8>(W, x, ldx, N, K, epi, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// ------------------------------------------------------------------ decode attention
+static constexpr int kMaxChunk = 512;
+static constexpr float kLog2e = 1.4426950408889634f;
+
+template <int RK, int RV, int G>
+__global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs a) {
+  constexpr int UK = RK / 8, RPW = 32 / UK;   // lanes per K' row, rows per warp step
+  constexpr int UV = RV / 8, RPWV = 32 / UV;  // lanes per V' row, rows per warp step
+  __shared__ float sc[G][kMaxChunk];
+  __shared__ float red[4][G][RV];
+  __shared__ float stat[2][4][G];
+  const int split = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int chunk = (a.len + a.splits - 1) / a.splits;
+  const int s0 = split * chunk;
+  const int s1 = min(a.len, s0 + chunk);
+  const int n = max(0, s1 - s0);
+  const float scl = a.scale * kLog2e;
+  const int64_t row0 = (static_cast<int64_t>(b) * a.Nkv + g) * a.S_cap;
+
+  // ---- scores s = q . k * scale * log2(e), all G heads of the group per K' row load
+  {
+    const int sub = lane / UK, u = lane % UK;
+    float qf[G][8];
+#pragma unroll
+    for (int gi = 0; gi < G; ++gi) {
+      const uint4 qv = *reinterpret_cast<const uint4*>(a.q + b * a.ldq + (g * G + gi) * RK + u * 8);
+      bf16x8_to_f32(qv, qf[gi]);
+    }
+#pragma unroll 4
+    for (int jb = warp * RPW; jb < n; jb += 4 * RPW) {  // warp-uniform trip count (shuffles inside)
+      const int j = jb + sub;
+      const bool valid = j < n;
+      const uint4 kv = valid ? ldg_stream(a.k + (row0 + s0 + j) * RK + u * 8) : make_uint4(0, 0, 0, 0);
+      float kf[8];
+      bf16x8_to_f32(kv, kf);
+#pragma unroll
+      for (int gi = 0; gi < G; ++gi) {
+        float p = 0.f;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) p = fmaf(qf[gi][e], kf[e], p);
+#pragma unroll
+        for (int off = UK / 2; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
+        if (u == 0 && valid) sc[gi][j] = p * scl;
+      }
+    }
+  }
+  __syncthreads();
+  // ---- chunk max and exponentials (P rounded to bf16 before PV; l from the unrounded P)
+  float mx[G], ls[G];
+#pragma unroll
+  for (int gi = 0; gi < G; ++gi) {
+    float m = -INFINITY;
+    for (int j = threadIdx.x; j < n; j += 128) m = fmaxf(m, sc[gi][j]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if (lane == 0) stat[0][warp][gi] = m;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int gi = 0; gi < G; ++gi) {
+    mx[gi] = fmaxf(fmaxf(stat[0][0][gi], stat[0][1][gi]), fmaxf(stat[0][2][gi], stat[0][3][gi]));
+    float l = 0.f;
+    for (int j = threadIdx.x; j < n; j += 128) {
+      const float p = exp2f(sc[gi][j] - mx[gi]);
+      l += p;
+      sc[gi][j] = __bfloat162float(__float2bfloat16_rn(p));
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+    if (lane == 0) stat[1][warp][gi] = l;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int gi = 0; gi < G; ++gi) ls[gi] = stat[1][0][gi] + stat[1][1][gi] + stat[1][2][gi] + stat[1][3][gi];
+  // ---- o = sum_j p_j V'_j  (unnormalised, relative to the chunk max)
+  {
+    const int sub = lane / UV, u = lane % UV;
+    float acc[G][8];
+#pragma unroll
+    for (int gi = 0; gi < G; ++gi)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[gi][e] = 0.f;
+#pragma unroll 4
+    for (int j = warp * RPWV + sub; j < n; j += 4 * RPWV) {
+      const uint4 vv = ldg_stream(a.v + (row0 + s0 + j) * RV + u * 8);
+      float vf[8];
+      bf16x8_to_f32(vv, vf);
+#pragma unroll
+      for (int gi = 0; gi < G; ++gi) {
+        const float p = sc[gi][j];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[gi][e] = fmaf(p, vf[e], acc[gi][e]);
+      }
+    }
+#pragma unroll
+    for (int gi = 0; gi < G; ++gi)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        float v = acc[gi][e];
+#pragma unroll
+        for (int off = UV; off < 32; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        acc[gi][e] = v;
+      }
+    if (sub == 0) {
+#pragma unroll
+      for (int gi = 0; gi < G; ++gi)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) red[warp][gi][u * 8 + e] = acc[gi][e];
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G * RV; i += 128) {
+    const int gi = i / RV, c = i - gi * RV;
+    const int h = g * G + gi;
+    float* dst = a.part + ((static_cast<int64_t>(b) * a.Nh + h) * a.splits + split) * (RV + 2);
+    dst[c] = red[0][gi][c] + red[1][gi][c] + red[2][gi][c] + red[3][gi][c];
+    if (c == 0) {
+      dst[RV] = n > 0 ? mx[gi] : -INFINITY;
+      dst[RV + 1] = n > 0 ? ls[gi] : 0.f;
+    }
+  }
+}
+
+template <int RV>
+__global__ void __launch_bounds__(128) decode_attn_combine(const DecodeAttnArgs a) {
+  const int h = blockIdx.x, b = blockIdx.y;
+  const float* part = a.part + (static_cast<int64_t>(b) * a.Nh + h) * a.splits * (RV + 2);
+  __shared__ float w[64];
+  __shared__ float tot;
+  if (threadIdx.x == 0) {
+    float M = -INFINITY;
+    for (int s = 0; s < a.splits; ++s) M = fmaxf(M, part[s * (RV + 2) + RV]);
+    float L = 0.f;
+    for (int s = 0; s < a.splits; ++s) {
+      const float m = part[s * (RV + 2) + RV];
+      const float ws = m == -INFINITY ? 0.f : exp2f(m - M);
+      w[s] = ws;
+      L += ws * part[s * (RV + 2) + RV + 1];
+    }
+    tot = L;
+    if (a.lse) a.lse[b * a.Nh + h] = (M + log2f(L)) / kLog2e;
+  }
+  __syncthreads();
+  const float inv = 1.f / tot;
+  for (int c = threadIdx.x; c < RV; c += blockDim.x) {
+    float o = 0.f;
+    for (int s = 0; s < a.splits; ++s) o = fmaf(w[s], part[s * (RV + 2) + c], o);
+    a.o[b * a.ldo + h * RV + c] = f32_to_bf16_bits(o * inv);
+  }
+}
+
+int decode_splits(int B, int Nkv, int len) {
+  const int pairs = B * Nkv;
+  int s = (4 * num_sms() + pairs - 1) / pairs;     // ~4 CTAs per SM
+  const int min_for_smem = (len + kMaxChunk - 1) / kMaxChunk;
+  if (s < min_for_smem) s = min_for_smem;
+  const int max_useful = (len + 31) / 32;            // >= 32 keys per chunk
+  if (s > max_useful) s = max_useful;
+  if (s < min_for_smem) s = min_for_smem;
+  if (s > 64) s = 64;
+  if (s < 1) s = 1;
+  return s;
+}
+
+template <int RK, int RV, int G>
+static cudaError_t launch_decode_t(const DecodeAttnArgs& a, cudaStream_t stream) {
+  dim3 grid(a.splits, a.Nkv, a.B);
+  decode_attn_partial<RK, RV, G><<<grid, 128, 0, stream>>>(a);
+  decode_attn_combine<RV><<<dim3(a.Nh, a.B), 128, 0, stream>>>(a);
+  g_launches += 2;
+  return cudaGetLastError();
+}
+
+template <int RK, int RV>
+static cudaError_t launch_decode_g(const DecodeAttnArgs& a, cudaStream_t stream) {
+  const int G = a.Nh / a.Nkv;
+  switch (G) {
+    case 1: return launch_decode_t<RK, RV, 1>(a, stream);
+    case 2: return launch_decode_t<RK, RV, 2>(a, stream);
+    case 4: return launch_decode_t<RK, RV, 4>(a, stream);
+    case 8: return launch_decode_t<RK, RV, 8>(a, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t stream) {
+  if (a.splits > 64 || (a.len + a.splits - 1) / a.splits > kMaxChunk) return cudaErrorInvalidValue;
+  if (a.rk != a.rv) return cudaErrorInvalidValue;
+  switch (a.rk) {
+    case 16: return launch_decode_g<16, 16>(a, stream);
+    case 32: return launch_decode_g<32, 32>(a, stream);
+    case 64: return launch_decode_g<64, 64>(a, stream);
+    case 128: return launch_decode_g<128, 128>(a, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// ------------------------------------------------------------------ weight packing (load time)
+// W_qkv^T [nq + nk + nv][d]: row h*rk_p + c (c < rk) = column h*dh + c of W_Q^R (zero for c >= rk),
+// then K groups, then V groups (rank rv).  W_o^T [d][ko_p]: column h*rv_p + c (c < rv) = row
+// h*dh + c of W_O^R; padding columns zero.
+__global__ void pack_qkv_kernel(const uint16_t* __restrict__ wq, const uint16_t* __restrict__ wk,
+                                const uint16_t* __restrict__ wv, uint16_t* __restrict__ out, int d, int Nh, int Nkv,
+                                int dh, int rk, int rv, int rk_p, int rv_p) {
+  const int64_t nq = static_cast<int64_t>(Nh) * rk_p, nk = static_cast<int64_t>(Nkv) * rk_p,
+                nv = static_cast<int64_t>(Nkv) * rv_p;
+  const int64_t total = (nq + nk + nv) * d;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t n = i / d;
+    const int k = static_cast<int>(i - n * d);
+    uint16_t val = 0;
+    if (n < nq) {
+      const int h = static_cast<int>(n / rk_p), c = static_cast<int>(n % rk_p);
+      if (c < rk) val = wq[static_cast<int64_t>(k) * Nh * dh + h * dh + c];
+    } else if (n < nq + nk) {
+      const int g = static_cast<int>((n - nq) / rk_p), c = static_cast<int>((n - nq) % rk_p);
+      if (c < rk) val = wk[static_cast<int64_t>(k) * Nkv * dh + g * dh + c];
+    } else {
+      const int g = static_cast<int>((n - nq - nk) / rv_p), c = static_cast<int>((n - nq - nk) % rv_p);
+      if (c < rv) val = wv[static_cast<int64_t>(k) * Nkv * dh + g * dh + c];
+    }
+    out[i] = val;
+  }
+}
+
+__global__ void pack_o_kernel(const uint16_t* __restrict__ wo, uint16_t* __restrict__ out, int d, int Nh, int dh,
+                              int rv, int rv_p, int ko_p) {
+  const int64_t total = static_cast<int64_t>(d) * ko_p;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(i / ko_p);
+    const int col = static_cast<int>(i - static_cast<int64_t>(j) * ko_p);
+    const int h = col / rv_p, c = col - h * rv_p;
+    uint16_t val = 0;
+    if (h < Nh && c < rv) val = wo[static_cast<int64_t>(h * dh + c) * d + j];
+    out[i] = val;
+  }
+}
+
+cudaError_t launch_pack_weights_bf16(const uint16_t* wq, const uint16_t* wk, const uint16_t* wv, const uint16_t* wo,
+                                     uint16_t* wqkv_t, uint16_t* wo_t, int d, int Nh, int Nkv, int dh, int rk, int rv,
+                                     int rk_p, int rv_p, int ko_p, cudaStream_t stream) {
+  pack_qkv_kernel<<<4 * num_sms(), 256, 0, stream>>>(wq, wk, wv, wqkv_t, d, Nh, Nkv, dh, rk, rv, rk_p, rv_p);
+  pack_o_kernel<<<4 * num_sms(), 256, 0, stream>>>(wo, wo_t, d, Nh, dh, rv, rv_p, ko_p);
+  return cudaGetLastError();
+}
+
+}  // namespace zdc

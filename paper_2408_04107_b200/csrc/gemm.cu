@@ -1,0 +1,273 @@
+// gemm.cu — the a1 / a5 projection engine: D[M][N] = A[M][K] * B[N][K]^T.
+//
+// a1 (Eq. 1, with the folded, pre-truncated W^R of P:1206 / P:1218): A = x [B*S][d],
+//    B = packed W_QKV^R transposed [N_h r_k + N_kv (r_k + r_v)][d]; the epilogue scatters Q' to
+//    a staging matrix and K'/V' straight into the compressed KV cache (a2 fused).
+// a5 (Eq. 4, folded W_O of P:1219-1221): A = O' [B*S][N_h r_v], B = W_O^R transposed.
+//
+// sm_100a design: persistent CTAs (one per SM), warp-specialised:
+//   warp 0   TMA producer   (cp.async.bulk.tensor, 128B swizzle, STAGES-deep mbarrier ring)
+//   warp 1   MMA issuer     (one elected thread, tcgen05.mma kind::f16 M=128 N=BN K=16)
+//   warp 2   TMEM allocator (2 x BN f32 columns: double-buffered accumulators)
+//   warps 4-7 epilogue     (tcgen05.ld 32x32b -> bf16 RNE -> global), overlapping the next
+//                           tile's mainloop through the accumulator double buffer.
+#include "common.cuh"
+#include "kernels.h"
+
+#include <mutex>
+
+namespace zdc {
+
+int64_t g_launches = 0;
+
+// ------------------------------------------------------------------ host: tensor maps
+typedef CUresult (*PFN_tmapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                        const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                        CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                        CUtensorMapFloatOOBfill);
+
+static PFN_tmapEncodeTiled get_encode_fn() {
+  static PFN_tmapEncodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_tmapEncodeTiled>(p);
+  });
+  return fn;
+}
+
+bool make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner_elems, uint64_t outer_rows,
+                  uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes) {
+  PFN_tmapEncodeTiled fn = get_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner_elems, outer_rows};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMapSwizzle sw = swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                          : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                : CU_TENSOR_MAP_SWIZZLE_NONE;
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = kNumSMsB200;
+  }
+  return n;
+}
+
+// ------------------------------------------------------------------ device: epilogue store
+// Store 8 consecutive output columns [n, n+8) of row m (already packed to bf16x2 x 4).
+__device__ __forceinline__ void store_unit(const Epilogue& e, int m, int n, uint4 val) {
+  uint16_t* dst;
+  if (e.mode == 0) {
+    dst = e.d + static_cast<int64_t>(m) * e.ldd + n;
+  } else {
+    const QkvDest& q = e.qkv;
+    if (n < q.nq) {
+      dst = q.q + static_cast<int64_t>(m) * q.ldq + n;
+    } else {
+      const int b = m / q.S, t = m - (m / q.S) * q.S;
+      const int pos = q.posmap ? q.posmap[t] : q.pos0 + t;
+      if (n < q.nq + q.nk) {
+        const int nn = n - q.nq, g = nn / q.rk, c = nn - g * q.rk;
+        dst = q.k + b * q.kb + g * q.kg + static_cast<int64_t>(pos) * q.rk + c;
+      } else {
+        const int nn = n - q.nq - q.nk, g = nn / q.rv, c = nn - g * q.rv;
+        dst = q.v + b * q.vb + g * q.vg + static_cast<int64_t>(pos) * q.rv + c;
+      }
+    }
+  }
+  *reinterpret_cast<uint4*>(dst) = val;
+}
+
+// ------------------------------------------------------------------ device: the GEMM
+template <int BN>
+struct GemmCfg {
+  static constexpr int BM = 128, BK = 64;
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr uint32_t TMEM_COLS = 2 * BN;
+  static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(256, 1)
+    gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, int M,
+                        int N, int K, const Epilogue epi) {
+  using C = GemmCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int m_tiles = (M + C::BM - 1) / C::BM;
+  const int n_tiles = (N + BN - 1) / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int k_blocks = K / C::BK;
+  const uint32_t warp = warp_id(), lane = lane_id();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tma_a);
+    tma_prefetch_desc(&tma_b);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int mb = tile % m_tiles, nb = tile / m_tiles;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          tma_load_2d(sA + stage * C::A_BYTES, &tma_a, &full[stage], kb * C::BK, mb * C::BM);
+          tma_load_2d(sB + stage * C::B_BYTES, &tma_b, &full[stage], kb * C::BK, nb * BN);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    if (elect_one()) {
+      constexpr uint32_t idesc = make_idesc_bf16(C::BM, BN, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < C::BK / 16; ++kk) {
+            const uint64_t ad = make_sdesc(a_addr + kk * 32, 16, 1024, kSw128);
+            const uint64_t bd = make_sdesc(b_addr + kk * 32, 16, 1024, kSw128);
+            umma_bf16_ss(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);  // frees the smem slot once these MMAs have read it
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM -> registers -> bf16 -> global
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int mb = tile % m_tiles, nb = tile / m_tiles;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * C::BM + q * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((q * 32) << 16) + acc * BN + c, r);
+        tc_wait_ld();
+        const int n0 = nb * BN + c;
+        if (row < M && n0 < N) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int n = n0 + u * 8;
+            if (n + 8 <= N) {
+              uint4 val;
+              val.x = pack_bf16x2(__uint_as_float(r[u * 8 + 0]), __uint_as_float(r[u * 8 + 1]));
+              val.y = pack_bf16x2(__uint_as_float(r[u * 8 + 2]), __uint_as_float(r[u * 8 + 3]));
+              val.z = pack_bf16x2(__uint_as_float(r[u * 8 + 4]), __uint_as_float(r[u * 8 + 5]));
+              val.w = pack_bf16x2(__uint_as_float(r[u * 8 + 6]), __uint_as_float(r[u * 8 + 7]));
+              store_unit(epi, row, n, val);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+template <int BN>
+static cudaError_t launch_gemm_bn(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
+                                  const Epilogue& epi, cudaStream_t stream) {
+  using C = GemmCfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(C::SMEM));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int tiles = ((M + C::BM - 1) / C::BM) * ((N + BN - 1) / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  gemm_bf16_tc_kernel<BN><<<grid, 256, C::SMEM, stream>>>(ta, tb, M, N, K, epi);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemm(const uint16_t* A, int64_t lda, const uint16_t* B, int64_t ldb, int M, int N, int K,
+                        const Epilogue& epi, cudaStream_t stream) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  if (K % 64 != 0) return cudaErrorInvalidValue;
+  const int BN = N > 128 ? 256 : 128;
+  CUtensorMap ta, tb;
+  if (!make_tmap_2d(&ta, A, K, M, lda * 2, 64, 128, 128)) return cudaErrorInvalidValue;
+  if (!make_tmap_2d(&tb, B, K, N, ldb * 2, 64, BN, 128)) return cudaErrorInvalidValue;
+  return BN == 256 ? launch_gemm_bn<256>(ta, tb, M, N, K, epi, stream)
+                   : launch_gemm_bn<128>(ta, tb, M, N, K, epi, stream);
+}
+
+}  // namespace zdc

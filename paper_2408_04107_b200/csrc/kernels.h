@@ -1,0 +1,93 @@
+// kernels.h — host-side launch interface of the ZDC sm_100a kernels (internal to libzdc.so).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace zdc {
+
+// Where the a1 projection writes its outputs: Q' to a staging matrix,
+// K'/V' straight into the compressed KV cache (the append of a2 fused into the epilogue).
+// Output column n of the packed [Q'|K'|V'] row: n < nq -> Q' col n; n < nq+nk -> K' of KV head
+// (n-nq)/rk, dim (n-nq)%rk; else V' of head (n-nq-nk)/rv, dim (n-nq-nk)%rv.
+// Token row m = b*S + t is written at cache position posmap ? posmap[t] : pos0 + t.
+struct QkvDest {
+  uint16_t* q = nullptr;
+  int64_t ldq = 0;
+  int nq = 0, nk = 0;
+  uint16_t* k = nullptr;
+  uint16_t* v = nullptr;
+  int rk = 0, rv = 0;
+  int S = 1;
+  int64_t kb = 0, kg = 0, vb = 0, vg = 0;  // element strides per sequence / per KV head
+  int pos0 = 0;
+  const int* posmap = nullptr;
+};
+
+struct Epilogue {
+  int mode = 0;  // 0 = plain bf16 D[M][ldd]; 1 = QKV scatter (QkvDest)
+  uint16_t* d = nullptr;
+  int64_t ldd = 0;
+  QkvDest qkv;
+};
+
+// ---- tensor maps (driver entry point resolved at runtime; no -lcuda link)
+bool make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner_elems, uint64_t outer_rows,
+                  uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes);
+
+int num_sms();
+
+// ---- a1 / a5 projection GEMM: D[M][N] = A[M][K] * B[N][K]^T (tcgen05, TMA, TMEM)
+cudaError_t launch_gemm(const uint16_t* A, int64_t lda, const uint16_t* B, int64_t ldb, int M, int N, int K,
+                        const Epilogue& epi, cudaStream_t stream);
+
+// ---- decode: skinny projection (B <= 8 rows), weights streamed once from HBM
+cudaError_t launch_gemv(const uint16_t* W, const uint16_t* x, int64_t ldx, int B, int N, int K,
+                        const Epilogue& epi, cudaStream_t stream);
+
+// ---- a3 prefill attention (tcgen05 flash attention at head dim r, causal, LSE out)
+struct PrefillAttnArgs {
+  const uint16_t* q;   // Q' staging [B*S][ldq]; head h at cols h*rk
+  int64_t ldq;
+  const uint16_t* k;   // K' cache rows: sequence b, KV head g, position p at ((b*Nkv+g)*S_cap + p)*rk
+  const uint16_t* v;   // V' likewise with rv
+  int S_cap;           // row capacity per (b, g) of the K/V buffers
+  uint16_t* o;         // O' [B*S][ldo]; head h at cols h*rv
+  int64_t ldo;
+  float* lse;          // [B][Nh][S] (natural log of the Eq. 3 denominator), may be null
+  int B, S, Nh, Nkv, rk, rv;
+  float scale;         // 1/sqrt(d_h) (reading c2)
+  int q_pos0;          // global position of query row t is q_pos0 + t (SP chunks)
+  int q_row0;          // first row of this chunk inside the Q'/O' matrices
+  int n_q;             // number of query rows of this launch (per sequence)
+};
+cudaError_t launch_prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream);
+
+// ---- a3 decode attention: split-K over the context + LSE-merge combine
+struct DecodeAttnArgs {
+  const uint16_t* q;   // Q' [B][ldq]
+  int64_t ldq;
+  const uint16_t* k;   // cache, same addressing as PrefillAttnArgs
+  const uint16_t* v;
+  int S_cap;
+  int len;             // keys visible: positions [0, len)
+  uint16_t* o;         // O' [B][ldo]
+  int64_t ldo;
+  float* lse;          // [B][Nh]
+  float* part;         // scratch [B][Nh][splits][rv + 2]
+  int B, Nh, Nkv, rk, rv;
+  float scale;
+  int splits;
+};
+cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t stream);
+int decode_splits(int B, int Nkv, int len);
+
+// ---- weight packing (load time): f32/bf16 full-rank folded -> truncated, padded, bf16
+cudaError_t launch_pack_weights_bf16(const uint16_t* wq, const uint16_t* wk, const uint16_t* wv,
+                                     const uint16_t* wo, uint16_t* wqkv_t, uint16_t* wo_t, int d, int Nh,
+                                     int Nkv, int dh, int rk, int rv, int rk_p, int rv_p, int ko_p,
+                                     cudaStream_t stream);
+
+extern int64_t g_launches;  // kernels enqueued by the last API call
+
+}  // namespace zdc
