@@ -1,5 +1,313 @@
-// attn_prefill.cu — placeholder until the tcgen05 prefill attention lands.
+// attn_prefill.cu — a3 for prompt processing: causal attention at head dimension r run directly
+// on the compressed Q'/K'/V' (Lemma 2: Q'(K')^T ~ QK^T needs no decompression; the
+// V' decompression happens inside a5).  Eqs. 2-3 with the ORIGINAL
+// scale 1/sqrt(d_h) (reading c2), and the log of each row's softmax denominator (LSE) written
+// out in f32 — the "reused softmax denominators" of P:1442 that a4 ranks.
+//
+// One CTA per (128-query tile, head, sequence), FlashAttention-style online softmax with the
+// two contractions on tcgen05:
+//   S_j  = Q' K'_j^T   tcgen05.mma M=128 N=128 K=r   (A = Q' smem K-major, B = K' smem K-major)
+//   O   += P_j V'_j    tcgen05.mma M=128 N=r  K=128  (A = P smem K-major,  B = V' smem MN-major)
+// S is double-buffered in TMEM so the MMA of S_{j+1} overlaps the softmax of S_j; O stays in
+// TMEM for the whole KV loop and is rescaled in place when the running max moves.
+// Warps 0-3: softmax (thread = query row = TMEM lane); warp 4: TMA producer; warp 5: MMA issuer.
+// Rounding points: P = exp(s - m) rounded to bf16 before PV, l from the
+// unrounded P; O' rounded to bf16 after the division by l.
+#include "common.cuh"
 #include "kernels.h"
+
 namespace zdc {
-cudaError_t launch_prefill_attention(const PrefillAttnArgs&, cudaStream_t) { return cudaErrorNotSupported; }
+
+static constexpr float kLog2eF = 1.4426950408889634f;
+static constexpr float kLn2F = 0.6931471805599453f;
+
+template <int HD>
+struct AttnCfg {
+  static constexpr int BM = 128, BN = 128;                 // query rows / keys per tile
+  static constexpr int CW = HD < 64 ? HD : 64;             // elements per swizzle chunk row
+  static constexpr int NCH = HD / CW;                      // chunks across the head dim
+  static constexpr int SWB = CW * 2;                       // swizzle width in bytes (32/64/128)
+  static constexpr uint32_t LAYOUT = SWB == 128 ? kSw128 : SWB == 64 ? kSw64 : kSw32;
+  static constexpr uint32_t CHUNK = BM * SWB;              // bytes of one [128][CW] chunk
+  static constexpr uint32_t TILE = CHUNK * NCH;            // bytes of one [128][HD] tile
+  static constexpr uint32_t P_BYTES = BM * BN * 2;         // P as two [128][64] SW128 chunks
+  static constexpr uint32_t OFF_Q = 0;
+  static constexpr uint32_t OFF_K = TILE;
+  static constexpr uint32_t OFF_V = OFF_K + 2 * TILE;
+  static constexpr uint32_t OFF_P = OFF_V + 2 * TILE;
+  static constexpr uint32_t OFF_BAR = OFF_P + P_BYTES;
+  static constexpr uint32_t SMEM = OFF_BAR + 256 + 1024;
+  static constexpr uint32_t TMEM_COLS = 512;               // S0 [0,128) S1 [128,256) O [256, 256+HD)
+  static constexpr uint32_t O_COL = 256;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(192, 1)
+    prefill_attn_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                        const __grid_constant__ CUtensorMap tv, const PrefillAttnArgs a) {
+  using C = AttnCfg<HD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* q_full = bar + 0;
+  uint64_t* k_full = bar + 1;   // [2]
+  uint64_t* k_empty = bar + 3;  // [2]
+  uint64_t* v_full = bar + 5;   // [2]
+  uint64_t* v_empty = bar + 7;  // [2]
+  uint64_t* s_full = bar + 9;   // [2]
+  uint64_t* s_empty = bar + 11; // [2]
+  uint64_t* p_full = bar + 13;
+  uint64_t* pv_done = bar + 14;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+
+  // heavy (long causal row) tiles first
+  const int n_qt = (a.n_q + C::BM - 1) / C::BM;
+  const int qt = n_qt - 1 - static_cast<int>(blockIdx.x);
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int G = a.Nh / a.Nkv, g = h / G;
+  const int q0 = qt * C::BM;                                 // first query row of the tile (chunk-relative)
+  const int last_q = min(q0 + C::BM, a.n_q) - 1;
+  const int kv_end = a.q_pos0 + last_q + 1;                   // keys [0, kv_end) are visible to some row
+  const int n_kv = (kv_end + C::BN - 1) / C::BN;
+  const int q_row = b * a.S + a.q_row0 + q0;                  // row in the Q'/O' matrices
+  const int kv_row0 = (b * a.Nkv + g) * a.S_cap;              // row of key 0 in the K'/V' buffers
+  const uint32_t warp = warp_id(), lane = lane_id();
+
+  if (warp == 4) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tq);
+      tma_prefetch_desc(&tk);
+      tma_prefetch_desc(&tv);
+      mbar_init(q_full, 1);
+      for (int i = 0; i < 2; ++i) {
+        mbar_init(&k_full[i], 1);
+        mbar_init(&k_empty[i], 1);
+        mbar_init(&v_full[i], 1);
+        mbar_init(&v_empty[i], 1);
+        mbar_init(&s_full[i], 1);
+        mbar_init(&s_empty[i], 128);
+      }
+      mbar_init(p_full, 128);
+      mbar_init(pv_done, 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    tmem_alloc(tmem_slot, C::TMEM_COLS);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 4) {
+    // ------------------------------------------------ TMA producer
+    if (elect_one()) {
+      const uint64_t keep = policy_evict_last();
+      mbar_arrive_expect_tx(q_full, C::TILE);
+#pragma unroll
+      for (int c = 0; c < C::NCH; ++c)
+        tma_load_2d(smem + C::OFF_Q + c * C::CHUNK, &tq, q_full, h * HD + c * C::CW, q_row);
+      for (int j = 0; j < n_kv; ++j) {
+        const int s = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(&k_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&k_full[s], C::TILE);
+#pragma unroll
+        for (int c = 0; c < C::NCH; ++c)
+          tma_load_2d_hint(smem + C::OFF_K + s * C::TILE + c * C::CHUNK, &tk, &k_full[s], c * C::CW,
+                           kv_row0 + j * C::BN, keep);
+        mbar_wait(&v_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&v_full[s], C::TILE);
+#pragma unroll
+        for (int c = 0; c < C::NCH; ++c)
+          tma_load_2d_hint(smem + C::OFF_V + s * C::TILE + c * C::CHUNK, &tv, &v_full[s], c * C::CW,
+                           kv_row0 + j * C::BN, keep);
+      }
+    }
+  } else if (warp == 5) {
+    // ------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      constexpr uint32_t idesc_s = make_idesc_bf16(C::BM, C::BN, 0, 0);
+      constexpr uint32_t idesc_o = make_idesc_bf16(C::BM, HD, 0, 1);
+      const uint32_t q_addr = smem_u32(smem + C::OFF_Q);
+      const uint32_t p_addr = smem_u32(smem + C::OFF_P);
+      auto issue_s = [&](int j) {
+        const int s = j & 1;
+        mbar_wait(&k_full[s], (j >> 1) & 1);
+        mbar_wait(&s_empty[s], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(smem + C::OFF_K + s * C::TILE);
+#pragma unroll
+        for (int c = 0; c < C::NCH; ++c)
+#pragma unroll
+          for (int kk = 0; kk < C::CW / 16; ++kk) {
+            const uint64_t ad = make_sdesc(q_addr + c * C::CHUNK + kk * 32, 16, 8 * C::SWB, C::LAYOUT);
+            const uint64_t bd = make_sdesc(k_addr + c * C::CHUNK + kk * 32, 16, 8 * C::SWB, C::LAYOUT);
+            umma_bf16_ss(tmem + s * 128, ad, bd, idesc_s, (c | kk) != 0 ? 1u : 0u);
+          }
+        umma_commit(&k_empty[s]);
+        umma_commit(&s_full[s]);
+      };
+      mbar_wait(q_full, 0);
+      issue_s(0);
+      for (int j = 0; j < n_kv; ++j) {
+        if (j + 1 < n_kv) issue_s(j + 1);
+        const int s = j & 1;
+        mbar_wait(p_full, j & 1);
+        mbar_wait(&v_full[s], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t v_addr = smem_u32(smem + C::OFF_V + s * C::TILE);
+#pragma unroll
+        for (int kk = 0; kk < C::BN / 16; ++kk) {
+          const uint64_t ad = make_sdesc(p_addr + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, kSw128);
+          const uint64_t bd = make_sdesc(v_addr + kk * 16 * C::SWB, C::CHUNK, 8 * C::SWB, C::LAYOUT);
+          umma_bf16_ss(tmem + C::O_COL, ad, bd, idesc_o, (j | kk) != 0 ? 1u : 0u);
+        }
+        umma_commit(&v_empty[s]);
+        umma_commit(pv_done);
+      }
+    }
+  } else {
+    // ------------------------------------------------ softmax warps 0..3: thread = query row
+    const int r = warp * 32 + lane;
+    const int qpos = a.q_pos0 + q0 + r;                      // global position of this query row
+    const uint32_t lane_base = (warp * 32) << 16;
+    const float sl = a.scale * kLog2eF;
+    float m_run = -INFINITY, l_run = 0.f;
+    uint8_t* p_smem = smem + C::OFF_P;
+    for (int j = 0; j < n_kv; ++j) {
+      const int s = j & 1;
+      mbar_wait(&s_full[s], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t sv[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(tmem + lane_base + s * 128 + c * 32, sv[c]);
+      tc_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&s_empty[s]);
+      const int key0 = j * C::BN;
+      const bool diag = key0 + C::BN - 1 > qpos;             // some key of this tile is in the future
+      float tmax = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          float x = __uint_as_float(sv[c][e]) * sl;
+          if (diag && key0 + c * 32 + e > qpos) x = -INFINITY;
+          sv[c][e] = __float_as_uint(x);
+          tmax = fmaxf(tmax, x);
+        }
+      const float m_new = fmaxf(m_run, tmax);
+      const float alpha = exp2f(m_run - m_new);              // 0 on the first tile
+      float psum = 0.f;
+      uint32_t pk[4][16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float p0 = fast_exp2(__uint_as_float(sv[c][2 * e]) - m_new);
+          const float p1 = fast_exp2(__uint_as_float(sv[c][2 * e + 1]) - m_new);
+          psum += p0 + p1;
+          pk[c][e] = pack_bf16x2(p0, p1);
+        }
+      l_run = l_run * alpha + psum;
+      m_run = m_new;
+      // O (TMEM) and the P buffer (smem) are free once PV_{j-1} has completed
+      if (j > 0) {
+        mbar_wait(pv_done, (j - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+          for (int c0 = 0; c0 < HD; c0 += 16) {
+            uint32_t ov[16];
+            tmem_ld16(tmem + lane_base + C::O_COL + c0, ov);
+            tc_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+            tmem_st16(tmem + lane_base + C::O_COL + c0, ov);
+          }
+          tc_wait_st();
+        }
+      }
+      // P row r -> two [128][64] K-major SW128 chunks
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int c = u >> 3, uu = u & 7;
+        uint4 val = make_uint4(pk[u >> 2][(u & 3) * 4 + 0], pk[u >> 2][(u & 3) * 4 + 1],
+                               pk[u >> 2][(u & 3) * 4 + 2], pk[u >> 2][(u & 3) * 4 + 3]);
+        *reinterpret_cast<uint4*>(p_smem + c * 16384 + sw128_off(r, uu)) = val;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      mbar_arrive(p_full);
+    }
+    // ---- epilogue: O / l -> bf16, LSE
+    mbar_wait(pv_done, (n_kv - 1) & 1);
+    tc_fence_after();
+    const float inv_l = 1.f / l_run;
+    const bool valid = q0 + r < a.n_q;
+    uint16_t* orow = a.o + static_cast<int64_t>(q_row + r) * a.ldo + h * HD;
+#pragma unroll
+    for (int c0 = 0; c0 < HD; c0 += 16) {
+      uint32_t ov[16];
+      tmem_ld16(tmem + lane_base + C::O_COL + c0, ov);
+      tc_wait_ld();
+      if (valid) {
+        uint4 w0, w1;
+        w0.x = pack_bf16x2(__uint_as_float(ov[0]) * inv_l, __uint_as_float(ov[1]) * inv_l);
+        w0.y = pack_bf16x2(__uint_as_float(ov[2]) * inv_l, __uint_as_float(ov[3]) * inv_l);
+        w0.z = pack_bf16x2(__uint_as_float(ov[4]) * inv_l, __uint_as_float(ov[5]) * inv_l);
+        w0.w = pack_bf16x2(__uint_as_float(ov[6]) * inv_l, __uint_as_float(ov[7]) * inv_l);
+        w1.x = pack_bf16x2(__uint_as_float(ov[8]) * inv_l, __uint_as_float(ov[9]) * inv_l);
+        w1.y = pack_bf16x2(__uint_as_float(ov[10]) * inv_l, __uint_as_float(ov[11]) * inv_l);
+        w1.z = pack_bf16x2(__uint_as_float(ov[12]) * inv_l, __uint_as_float(ov[13]) * inv_l);
+        w1.w = pack_bf16x2(__uint_as_float(ov[14]) * inv_l, __uint_as_float(ov[15]) * inv_l);
+        *reinterpret_cast<uint4*>(orow + c0) = w0;
+        *reinterpret_cast<uint4*>(orow + c0 + 8) = w1;
+      }
+    }
+    if (valid && a.lse) a.lse[(static_cast<int64_t>(b) * a.Nh + h) * a.S + a.q_row0 + q0 + r] = (m_run + log2f(l_run)) * kLn2F;
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+template <int HD>
+static cudaError_t launch_attn_t(const PrefillAttnArgs& a, cudaStream_t stream) {
+  using C = AttnCfg<HD>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(prefill_attn_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(C::SMEM));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  CUtensorMap tq, tk, tv;
+  const uint64_t q_rows = static_cast<uint64_t>(a.B) * a.S;
+  const uint64_t kv_rows = static_cast<uint64_t>(a.B) * a.Nkv * a.S_cap;
+  if (!make_tmap_2d(&tq, a.q, static_cast<uint64_t>(a.ldq), q_rows, a.ldq * 2, C::CW, C::BM, C::SWB))
+    return cudaErrorInvalidValue;
+  if (!make_tmap_2d(&tk, a.k, HD, kv_rows, HD * 2, C::CW, C::BN, C::SWB)) return cudaErrorInvalidValue;
+  if (!make_tmap_2d(&tv, a.v, HD, kv_rows, HD * 2, C::CW, C::BN, C::SWB)) return cudaErrorInvalidValue;
+  dim3 grid((a.n_q + C::BM - 1) / C::BM, a.Nh, a.B);
+  prefill_attn_kernel<HD><<<grid, 192, C::SMEM, stream>>>(tq, tk, tv, a);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream) {
+  if (a.rk != a.rv) return cudaErrorInvalidValue;
+  switch (a.rk) {
+    case 16: return launch_attn_t<16>(a, stream);
+    case 32: return launch_attn_t<32>(a, stream);
+    case 64: return launch_attn_t<64>(a, stream);
+    case 128: return launch_attn_t<128>(a, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 }  // namespace zdc
