@@ -1,0 +1,422 @@
+#!/usr/bin/env python
+"""bench.py — ZDC compressed-attention hot path on B200 (BASELINE.json metric, configs[1] = c2).
+
+Workload (config "c2_llama2_7b"): Llama-2-7B-shaped attention stack, 32 layers, d=4096, 32 heads,
+d_h=128, rank r = d_h/2 = 64 (uniform plan), batch 1, prompt 2048 tokens, then 256 decode steps.
+One STEP = the whole hot path over one request: prefill of the 2048-token prompt through the 32
+layers (a1 QKV projection + fused cache append, a3 causal attention, a5 output projection), then
+256 decode steps x 32 layers.  value = tokens processed per second (2048 prompt + 256 generated
+per step per GPU), whole job; prefill and decode tok/s are reported alongside.
+
+Timing: CUDA events on the launching stream, W warm-up steps, K timed steps bracketed by a
+barrier + synchronize, max over ranks.  Inputs are larger than L2 (2.1 GB of folded weights
+stream through every step), so no explicit flush.  Each layer is called with the same seeded x
+(no chaining: a chained stack shrinks activations towards underflow), 32
+per-layer calls captured in one CUDA graph for the prefill and one per decode step.
+
+N > 1: independent replicas (decode is "replicas only"; the c2 prefill fits one GPU), weak scaling.
+--impl reference: the fp64 CPU oracle (oracle/) on a bounded sample, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "compressed-attn prefill tok/s & decode tok/s per B200 (% roofline); SP K/V exchange GB/s"
+CONFIG_NAME = "c2_llama2_7b"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="zdc", choices=["zdc", "reference"])
+    p.add_argument("--decode-steps", type=int, default=256)
+    p.add_argument("--prompt", type=int, default=2048)
+    p.add_argument("--rank", type=int, default=64)
+    p.add_argument("--layers", type=int, default=32)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--profile-only", action="store_true", help="one eager step (for ncu), no JSON")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------------------------ peaks
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return dict(hbm=float(d["hbm_gbs"]), tf=float(d["bf16_tflops"]),
+                    tf_sus=float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), src="measured")
+    return dict(hbm=6650.0, tf=1590.0, tf_sus=1400.0, src="fallback")
+
+
+# ------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev: int):
+        self.dev, self.proc, self.lines = dev, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.dev)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, pw, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+                pw.append(float(f[3]))
+            except ValueError:
+                continue
+            for i, n in enumerate(names):
+                if f[5 + i].lower().startswith("active"):
+                    reasons.add(n)
+        loaded = [s for s, p in zip(sm, pw) if p > 200.0] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(pw) if pw else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------------------------ oracle baseline
+def oracle_sample(n_decode: int = 16, prompt: int = 2048):
+    """The fp64 oracle as it stands, on a bounded sample of the c2 workload: one layer's fold
+    (untimed, like the GPU path's), one layer prefill of the full prompt, n_decode decode steps.
+    Returns (seconds_prefill_layer, seconds_per_decode_layer_step, cores)."""
+    import numpy as np
+    import oracle as O
+    import zdc_synth as Z
+    dims = Z.dims_of(2, n_layers=1)
+    plan = Z.plan_uniform(1, 64)
+    w = Z.layer_weights(dims, 2, 0)
+    xc = Z.calibration(dims, 2, 0, 4096)
+    folded = O.fold_layer(dims, w.wq, w.wk, w.wv, w.wo, xc)
+    x = Z.prompt(dims, 2, 1, prompt, seed=21)
+    m = O.OracleModel(dims, plan, [folded])
+    t0 = time.perf_counter()
+    m.prefill(x)
+    t1 = time.perf_counter()
+    for s in range(n_decode):
+        m.decode(Z.decode_input(dims, 2, 1, s))
+    t2 = time.perf_counter()
+    cores = len(os.sched_getaffinity(0))
+    try:
+        from threadpoolctl import threadpool_info
+        nthreads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+        cores = nthreads
+    except Exception:
+        pass
+    return t1 - t0, (t2 - t1) / n_decode, cores
+
+
+def oracle_step_tok_s(t_pre_layer, t_dec_layer, L, S, T, B=1):
+    step = L * t_pre_layer + L * T * t_dec_layer
+    return B * (S + T) / step, step
+
+
+# ------------------------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    L, S, T = args.layers, args.prompt, args.decode_steps
+    vals = []
+    for i in range(args.warmup + args.steps):
+        tp, td, cores = oracle_sample(n_decode=4, prompt=512 if i < args.warmup else S)
+        if i >= args.warmup:
+            vals.append((tp, td))
+    tp = statistics.median(v[0] for v in vals)
+    td = statistics.median(v[1] for v in vals)
+    v, step_s = oracle_step_tok_s(tp, td, L, S, T)
+    sample = "per step: 1 layer fp64 prefill of S=%d + 4 decode steps (oracle/), extrapolated x%d layers, %d decode steps" % (S, L, T)
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tok/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": CONFIG_NAME, "layers": L, "prompt": S, "decode_steps": T, "batch": 1, "rank": 64},
+           "cpu_baseline": {"value": v, "unit": "tok/s", "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": v, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------------------------ zdc arm
+def run_zdc(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2408_04107_b200 as zdc
+    import zdc_synth as Z
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    L, S, T, r = args.layers, args.prompt, args.decode_steps, args.rank
+    base = Z.dims_of(2)
+    dims = Z.Dims(L, base.d_model, base.n_heads, base.n_kv_heads, base.d_head)
+    d, nh, nkv, dh = dims.d_model, dims.n_heads, dims.n_kv_heads, dims.d_head
+    B = 1
+    plan = Z.plan_uniform(L, r)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    ctx = zdc.Context(dims, plan, B, S + T)
+
+    # Timing-only weights (SURVEY.md §8(d) "ideal fold" shortcut): folded weights W^R = W R with
+    # R = the generator's own basis, i.e. column j of W_Q^{R,h} is a * s_j * (orthonormal-like
+    # column); generated on the device with a seeded generator, same shapes/bytes as a real fold.
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    s = torch.tensor([10.0 ** (-2.0 * j / (dh - 1)) for j in range(dh)], device=dev)
+    a = (4.0 * dh / float((s ** 4).sum())) ** 0.25
+    bta = math.sqrt(dh / float((s ** 2).sum()))
+    gam = math.sqrt(dh / (nh * float((s ** 2).sum())))
+    for l in range(L):
+        wq = (torch.randn(d, nh, dh, device=dev, generator=g) * (a * s / math.sqrt(d))).reshape(d, nh * dh)
+        wk = (torch.randn(d, nkv, dh, device=dev, generator=g) * (a * s / math.sqrt(d))).reshape(d, nkv * dh)
+        wv = (torch.randn(d, nkv, dh, device=dev, generator=g) * (bta * s / math.sqrt(d))).reshape(d, nkv * dh)
+        wo = (torch.randn(nh, dh, d, device=dev, generator=g) * (gam * s[:, None] / math.sqrt(d))).reshape(nh * dh, d)
+        ctx.load_folded_device(l, *[t.to(torch.bfloat16).contiguous() for t in (wq, wk, wv, wo)])
+        del wq, wk, wv, wo
+    torch.cuda.synchronize()
+
+    x_prompt = torch.randn(B, S, d, device=dev, generator=g).to(torch.bfloat16)
+    x_dec = torch.randn(T, B, d, device=dev, generator=g).to(torch.bfloat16)
+    y = torch.empty(B, S, d, device=dev, dtype=torch.bfloat16)
+    x_buf = torch.empty(B, d, device=dev, dtype=torch.bfloat16)
+    y_dec = torch.empty(B, d, device=dev, dtype=torch.bfloat16)
+    y_all = torch.empty(T, B, d, device=dev, dtype=torch.bfloat16)
+
+    def eager_step():
+        ctx.reset()
+        for l in range(L):
+            ctx.prefill(x_prompt, y, l, l + 1)
+        for t in range(T):
+            x_buf.copy_(x_dec[t])
+            for l in range(L):
+                ctx.decode(x_buf, y_dec, l, l + 1)
+            y_all[t].copy_(y_dec)
+
+    # warm-up eagerly (kernel attributes, decode graphs of the library), then capture the step
+    eager_step()
+    torch.cuda.synchronize()
+    if args.profile_only:
+        eager_step()
+        torch.cuda.synchronize()
+        return
+
+    launches = {"prefill": 0, "decode": 0}
+    ctx.reset()
+    g_pre = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_pre, stream=stream):
+        for l in range(L):
+            ctx.prefill(x_prompt, y, l, l + 1)
+            launches["prefill"] += zdc.last_launch_count()
+    g_dec = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_dec, stream=stream):
+        for l in range(L):
+            ctx.decode(x_buf, y_dec, l, l + 1)
+            launches["decode"] += zdc.last_launch_count()
+    torch.cuda.synchronize()
+    kernels_per_step = launches["prefill"] + T * launches["decode"]
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+
+    def graph_step(times=None):
+        ctx.reset()  # lengths only (the prefill graph sets them to S); host bookkeeping
+        if times is not None:
+            ev[0].record(stream)
+        g_pre.replay()
+        if times is not None:
+            ev[1].record(stream)
+        for t in range(T):
+            x_buf.copy_(x_dec[t])
+            g_dec.replay()
+            y_all[t].copy_(y_dec)
+        if times is not None:
+            ev[2].record(stream)
+
+    for _ in range(args.warmup):
+        graph_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    pre_ms, dec_ms = [], []
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_start.record(stream)
+    for _ in range(args.steps):
+        graph_step(times=True)
+        # per-phase split from the last step's events (sync-free: read after the loop)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    pre_ms.append(ev[0].elapsed_time(ev[1]))
+    dec_ms.append(ev[1].elapsed_time(ev[2]))
+    clocks = clk.stop()
+    if world > 1:
+        tt = torch.tensor([total_ms, pre_ms[-1], dec_ms[-1]], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms, pre_ms[-1], dec_ms[-1] = [float(v) for v in tt]
+    ms_per_step = total_ms / args.steps
+    tok_per_step = B * (S + T)
+    value = world * tok_per_step * args.steps / (total_ms / 1e3)
+
+    # ---- per-kernel timing (eager, zdc_profile): one extra step after the timed region
+    zdc.profile(True)
+    eager_step()
+    prof = zdc.profile_read()
+    zdc.profile(False)
+    peaks = load_peaks()
+    Nqkv = nh * r + 2 * nkv * r
+    ko = ((nh * r + 63) // 64) * 64
+    avg_ctx = S + (T + 1) / 2.0
+    algo = {
+        # bytes: folded packed weights read once + x in + outputs
+        "a1_decode_gemv": ("hbm", Nqkv * d * 2 + B * d * 2 + B * Nqkv * 2),
+        "a5_decode_gemv": ("hbm", d * ko * 2 + B * ko * 2 + B * d * 2),
+        # K'/V' at the packed widths for the average context + q + partials
+        "a3_decode_attention": ("hbm", B * nkv * avg_ctx * (r + r) * 2 + B * nh * r * 2),
+        # flops
+        "a1_prefill_gemm": ("tensor", 2.0 * B * S * Nqkv * d),
+        "a5_prefill_gemm": ("tensor", 2.0 * B * S * d * nh * r),
+        "a3_prefill_attention": ("tensor", 4.0 * r * nh * B * S * (S + 1) / 2.0),
+    }
+    traffic_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
+    kernels = {}
+    for k, (ms, n) in prof.items():
+        if n == 0 or k not in algo:
+            continue
+        bound, work = algo[k]
+        avg_s = ms / n / 1e3
+        if bound == "hbm":
+            ach, peak, unit = work / avg_s / 1e9, peaks["hbm"], "GB/s"
+        else:
+            ach, peak, unit = work / avg_s / 1e12, peaks["tf_sus"], "TFLOP/s"
+        kernels[k] = {"bound": bound, "achieved": round(ach, 1), "peak": peak, "unit": unit,
+                      "frac": round(ach / peak, 4), "avg_us": round(avg_s * 1e6, 2), "launches": n,
+                      "share_of_step": None, "traffic": traffic.get(k)}
+    prof_total = sum(ms for ms, n in prof.values())
+    for k in kernels:
+        kernels[k]["share_of_step"] = round(prof[k][0] / prof_total, 4) if prof_total else None
+    dom = max(kernels, key=lambda k: prof[k][0])
+    roof = dict(kernels[dom])
+    roof["kernel"] = dom
+    roof.pop("share_of_step", None)
+
+    # ---- end to end through the public API with host buffers (pinned), copies inside the region
+    e2e = None
+    if not args.no_e2e:
+        hx = torch.empty(B, S, d, dtype=torch.bfloat16, pin_memory=True).copy_(x_prompt.cpu())
+        hxd = torch.empty(T, B, d, dtype=torch.bfloat16, pin_memory=True).copy_(x_dec.cpu())
+        hy = torch.empty(B, S, d, dtype=torch.bfloat16, pin_memory=True)
+        hyd = torch.empty(T, B, d, dtype=torch.bfloat16, pin_memory=True)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            x_prompt.copy_(hx, non_blocking=True)
+            x_dec.copy_(hxd, non_blocking=True)
+            graph_step()
+            hy.copy_(y, non_blocking=True)
+            hyd.copy_(y_all, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1)
+        if world > 1:
+            tt = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e_ms = float(tt[0])
+        bpe = 2
+        e2e = {"value": world * tok_per_step * args.steps / (e_ms / 1e3), "unit": "tok/s",
+               "h2d_bytes_per_step": (B * S * d + T * B * d) * bpe,
+               "d2h_bytes_per_step": (B * S * d + T * B * d) * bpe}
+
+    # ---- CPU baseline (oracle as it stands), rank 0 at N=1 only
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        tp, td, cores = oracle_sample(n_decode=16, prompt=S)
+        v, _ = oracle_step_tok_s(tp, td, L, S, T)
+        cpu = {"value": v, "unit": "tok/s", "cores": cores, "kind": "oracle",
+               "sample": "1 c2 layer fp64 prefill S=%d (%.2f s) + 16 decode steps (%.3f s/step), extrapolated to "
+                         "%d layers x (prefill + %d decode steps)" % (S, tp, td, L, T)}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": CONFIG_NAME, "layers": L, "d_model": d, "n_heads": nh, "n_kv_heads": nkv,
+                       "d_head": dh, "rank": r, "batch": B, "prompt": S, "decode_steps": T,
+                       "tokens_per_step_per_gpu": tok_per_step, "parallelism": "replicas%d" % world,
+                       "l2": "inputs larger than L2 (2.1 GB folded weights per step)",
+                       "timing": "CUDA graphs of per-layer zdc_prefill / zdc_decode calls"},
+            "prefill_tok_s": world * B * S / (pre_ms[-1] / 1e3),
+            "decode_tok_s": world * B * T / (dec_ms[-1] / 1e3),
+            "prefill_ms": pre_ms[-1], "decode_ms": dec_ms[-1],
+            "roofline": roof, "kernels": kernels, "peaks_source": peaks["src"],
+            "clocks": clocks, "gpu_launches": kernels_per_step * args.steps,
+            "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(out), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_zdc(args)
+
+
+if __name__ == "__main__":
+    main()

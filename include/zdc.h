@@ -101,8 +101,9 @@ zdc_status zdc_fold_weights(const zdc_dims* dims,
 
 /* ------------------------------------------------------------------------------------
  * Context: host metadata only.  Device memory is caller-owned: query the three sizes,
- * allocate (any allocator; 256-byte aligned), bind.  The cache region is zeroed by
- * zdc_ctx_bind / zdc_cache_reset.
+ * allocate (any allocator; 256-byte aligned), bind.  zdc_ctx_bind zeroes the regions;
+ * zdc_cache_reset empties the cache by resetting the per-layer lengths (host and device):
+ * no kernel reads a cache row at or beyond its layer's length.
  *
  * Supported shapes (else ZDC_ERR_UNSUPPORTED): d_model % 64 == 0; d_head <= 128;
  * n_heads % n_kv_heads == 0; every kept rank is stored zero-padded to a multiple of 16
@@ -207,6 +208,15 @@ zdc_status zdc_gemm_bf16(const uint16_t* a, const uint16_t* b, uint16_t* d,
 
 /* Number of kernels the last prefill / decode call enqueued (for bench.py's gpu_launches). */
 int64_t zdc_kernel_launch_count(void);
+
+/* Per-kernel-class device timing (bench.py's roofline): zdc_profile(1) brackets every launch
+ * with CUDA events on its stream (zdc_decode then runs eagerly instead of replaying its CUDA
+ * graph); zdc_profile_read synchronises, writes per class the summed milliseconds and launch
+ * counts since the previous read, clears them, and returns the number of classes:
+ * 0 a1 prefill GEMM, 1 a3 prefill attention, 2 a5 prefill GEMM, 3 a1 decode GEMV,
+ * 4 a3 decode attention (partial), 5 a3 decode combine, 6 a5 decode GEMV, 7 other. */
+void zdc_profile(int enable);
+int zdc_profile_read(float* ms, int64_t* count, int n);
 
 #ifdef __cplusplus
 }

@@ -29,7 +29,7 @@ EXPORTED_SYMBOLS = ["zdc_last_error", "zdc_version", "zdc_fold_weights", "zdc_ct
                     "zdc_ctx_bind", "zdc_ctx_destroy", "zdc_load_folded", "zdc_load_folded_device",
                     "zdc_prefill", "zdc_decode", "zdc_comm_init", "zdc_sp_prefill", "zdc_sp_positions",
                     "zdc_cache_export", "zdc_cache_length", "zdc_cache_reset", "zdc_last_lse",
-                    "zdc_gemm_bf16", "zdc_kernel_launch_count"]
+                    "zdc_gemm_bf16", "zdc_kernel_launch_count", "zdc_profile", "zdc_profile_read"]
 
 
 class ZdcError(RuntimeError):
@@ -89,6 +89,8 @@ def lib():
             "zdc_last_lse": ([P, I32, P, P], I32),
             "zdc_gemm_bf16": ([P, P, P, I32, I32, I32, P], I32),
             "zdc_kernel_launch_count": ([], I64),
+            "zdc_profile": ([ctypes.c_int], None),
+            "zdc_profile_read": ([ctypes.POINTER(F), ctypes.POINTER(I64), ctypes.c_int], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -106,6 +108,24 @@ def _check(status: int, fn: str):
 
 def last_launch_count() -> int:
     return int(lib().zdc_kernel_launch_count())
+
+
+PROFILE_CLASSES = ["a1_prefill_gemm", "a3_prefill_attention", "a5_prefill_gemm", "a1_decode_gemv",
+                   "a3_decode_attention", "a3_decode_combine", "a5_decode_gemv", "other"]
+
+
+def profile(enable: bool):
+    """Per-kernel-class CUDA-event timing inside the library (zdc_profile)."""
+    lib().zdc_profile(1 if enable else 0)
+
+
+def profile_read():
+    """{class: (ms_total, launches)} since the previous read (synchronises)."""
+    n = len(PROFILE_CLASSES)
+    ms = (ctypes.c_float * n)()
+    cnt = (ctypes.c_int64 * n)()
+    lib().zdc_profile_read(ms, cnt, n)
+    return {PROFILE_CLASSES[i]: (float(ms[i]), int(cnt[i])) for i in range(n)}
 
 
 def _dptr(a: np.ndarray):

@@ -60,6 +60,12 @@ static zdc_status check_sticky() {
   return ZDC_OK;
 }
 
+void graphs_destroy(zdc_ctx* c) {
+  for (auto& kv : c->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  c->graphs.clear();
+}
+
 }  // namespace zdc
 
 using namespace zdc;
@@ -169,6 +175,8 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
     if (L.ko_p > max_ko) max_ko = L.ko_p;
     if (L.rv_p > max_rv) max_rv = L.rv_p;
   }
+  c->len_dev_off = coff;
+  coff = align_up(coff + static_cast<int64_t>(d.n_layers) * 4, 256);
   if (any_split) {
     delete c;
     return fail(ZDC_ERR_UNSUPPORTED, "token-level split (g_bp < 10000) is not implemented in this build");
@@ -205,6 +213,7 @@ zdc_status zdc_ctx_bind(zdc_ctx* c, void* w, void* cache, void* scratch) {
   if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(cache) | reinterpret_cast<uintptr_t>(scratch)) &
       255)
     return fail(ZDC_ERR_INVALID_ARG, "zdc_ctx_bind: buffers must be 256-byte aligned");
+  graphs_destroy(c);
   c->w = static_cast<uint8_t*>(w);
   c->cache = static_cast<uint8_t*>(cache);
   c->scratch = static_cast<uint8_t*>(scratch);
@@ -219,6 +228,7 @@ zdc_status zdc_ctx_bind(zdc_ctx* c, void* w, void* cache, void* scratch) {
 void zdc_ctx_destroy(zdc_ctx* c) {
   if (!c) return;
   comm_destroy(c);
+  graphs_destroy(c);
   delete c;
 }
 
@@ -341,6 +351,7 @@ zdc_status zdc_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, ui
     Epilogue e1;
     e1.mode = 1;
     e1.qkv = qkv_dest(c, L, S, 0, nullptr);
+    g_prof_class = kProfGemmQkv;
     ZDC_CUDA_TRY(launch_gemm(xin, d, reinterpret_cast<const uint16_t*>(c->w + L.w_qkv), d, M, L.n_qkv, d, e1, s));
     // a3: causal attention at head dim r, O' and LSE
     PrefillAttnArgs a;
@@ -368,13 +379,72 @@ zdc_status zdc_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, ui
     e5.mode = 0;
     e5.d = y;
     e5.ldd = d;
+    g_prof_class = kProfGemmO;
     ZDC_CUDA_TRY(launch_gemm(a.o, L.ko_p, reinterpret_cast<const uint16_t*>(c->w + L.w_o), L.ko_p, M, d, L.ko_p, e5,
                              s));
+    g_prof_class = kProfOther;
+    ZDC_CUDA_TRY(launch_set_int(c->len_dev() + l, S, s));
     c->len[l] = S;
     c->last_layer = l;
     c->last_T = S;
   }
   c->batch = B;
+  return ZDC_OK;
+}
+
+static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, uint16_t* y, int B,
+                                 cudaStream_t s) {
+  const int d = c->dims.d_model, Nh = c->dims.n_heads, Nkv = c->dims.n_kv_heads;
+  for (int l = l0; l < l1; ++l) {
+    const LayerInfo& L = c->layers[l];
+    const uint16_t* xin = l == l0 ? x : y;
+    int* len_dev = c->len_dev() + l;  // tokens in the cache before this step
+    // a1 + a2: the new token's Q' to staging, K'/V' into the cache at position *len_dev
+    Epilogue e1;
+    e1.mode = 1;
+    e1.qkv = qkv_dest(c, L, 1, 0, nullptr);
+    e1.qkv.pos_ptr = len_dev;
+    const uint16_t* wqkv = reinterpret_cast<const uint16_t*>(c->w + L.w_qkv);
+    const uint16_t* wo = reinterpret_cast<const uint16_t*>(c->w + L.w_o);
+    g_prof_class = kProfGemvQkv;
+    if (B <= 8)
+      ZDC_CUDA_TRY(launch_gemv(wqkv, xin, d, B, L.n_qkv, d, e1, s));
+    else
+      ZDC_CUDA_TRY(launch_gemm(xin, d, wqkv, d, B, L.n_qkv, d, e1, s));
+    // a3: split-K attention over the *len_dev + 1 cached keys
+    DecodeAttnArgs a;
+    a.q = reinterpret_cast<const uint16_t*>(c->scratch + c->s_q);
+    a.ldq = L.nq;
+    a.k = reinterpret_cast<const uint16_t*>(c->cache + L.k_off);
+    a.v = reinterpret_cast<const uint16_t*>(c->cache + L.v_off);
+    a.S_cap = c->max_seq;
+    a.len = c->max_seq;  // upper bound (fixes the split count, so the graph is length-independent)
+    a.len_ptr = len_dev;
+    a.o = reinterpret_cast<uint16_t*>(c->scratch + c->s_o);
+    a.ldo = L.ko_p;
+    a.lse = reinterpret_cast<float*>(c->scratch + c->s_lse);
+    a.part = reinterpret_cast<float*>(c->scratch + c->s_part);
+    a.B = B;
+    a.Nh = Nh;
+    a.Nkv = Nkv;
+    a.rk = L.rk_p;
+    a.rv = L.rv_p;
+    a.scale = 1.0f / std::sqrt(static_cast<float>(c->dims.d_head));
+    a.splits = decode_splits(B, Nkv, c->max_seq);
+    ZDC_CUDA_TRY(launch_decode_attention(a, s));
+    // a5: y = O' W_O^R; this kernel also advances *len_dev (all readers of it have run)
+    Epilogue e5;
+    e5.mode = 0;
+    e5.d = y;
+    e5.ldd = d;
+    e5.len_inc = len_dev;
+    g_prof_class = kProfGemvO;
+    if (B <= 8)
+      ZDC_CUDA_TRY(launch_gemv(wo, a.o, L.ko_p, B, d, L.ko_p, e5, s));
+    else
+      ZDC_CUDA_TRY(launch_gemm(a.o, L.ko_p, wo, L.ko_p, B, d, L.ko_p, e5, s));
+    g_prof_class = kProfOther;
+  }
   return ZDC_OK;
 }
 
@@ -388,51 +458,42 @@ zdc_status zdc_decode(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, uin
       return fail(ZDC_ERR_CAPACITY, "zdc_decode: layer %d len %d + 1 > max_seq %d", l, c->len[l], c->max_seq);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   g_launches = 0;
-  const int d = c->dims.d_model, Nh = c->dims.n_heads, Nkv = c->dims.n_kv_heads;
-  for (int l = l0; l < l1; ++l) {
-    const LayerInfo& L = c->layers[l];
-    const uint16_t* xin = l == l0 ? x : y;
-    const int pos = c->len[l];
-    Epilogue e1;
-    e1.mode = 1;
-    e1.qkv = qkv_dest(c, L, 1, pos, nullptr);
-    const uint16_t* wqkv = reinterpret_cast<const uint16_t*>(c->w + L.w_qkv);
-    const uint16_t* wo = reinterpret_cast<const uint16_t*>(c->w + L.w_o);
-    if (B <= 8)
-      ZDC_CUDA_TRY(launch_gemv(wqkv, xin, d, B, L.n_qkv, d, e1, s));
-    else
-      ZDC_CUDA_TRY(launch_gemm(xin, d, wqkv, d, B, L.n_qkv, d, e1, s));
-    DecodeAttnArgs a;
-    a.q = reinterpret_cast<const uint16_t*>(c->scratch + c->s_q);
-    a.ldq = L.nq;
-    a.k = reinterpret_cast<const uint16_t*>(c->cache + L.k_off);
-    a.v = reinterpret_cast<const uint16_t*>(c->cache + L.v_off);
-    a.S_cap = c->max_seq;
-    a.len = pos + 1;
-    a.o = reinterpret_cast<uint16_t*>(c->scratch + c->s_o);
-    a.ldo = L.ko_p;
-    a.lse = reinterpret_cast<float*>(c->scratch + c->s_lse);
-    a.part = reinterpret_cast<float*>(c->scratch + c->s_part);
-    a.B = B;
-    a.Nh = Nh;
-    a.Nkv = Nkv;
-    a.rk = L.rk_p;
-    a.rv = L.rv_p;
-    a.scale = 1.0f / std::sqrt(static_cast<float>(c->dims.d_head));
-    a.splits = decode_splits(B, Nkv, a.len);
-    ZDC_CUDA_TRY(launch_decode_attention(a, s));
-    Epilogue e5;
-    e5.mode = 0;
-    e5.d = y;
-    e5.ldd = d;
-    if (B <= 8)
-      ZDC_CUDA_TRY(launch_gemv(wo, a.o, L.ko_p, B, d, L.ko_p, e5, s));
-    else
-      ZDC_CUDA_TRY(launch_gemm(a.o, L.ko_p, wo, L.ko_p, B, d, L.ko_p, e5, s));
-    c->len[l] = pos + 1;
-    c->last_layer = l;
-    c->last_T = 1;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (s) ZDC_CUDA_TRY(cudaStreamIsCapturing(s, &cap));
+  const bool graph = c->use_graphs && !prof_enabled() && s != nullptr && s != cudaStreamPerThread &&
+                     cap == cudaStreamCaptureStatusNone;
+  if (graph) {
+    // The whole [l0, l1) decode step is one CUDA graph, replayed every step: lengths live on the
+    // device, so the same graph serves every position.
+    auto key = std::make_tuple(static_cast<int>(l0), static_cast<int>(l1), static_cast<int>(B),
+                               static_cast<const void*>(x), static_cast<void*>(y), s);
+    auto it = c->graphs.find(key);
+    if (it == c->graphs.end()) {
+      cudaGraph_t gr = nullptr;
+      ZDC_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      zdc_status est = enqueue_decode(c, l0, l1, x, y, B, s);
+      cudaError_t ce = cudaStreamEndCapture(s, &gr);
+      if (est != ZDC_OK) {
+        if (gr) cudaGraphDestroy(gr);
+        return est;
+      }
+      if (ce != cudaSuccess) return fail(ZDC_ERR_CUDA, "zdc_decode: capture failed: %s", cudaGetErrorString(ce));
+      zdc_ctx::GraphEntry ent;
+      ce = cudaGraphInstantiate(&ent.exec, gr, 0);
+      cudaGraphDestroy(gr);
+      if (ce != cudaSuccess) return fail(ZDC_ERR_CUDA, "zdc_decode: instantiate: %s", cudaGetErrorString(ce));
+      ent.kernels = g_launches;
+      it = c->graphs.emplace(key, ent).first;
+    }
+    ZDC_CUDA_TRY(cudaGraphLaunch(it->second.exec, s));
+    g_launches = it->second.kernels;
+  } else {
+    st = enqueue_decode(c, l0, l1, x, y, B, s);
+    if (st != ZDC_OK) return st;
   }
+  for (int l = l0; l < l1; ++l) c->len[l] += 1;
+  c->last_layer = l1 - 1;
+  c->last_T = 1;
   c->batch = B;
   return ZDC_OK;
 }
@@ -448,7 +509,9 @@ zdc_status zdc_cache_length(const zdc_ctx* c, int32_t layer, int32_t* len) {
 zdc_status zdc_cache_reset(zdc_ctx* c, void* stream) {
   if (!c) return fail(ZDC_ERR_INVALID_ARG, "zdc_cache_reset: null ctx");
   if (!c->cache) return fail(ZDC_ERR_STATE, "zdc_cache_reset: ctx not bound");
-  ZDC_CUDA_TRY(cudaMemsetAsync(c->cache, 0, c->cache_bytes, static_cast<cudaStream_t>(stream)));
+  // Only the lengths are reset: no kernel ever reads a cache row at or beyond its layer's length.
+  ZDC_CUDA_TRY(cudaMemsetAsync(c->len_dev(), 0, static_cast<size_t>(c->dims.n_layers) * 4,
+                               static_cast<cudaStream_t>(stream)));
   c->len.assign(c->dims.n_layers, 0);
   c->batch = 0;
   return ZDC_OK;

@@ -294,7 +294,9 @@ static cudaError_t launch_attn_t(const PrefillAttnArgs& a, cudaStream_t stream) 
   if (!make_tmap_2d(&tk, a.k, HD, kv_rows, HD * 2, C::CW, C::BN, C::SWB)) return cudaErrorInvalidValue;
   if (!make_tmap_2d(&tv, a.v, HD, kv_rows, HD * 2, C::CW, C::BN, C::SWB)) return cudaErrorInvalidValue;
   dim3 grid((a.n_q + C::BM - 1) / C::BM, a.Nh, a.B);
+  prof_mark(stream, true, kProfAttnPrefill);
   prefill_attn_kernel<HD><<<grid, 192, C::SMEM, stream>>>(tq, tk, tv, a);
+  prof_mark(stream, false, kProfAttnPrefill);
   ++g_launches;
   return cudaGetLastError();
 }

@@ -2,7 +2,11 @@
 #pragma once
 #include <stdint.h>
 
+#include <map>
+#include <tuple>
 #include <vector>
+
+#include <cuda_runtime.h>
 
 #include "zdc.h"
 
@@ -40,8 +44,18 @@ struct zdc_ctx {
   int batch = 0;
   int last_layer = -1, last_T = 0;
   zdc::CommState* comm = nullptr;
+  int64_t len_dev_off = 0;  // int32 [n_layers] device-side cache lengths (in the cache region)
+  // zdc_decode CUDA graphs, keyed by (l0, l1, B, x, y, stream)
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    int64_t kernels = 0;
+  };
+  std::map<std::tuple<int, int, int, const void*, void*, cudaStream_t>, GraphEntry> graphs;
+  bool use_graphs = true;
+  int* len_dev() { return reinterpret_cast<int*>(cache + len_dev_off); }
 };
 
 namespace zdc {
 void comm_destroy(zdc_ctx* c);
+void graphs_destroy(zdc_ctx* c);
 }

@@ -54,7 +54,7 @@ __device__ __forceinline__ void store_scalar(const Epilogue& e, int m, int n, ui
       dst = q.q + static_cast<int64_t>(m) * q.ldq + n;
     } else {
       const int b = m / q.S, t = m - b * q.S;
-      const int pos = q.posmap ? q.posmap[t] : q.pos0 + t;
+      const int pos = q.posmap ? q.posmap[t] : (q.pos_ptr ? *q.pos_ptr : q.pos0) + t;
       if (n < q.nq + q.nk) {
         const int nn = n - q.nq, g = nn / q.rk, c = nn - g * q.rk;
         dst = q.k + b * q.kb + g * q.kg + static_cast<int64_t>(pos) * q.rk + c;
@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(256) gemv_kernel(const uint16_t* __restrict__ 
                                                    int64_t ldx, int N, int K, const Epilogue epi) {
   extern __shared__ uint4 xs[];  // [NB][K/8] bf16 units
   const int kc = K >> 3;
+  if (epi.len_inc && blockIdx.x == 0 && threadIdx.x == 0) *epi.len_inc += 1;
   for (int i = threadIdx.x; i < NB * kc; i += blockDim.x) {
     const int b = i / kc, c = i - b * kc;
     xs[i] = *reinterpret_cast<const uint4*>(x + b * ldx + c * 8);
@@ -131,7 +132,9 @@ static cudaError_t launch_gemv_nb(const uint16_t* W, const uint16_t* x, int64_t 
   int blocks = (N + 7) / 8;
   const int cap = num_sms() * 8;
   if (blocks > cap) blocks = cap;
+  prof_mark(stream, true, g_prof_class);
   gemv_kernel<NB><<<blocks, 256, smem, stream>>>(W, x, ldx, N, K, epi);
+  prof_mark(stream, false, g_prof_class);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -165,9 +168,10 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
   __shared__ float stat[2][4][G];
   const int split = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int chunk = (a.len + a.splits - 1) / a.splits;
+  const int len = a.len_ptr ? *a.len_ptr + 1 : a.len;
+  const int chunk = (len + a.splits - 1) / a.splits;
   const int s0 = split * chunk;
-  const int s1 = min(a.len, s0 + chunk);
+  const int s1 = min(len, s0 + chunk);
   const int n = max(0, s1 - s0);
   const float scl = a.scale * kLog2e;
   const int64_t row0 = (static_cast<int64_t>(b) * a.Nkv + g) * a.S_cap;
@@ -320,8 +324,12 @@ int decode_splits(int B, int Nkv, int len) {
 template <int RK, int RV, int G>
 static cudaError_t launch_decode_t(const DecodeAttnArgs& a, cudaStream_t stream) {
   dim3 grid(a.splits, a.Nkv, a.B);
+  prof_mark(stream, true, kProfAttnDecode);
   decode_attn_partial<RK, RV, G><<<grid, 128, 0, stream>>>(a);
+  prof_mark(stream, false, kProfAttnDecode);
+  prof_mark(stream, true, kProfAttnCombine);
   decode_attn_combine<RV><<<dim3(a.Nh, a.B), 128, 0, stream>>>(a);
+  prof_mark(stream, false, kProfAttnCombine);
   g_launches += 2;
   return cudaGetLastError();
 }
@@ -339,6 +347,7 @@ static cudaError_t launch_decode_g(const DecodeAttnArgs& a, cudaStream_t stream)
 }
 
 cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t stream) {
+  // a.len is the largest length this launch (or graph replay) may see
   if (a.splits > 64 || (a.len + a.splits - 1) / a.splits > kMaxChunk) return cudaErrorInvalidValue;
   if (a.rk != a.rv) return cudaErrorInvalidValue;
   switch (a.rk) {

@@ -15,10 +15,54 @@
 #include "kernels.h"
 
 #include <mutex>
+#include <utility>
+#include <vector>
 
 namespace zdc {
 
 int64_t g_launches = 0;
+int g_prof_class = kProfOther;
+
+// ------------------------------------------------------------------ host: per-class event timing
+struct ProfState {
+  bool on = false;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+  cudaEvent_t pending = nullptr;
+  std::vector<cudaEvent_t> pool;
+};
+static ProfState g_prof;
+
+bool prof_enabled() { return g_prof.on; }
+
+static cudaEvent_t prof_event() {
+  if (!g_prof.pool.empty()) {
+    cudaEvent_t e = g_prof.pool.back();
+    g_prof.pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void prof_mark(cudaStream_t s, bool begin, int cls) {
+  if (!g_prof.on) return;
+  cudaEvent_t e = prof_event();
+  cudaEventRecord(e, s);
+  if (begin) {
+    g_prof.pending = e;
+  } else {
+    g_prof.marks.push_back({cls, {g_prof.pending, e}});
+    g_prof.pending = nullptr;
+  }
+}
+
+__global__ void set_int_kernel(int* p, int v) { *p = v; }
+cudaError_t launch_set_int(int* p, int v, cudaStream_t s) {
+  set_int_kernel<<<1, 1, 0, s>>>(p, v);
+  ++g_launches;
+  return cudaGetLastError();
+}
 
 // ------------------------------------------------------------------ host: tensor maps
 typedef CUresult (*PFN_tmapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -80,7 +124,7 @@ __device__ __forceinline__ void store_unit(const Epilogue& e, int m, int n, uint
       dst = q.q + static_cast<int64_t>(m) * q.ldq + n;
     } else {
       const int b = m / q.S, t = m - (m / q.S) * q.S;
-      const int pos = q.posmap ? q.posmap[t] : q.pos0 + t;
+      const int pos = q.posmap ? q.posmap[t] : (q.pos_ptr ? *q.pos_ptr : q.pos0) + t;
       if (n < q.nq + q.nk) {
         const int nn = n - q.nq, g = nn / q.rk, c = nn - g * q.rk;
         dst = q.k + b * q.kb + g * q.kg + static_cast<int64_t>(pos) * q.rk + c;
@@ -123,6 +167,7 @@ __global__ void __launch_bounds__(256, 1)
   const int num_tiles = m_tiles * n_tiles;
   const int k_blocks = K / C::BK;
   const uint32_t warp = warp_id(), lane = lane_id();
+  if (epi.len_inc && blockIdx.x == 0 && threadIdx.x == 0) *epi.len_inc += 1;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tma_a);
@@ -253,7 +298,9 @@ static cudaError_t launch_gemm_bn(const CUtensorMap& ta, const CUtensorMap& tb, 
   }
   const int tiles = ((M + C::BM - 1) / C::BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
+  prof_mark(stream, true, g_prof_class);
   gemm_bf16_tc_kernel<BN><<<grid, 256, C::SMEM, stream>>>(ta, tb, M, N, K, epi);
+  prof_mark(stream, false, g_prof_class);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -271,3 +318,30 @@ cudaError_t launch_gemm(const uint16_t* A, int64_t lda, const uint16_t* B, int64
 }
 
 }  // namespace zdc
+
+extern "C" {
+// zdc_profile(1) starts per-kernel-class event timing (eager launches only: zdc_decode bypasses
+// its CUDA graphs while profiling); zdc_profile_read synchronises and returns, per class, the
+// summed milliseconds and launch counts since the last read, then clears them.
+void zdc_profile(int enable) { zdc::g_prof.on = enable != 0; }
+int zdc_profile_read(float* ms, int64_t* count, int n) {
+  using namespace zdc;
+  for (int i = 0; i < n; ++i) {
+    if (ms) ms[i] = 0.f;
+    if (count) count[i] = 0;
+  }
+  for (auto& m : g_prof.marks) {
+    cudaEventSynchronize(m.second.second);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, m.second.first, m.second.second);
+    if (m.first < n) {
+      if (ms) ms[m.first] += t;
+      if (count) count[m.first] += 1;
+    }
+    g_prof.pool.push_back(m.second.first);
+    g_prof.pool.push_back(m.second.second);
+  }
+  g_prof.marks.clear();
+  return kProfClasses;
+}
+}

@@ -21,6 +21,7 @@ struct QkvDest {
   int S = 1;
   int64_t kb = 0, kg = 0, vb = 0, vg = 0;  // element strides per sequence / per KV head
   int pos0 = 0;
+  const int* pos_ptr = nullptr;  // if set, pos0 is read from device memory (graph-replayable decode)
   const int* posmap = nullptr;
 };
 
@@ -29,6 +30,7 @@ struct Epilogue {
   uint16_t* d = nullptr;
   int64_t ldd = 0;
   QkvDest qkv;
+  int* len_inc = nullptr;  // if set, the kernel increments *len_inc once (decode: advances the layer length)
 };
 
 // ---- tensor maps (driver entry point resolved at runtime; no -lcuda link)
@@ -70,7 +72,8 @@ struct DecodeAttnArgs {
   const uint16_t* k;   // cache, same addressing as PrefillAttnArgs
   const uint16_t* v;
   int S_cap;
-  int len;             // keys visible: positions [0, len)
+  int len;             // keys visible: positions [0, len) ...
+  const int* len_ptr;  // ... or [0, *len_ptr + 1) when set (device-side length, graph-replayable)
   uint16_t* o;         // O' [B][ldo]
   int64_t ldo;
   float* lse;          // [B][Nh]
@@ -89,5 +92,13 @@ cudaError_t launch_pack_weights_bf16(const uint16_t* wq, const uint16_t* wk, con
                                      cudaStream_t stream);
 
 extern int64_t g_launches;  // kernels enqueued by the last API call
+
+// ---- per-kernel-class timing (zdc_profile): CUDA events bracket each launch on its stream
+enum ProfClass { kProfGemmQkv = 0, kProfAttnPrefill, kProfGemmO, kProfGemvQkv, kProfAttnDecode, kProfAttnCombine,
+                 kProfGemvO, kProfOther, kProfClasses };
+extern int g_prof_class;  // class the next launches belong to (set by the orchestration)
+void prof_mark(cudaStream_t s, bool begin, int cls);
+bool prof_enabled();
+cudaError_t launch_set_int(int* p, int v, cudaStream_t s);
 
 }  // namespace zdc
