@@ -106,9 +106,9 @@ zdc_status zdc_fold_weights(const zdc_dims* dims,
  * no kernel reads a cache row at or beyond its layer's length.
  *
  * Supported shapes (else ZDC_ERR_UNSUPPORTED): d_model % 64 == 0; d_head <= 128;
- * n_heads % n_kv_heads == 0; every kept rank is stored zero-padded to a multiple of 16
- * (zero columns are exact: they add 0 to every dot product); padded ranks in
- * {16, 32, 64, 128} for the tcgen05 attention tiles.
+ * n_heads % n_kv_heads in {1,2,4,8} groups; every kept rank is stored zero-padded to a
+ * multiple of 16 (zero columns are exact: they add 0 to every dot product); the padded
+ * QK and VL ranks of a class must be equal (r_qk_imp ~ r_vl_imp, r_qk_unimp ~ r_vl_unimp).
  * ---------------------------------------------------------------------------------- */
 typedef struct zdc_ctx zdc_ctx;
 

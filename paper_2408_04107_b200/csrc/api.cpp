@@ -143,11 +143,10 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
     L.rv_p = pad16(L.rv);
     L.rku_p = pad16(L.rku);
     L.rvu_p = pad16(L.rvu);
-    auto ok_w = [](int r) { return r == 16 || r == 32 || r == 64 || r == 128; };
-    if (!ok_w(L.rk_p) || L.rk_p != L.rv_p) {
+    if (L.rk_p != L.rv_p || L.rku_p != L.rvu_p) {
       delete c;
-      return fail(ZDC_ERR_UNSUPPORTED, "layer %d: padded ranks r_k=%d r_v=%d must be equal and in {16,32,64,128}", l,
-                  L.rk_p, L.rv_p);
+      return fail(ZDC_ERR_UNSUPPORTED, "layer %d: padded ranks must satisfy r_qk == r_vl (imp %d/%d, unimp %d/%d)", l,
+                  L.rk_p, L.rv_p, L.rku_p, L.rvu_p);
     }
     L.nq = d.n_heads * L.rk_p;
     L.nk = d.n_kv_heads * L.rk_p;
@@ -192,7 +191,7 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
   c->s_lse = s;
   s = align_up(s + rows * d.n_heads * 4, 256);
   c->s_part = s;
-  s = align_up(s + static_cast<int64_t>(max_batch) * d.n_heads * 64 * (max_rv + 2) * 4, 256);
+  s = align_up(s + static_cast<int64_t>(max_batch) * d.n_heads * 128 * (max_rv + 2) * 4, 256);
   c->ldq = max_nq;
   c->ldo = max_ko;
   c->scratch_bytes = s;

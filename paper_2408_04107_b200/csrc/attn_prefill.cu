@@ -24,7 +24,7 @@ static constexpr float kLn2F = 0.6931471805599453f;
 template <int HD>
 struct AttnCfg {
   static constexpr int BM = 128, BN = 128;                 // query rows / keys per tile
-  static constexpr int CW = HD < 64 ? HD : 64;             // elements per swizzle chunk row
+  static constexpr int CW = HD % 64 == 0 ? 64 : HD % 32 == 0 ? 32 : 16;  // elements per swizzle chunk row
   static constexpr int NCH = HD / CW;                      // chunks across the head dim
   static constexpr int SWB = CW * 2;                       // swizzle width in bytes (32/64/128)
   static constexpr uint32_t LAYOUT = SWB == 128 ? kSw128 : SWB == 64 ? kSw64 : kSw32;
@@ -306,7 +306,11 @@ cudaError_t launch_prefill_attention(const PrefillAttnArgs& a, cudaStream_t stre
   switch (a.rk) {
     case 16: return launch_attn_t<16>(a, stream);
     case 32: return launch_attn_t<32>(a, stream);
+    case 48: return launch_attn_t<48>(a, stream);
     case 64: return launch_attn_t<64>(a, stream);
+    case 80: return launch_attn_t<80>(a, stream);
+    case 96: return launch_attn_t<96>(a, stream);
+    case 112: return launch_attn_t<112>(a, stream);
     case 128: return launch_attn_t<128>(a, stream);
     default: return cudaErrorInvalidValue;
   }

@@ -159,16 +159,28 @@ cudaError_t launch_gemv(const uint16_t* W, const uint16_t* x, int64_t ldx, int B
 static constexpr int kMaxChunk = 512;
 static constexpr float kLog2e = 1.4426950408889634f;
 
+__host__ __device__ constexpr int pow2_at_least(int x) { return x <= 1 ? 1 : x <= 2 ? 2 : x <= 4 ? 4 : x <= 8 ? 8 : 16; }
+
+// One CTA per (chunk, KV head, sequence) of ONE pool (pool 0 = important / uniform rows at
+// width RK/RV, pool 1 = unimportant rows at their truncated width; the query is used at the
+// pool's width, which is exact because the truncated dims of pool-1 keys are zero, P:776 DEL).
+// Writes an unnormalised partial (o[0..RVO), m, l) to slot `slot0 + chunk`; o[c] = 0 for c >= RV.
 template <int RK, int RV, int G>
-__global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs a) {
-  constexpr int UK = RK / 8, RPW = 32 / UK;   // lanes per K' row, rows per warp step
-  constexpr int UV = RV / 8, RPWV = 32 / UV;  // lanes per V' row, rows per warp step
+__global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs a, const uint16_t* __restrict__ kp,
+                                                           const uint16_t* __restrict__ vp, int pool, int slot0,
+                                                           int nslots) {
+  constexpr int UK = RK / 8, UKP = pow2_at_least(UK), RPW = 32 / UKP;   // lanes per K' row (padded)
+  constexpr int UV = RV / 8, UVP = pow2_at_least(UV), RPWV = 32 / UVP;  // lanes per V' row (padded)
   __shared__ float sc[G][kMaxChunk];
   __shared__ float red[4][G][RV];
   __shared__ float stat[2][4][G];
   const int split = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int len = a.len_ptr ? *a.len_ptr + 1 : a.len;
+  int len;
+  if (pool == 0)
+    len = a.n0_ptr ? a.n0_ptr[b] : (a.len_ptr ? *a.len_ptr + 1 : a.len);
+  else
+    len = a.n1_ptr[b];
   const int chunk = (len + a.splits - 1) / a.splits;
   const int s0 = split * chunk;
   const int s1 = min(len, s0 + chunk);
@@ -178,18 +190,20 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
 
   // ---- scores s = q . k * scale * log2(e), all G heads of the group per K' row load
   {
-    const int sub = lane / UK, u = lane % UK;
+    const int sub = lane / UKP, u = lane % UKP;
+    const bool lane_on = sub < RPW && u < UK;
     float qf[G][8];
 #pragma unroll
     for (int gi = 0; gi < G; ++gi) {
-      const uint4 qv = *reinterpret_cast<const uint4*>(a.q + b * a.ldq + (g * G + gi) * RK + u * 8);
+      uint4 qv = make_uint4(0, 0, 0, 0);
+      if (lane_on) qv = *reinterpret_cast<const uint4*>(a.q + b * a.ldq + (g * G + gi) * a.rk + u * 8);
       bf16x8_to_f32(qv, qf[gi]);
     }
 #pragma unroll 4
     for (int jb = warp * RPW; jb < n; jb += 4 * RPW) {  // warp-uniform trip count (shuffles inside)
       const int j = jb + sub;
-      const bool valid = j < n;
-      const uint4 kv = valid ? ldg_stream(a.k + (row0 + s0 + j) * RK + u * 8) : make_uint4(0, 0, 0, 0);
+      const bool valid = lane_on && j < n;
+      const uint4 kv = valid ? ldg_stream(kp + (row0 + s0 + j) * RK + u * 8) : make_uint4(0, 0, 0, 0);
       float kf[8];
       bf16x8_to_f32(kv, kf);
 #pragma unroll
@@ -198,7 +212,7 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
 #pragma unroll
         for (int e = 0; e < 8; ++e) p = fmaf(qf[gi][e], kf[e], p);
 #pragma unroll
-        for (int off = UK / 2; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
+        for (int off = UKP / 2; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
         if (u == 0 && valid) sc[gi][j] = p * scl;
       }
     }
@@ -233,22 +247,26 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
   for (int gi = 0; gi < G; ++gi) ls[gi] = stat[1][0][gi] + stat[1][1][gi] + stat[1][2][gi] + stat[1][3][gi];
   // ---- o = sum_j p_j V'_j  (unnormalised, relative to the chunk max)
   {
-    const int sub = lane / UV, u = lane % UV;
+    const int sub = lane / UVP, u = lane % UVP;
+    const bool lane_on = sub < RPWV && u < UV;
     float acc[G][8];
 #pragma unroll
     for (int gi = 0; gi < G; ++gi)
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[gi][e] = 0.f;
 #pragma unroll 4
-    for (int j = warp * RPWV + sub; j < n; j += 4 * RPWV) {
-      const uint4 vv = ldg_stream(a.v + (row0 + s0 + j) * RV + u * 8);
-      float vf[8];
-      bf16x8_to_f32(vv, vf);
+    for (int jb = warp * RPWV; jb < n; jb += 4 * RPWV) {
+      const int j = jb + sub;
+      if (lane_on && j < n) {
+        const uint4 vv = ldg_stream(vp + (row0 + s0 + j) * RV + u * 8);
+        float vf[8];
+        bf16x8_to_f32(vv, vf);
 #pragma unroll
-      for (int gi = 0; gi < G; ++gi) {
-        const float p = sc[gi][j];
+        for (int gi = 0; gi < G; ++gi) {
+          const float p = sc[gi][j];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) acc[gi][e] = fmaf(p, vf[e], acc[gi][e]);
+          for (int e = 0; e < 8; ++e) acc[gi][e] = fmaf(p, vf[e], acc[gi][e]);
+        }
       }
     }
 #pragma unroll
@@ -257,10 +275,10 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
       for (int e = 0; e < 8; ++e) {
         float v = acc[gi][e];
 #pragma unroll
-        for (int off = UV; off < 32; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        for (int off = UVP; off < 32; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
         acc[gi][e] = v;
       }
-    if (sub == 0) {
+    if (sub == 0 && u < UV) {
 #pragma unroll
       for (int gi = 0; gi < G; ++gi)
 #pragma unroll
@@ -268,29 +286,36 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < G * RV; i += 128) {
-    const int gi = i / RV, c = i - gi * RV;
+  const int RVO = a.rv;
+  for (int i = threadIdx.x; i < G * RVO; i += 128) {
+    const int gi = i / RVO, c = i - gi * RVO;
     const int h = g * G + gi;
-    float* dst = a.part + ((static_cast<int64_t>(b) * a.Nh + h) * a.splits + split) * (RV + 2);
-    dst[c] = red[0][gi][c] + red[1][gi][c] + red[2][gi][c] + red[3][gi][c];
+    float* dst = a.part + ((static_cast<int64_t>(b) * a.Nh + h) * nslots + slot0 + split) * (RVO + 2);
+    dst[c] = c < RV ? red[0][gi][c] + red[1][gi][c] + red[2][gi][c] + red[3][gi][c] : 0.f;
     if (c == 0) {
-      dst[RV] = n > 0 ? mx[gi] : -INFINITY;
-      dst[RV + 1] = n > 0 ? ls[gi] : 0.f;
+      float m = -INFINITY, l = 0.f;
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg)
+        if (gg == gi) m = mx[gg], l = ls[gg];
+      dst[RVO] = n > 0 ? m : -INFINITY;
+      dst[RVO + 1] = n > 0 ? l : 0.f;
     }
   }
 }
 
-template <int RV>
-__global__ void __launch_bounds__(128) decode_attn_combine(const DecodeAttnArgs a) {
+// Merge the partials of one (sequence, head): O' = sum_s o_s 2^(m_s - M) / sum_s l_s 2^(m_s - M),
+// LSE = (M + log2 L) ln 2 (natural log of the Eq. 3 denominator).
+__global__ void __launch_bounds__(128) decode_attn_combine(const DecodeAttnArgs a, int nslots) {
   const int h = blockIdx.x, b = blockIdx.y;
-  const float* part = a.part + (static_cast<int64_t>(b) * a.Nh + h) * a.splits * (RV + 2);
-  __shared__ float w[64];
+  const int RV = a.rv;
+  const float* part = a.part + (static_cast<int64_t>(b) * a.Nh + h) * nslots * (RV + 2);
+  __shared__ float w[128];
   __shared__ float tot;
   if (threadIdx.x == 0) {
     float M = -INFINITY;
-    for (int s = 0; s < a.splits; ++s) M = fmaxf(M, part[s * (RV + 2) + RV]);
+    for (int s = 0; s < nslots; ++s) M = fmaxf(M, part[s * (RV + 2) + RV]);
     float L = 0.f;
-    for (int s = 0; s < a.splits; ++s) {
+    for (int s = 0; s < nslots; ++s) {
       const float m = part[s * (RV + 2) + RV];
       const float ws = m == -INFINITY ? 0.f : exp2f(m - M);
       w[s] = ws;
@@ -303,7 +328,7 @@ __global__ void __launch_bounds__(128) decode_attn_combine(const DecodeAttnArgs 
   const float inv = 1.f / tot;
   for (int c = threadIdx.x; c < RV; c += blockDim.x) {
     float o = 0.f;
-    for (int s = 0; s < a.splits; ++s) o = fmaf(w[s], part[s * (RV + 2) + c], o);
+    for (int s = 0; s < nslots; ++s) o = fmaf(w[s], part[s * (RV + 2) + c], o);
     a.o[b * a.ldo + h * RV + c] = f32_to_bf16_bits(o * inv);
   }
 }
@@ -312,7 +337,6 @@ int decode_splits(int B, int Nkv, int len) {
   const int pairs = B * Nkv;
   int s = (4 * num_sms() + pairs - 1) / pairs;     // ~4 CTAs per SM
   const int min_for_smem = (len + kMaxChunk - 1) / kMaxChunk;
-  if (s < min_for_smem) s = min_for_smem;
   const int max_useful = (len + 31) / 32;            // >= 32 keys per chunk
   if (s > max_useful) s = max_useful;
   if (s < min_for_smem) s = min_for_smem;
@@ -321,42 +345,56 @@ int decode_splits(int B, int Nkv, int len) {
   return s;
 }
 
-template <int RK, int RV, int G>
-static cudaError_t launch_decode_t(const DecodeAttnArgs& a, cudaStream_t stream) {
+template <int RK, int G>
+static void launch_partial_t(const DecodeAttnArgs& a, const uint16_t* kp, const uint16_t* vp, int pool, int slot0,
+                             int nslots, cudaStream_t stream) {
   dim3 grid(a.splits, a.Nkv, a.B);
-  prof_mark(stream, true, kProfAttnDecode);
-  decode_attn_partial<RK, RV, G><<<grid, 128, 0, stream>>>(a);
-  prof_mark(stream, false, kProfAttnDecode);
-  prof_mark(stream, true, kProfAttnCombine);
-  decode_attn_combine<RV><<<dim3(a.Nh, a.B), 128, 0, stream>>>(a);
-  prof_mark(stream, false, kProfAttnCombine);
-  g_launches += 2;
+  decode_attn_partial<RK, RK, G><<<grid, 128, 0, stream>>>(a, kp, vp, pool, slot0, nslots);
+}
+
+template <int G>
+static cudaError_t launch_partial_g(const DecodeAttnArgs& a, int width, const uint16_t* kp, const uint16_t* vp,
+                                    int pool, int slot0, int nslots, cudaStream_t stream) {
+  switch (width) {
+    case 16: launch_partial_t<16, G>(a, kp, vp, pool, slot0, nslots, stream); break;
+    case 32: launch_partial_t<32, G>(a, kp, vp, pool, slot0, nslots, stream); break;
+    case 48: launch_partial_t<48, G>(a, kp, vp, pool, slot0, nslots, stream); break;
+    case 64: launch_partial_t<64, G>(a, kp, vp, pool, slot0, nslots, stream); break;
+    case 80: launch_partial_t<80, G>(a, kp, vp, pool, slot0, nslots, stream); break;
+    case 96: launch_partial_t<96, G>(a, kp, vp, pool, slot0, nslots, stream); break;
+    case 112: launch_partial_t<112, G>(a, kp, vp, pool, slot0, nslots, stream); break;
+    case 128: launch_partial_t<128, G>(a, kp, vp, pool, slot0, nslots, stream); break;
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 
-template <int RK, int RV>
-static cudaError_t launch_decode_g(const DecodeAttnArgs& a, cudaStream_t stream) {
-  const int G = a.Nh / a.Nkv;
-  switch (G) {
-    case 1: return launch_decode_t<RK, RV, 1>(a, stream);
-    case 2: return launch_decode_t<RK, RV, 2>(a, stream);
-    case 4: return launch_decode_t<RK, RV, 4>(a, stream);
-    case 8: return launch_decode_t<RK, RV, 8>(a, stream);
+static cudaError_t launch_partial(const DecodeAttnArgs& a, int width, const uint16_t* kp, const uint16_t* vp, int pool,
+                                  int slot0, int nslots, cudaStream_t stream) {
+  switch (a.Nh / a.Nkv) {
+    case 1: return launch_partial_g<1>(a, width, kp, vp, pool, slot0, nslots, stream);
+    case 2: return launch_partial_g<2>(a, width, kp, vp, pool, slot0, nslots, stream);
+    case 4: return launch_partial_g<4>(a, width, kp, vp, pool, slot0, nslots, stream);
+    case 8: return launch_partial_g<8>(a, width, kp, vp, pool, slot0, nslots, stream);
     default: return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t stream) {
-  // a.len is the largest length this launch (or graph replay) may see
+  // a.len bounds the rows of either pool (graph replays may see any length up to it)
   if (a.splits > 64 || (a.len + a.splits - 1) / a.splits > kMaxChunk) return cudaErrorInvalidValue;
-  if (a.rk != a.rv) return cudaErrorInvalidValue;
-  switch (a.rk) {
-    case 16: return launch_decode_g<16, 16>(a, stream);
-    case 32: return launch_decode_g<32, 32>(a, stream);
-    case 64: return launch_decode_g<64, 64>(a, stream);
-    case 128: return launch_decode_g<128, 128>(a, stream);
-    default: return cudaErrorInvalidValue;
-  }
+  if (a.rk != a.rv || (a.k1 && a.rk1 != a.rv1)) return cudaErrorInvalidValue;
+  const int nslots = a.splits * (a.k1 ? 2 : 1);
+  prof_mark(stream, true, kProfAttnDecode);
+  cudaError_t e = launch_partial(a, a.rk, a.k, a.v, 0, 0, nslots, stream);
+  if (e == cudaSuccess && a.k1) e = launch_partial(a, a.rk1, a.k1, a.v1, 1, a.splits, nslots, stream);
+  prof_mark(stream, false, kProfAttnDecode);
+  if (e != cudaSuccess) return e;
+  prof_mark(stream, true, kProfAttnCombine);
+  decode_attn_combine<<<dim3(a.Nh, a.B), 128, 0, stream>>>(a, nslots);
+  prof_mark(stream, false, kProfAttnCombine);
+  g_launches += a.k1 ? 3 : 2;
+  return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ weight packing (load time)

@@ -65,22 +65,31 @@ struct PrefillAttnArgs {
 };
 cudaError_t launch_prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream);
 
-// ---- a3 decode attention: split-K over the context + LSE-merge combine
+// ---- a3 decode attention: split-K over the context (one or two pools) + LSE-merge combine
 struct DecodeAttnArgs {
-  const uint16_t* q;   // Q' [B][ldq]
-  int64_t ldq;
-  const uint16_t* k;   // cache, same addressing as PrefillAttnArgs
-  const uint16_t* v;
-  int S_cap;
-  int len;             // keys visible: positions [0, len) ...
-  const int* len_ptr;  // ... or [0, *len_ptr + 1) when set (device-side length, graph-replayable)
-  uint16_t* o;         // O' [B][ldo]
-  int64_t ldo;
-  float* lse;          // [B][Nh]
-  float* part;         // scratch [B][Nh][splits][rv + 2]
-  int B, Nh, Nkv, rk, rv;
-  float scale;
-  int splits;
+  const uint16_t* q = nullptr;  // Q' [B][ldq]; head h at cols h*rk
+  int64_t ldq = 0;
+  // pool 0 (important rows, or every row without a token split): row i of (b, g) at
+  // ((b*Nkv+g)*S_cap + i) * width
+  const uint16_t* k = nullptr;
+  const uint16_t* v = nullptr;
+  int rk = 0, rv = 0;
+  // pool 1 (unimportant rows, truncated width; token split only)
+  const uint16_t* k1 = nullptr;
+  const uint16_t* v1 = nullptr;
+  int rk1 = 0, rv1 = 0;
+  int S_cap = 0;
+  int len = 0;                   // upper bound on any pool's rows (fixes the split count)
+  const int* len_ptr = nullptr;  // uniform cache: pool-0 rows = *len_ptr + 1
+  const int* n0_ptr = nullptr;   // token split: per-sequence rows of pool 0 / pool 1 [B]
+  const int* n1_ptr = nullptr;
+  uint16_t* o = nullptr;  // O' [B][ldo]
+  int64_t ldo = 0;
+  float* lse = nullptr;   // [B][Nh]
+  float* part = nullptr;  // scratch [B][Nh][2 * splits][rv + 2]
+  int B = 0, Nh = 0, Nkv = 0;
+  float scale = 0.f;
+  int splits = 1;
 };
 cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t stream);
 int decode_splits(int B, int Nkv, int len);
