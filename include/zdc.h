@@ -193,6 +193,9 @@ zdc_status zdc_sp_positions(int32_t S_total, int32_t world, int32_t rank, int32_
 zdc_status zdc_cache_export(const zdc_ctx* ctx, int32_t layer, float* k, float* v,
                             uint8_t* is_important, float* tau, void* stream);
 zdc_status zdc_cache_length(const zdc_ctx* ctx, int32_t layer, int32_t* len);
+/* Importance scores (reading c9: log of sum_h sum_{k<=t} exp(s_k^h), f32 as computed on the GPU)
+ * of every cached token of a representative layer of a split group: scores [B][len], host. */
+zdc_status zdc_scores_export(const zdc_ctx* ctx, int32_t layer, float* scores, void* stream);
 zdc_status zdc_cache_reset(zdc_ctx* ctx, void* stream);
 
 /* Device LSE of the last prefill/decode call of a layer: f32 [B][N_h][T] (T = S for a

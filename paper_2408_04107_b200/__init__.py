@@ -28,7 +28,7 @@ ZDC_STATUS = {0: "ZDC_OK", -1: "ZDC_ERR_INVALID_ARG", -2: "ZDC_ERR_SHAPE", -3: "
 EXPORTED_SYMBOLS = ["zdc_last_error", "zdc_version", "zdc_fold_weights", "zdc_ctx_create", "zdc_ctx_sizes",
                     "zdc_ctx_bind", "zdc_ctx_destroy", "zdc_load_folded", "zdc_load_folded_device",
                     "zdc_prefill", "zdc_decode", "zdc_comm_init", "zdc_sp_prefill", "zdc_sp_positions",
-                    "zdc_cache_export", "zdc_cache_length", "zdc_cache_reset", "zdc_last_lse",
+                    "zdc_cache_export", "zdc_cache_length", "zdc_scores_export", "zdc_cache_reset", "zdc_last_lse",
                     "zdc_gemm_bf16", "zdc_kernel_launch_count", "zdc_profile", "zdc_profile_read"]
 
 
@@ -85,6 +85,7 @@ def lib():
             "zdc_sp_positions": ([I32, I32, I32, I32, ctypes.POINTER(I32)], I32),
             "zdc_cache_export": ([P, I32, P, P, P, P, P], I32),
             "zdc_cache_length": ([P, I32, ctypes.POINTER(I32)], I32),
+            "zdc_scores_export": ([P, I32, P, P], I32),
             "zdc_cache_reset": ([P, P], I32),
             "zdc_last_lse": ([P, I32, P, P], I32),
             "zdc_gemm_bf16": ([P, P, P, I32, I32, I32, P], I32),
@@ -266,6 +267,14 @@ class Context:
         _check(lib().zdc_cache_export(self.h, layer, ptr(k), ptr(v), ptr(imp), ptr(tau),
                                       ctypes.c_void_p(_stream(stream))), "zdc_cache_export")
         return k, v, imp.astype(bool), tau
+
+    def scores_export(self, layer: int, B: int, stream=None) -> np.ndarray:
+        """GPU importance scores (f32) of every cached token of a representative layer."""
+        length = self.cache_length(layer)
+        out = np.zeros((B, length), dtype=np.float32)
+        _check(lib().zdc_scores_export(self.h, layer, ctypes.c_void_p(out.ctypes.data),
+                                       ctypes.c_void_p(_stream(stream))), "zdc_scores_export")
+        return out
 
     def last_lse(self, layer: int, B: int, T: int, stream=None) -> np.ndarray:
         out = np.zeros((B, self.dims.n_heads, T), dtype=np.float32)

@@ -2,6 +2,7 @@
 // orchestration of the hot path (a1 projection -> a2 append -> a3 attention -> a4 selection
 // -> a5 output projection).  Host code only; every step of the path runs in the kernels of
 // gemm.cu / attn_prefill.cu / decode.cu / select.cu.
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -110,7 +111,7 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
   c->layers.resize(d.n_layers);
   c->len.assign(d.n_layers, 0);
   int64_t woff = 0, coff = 0;
-  int max_nq = 0, max_ko = 0, max_rv = 0;
+  int max_nq = 0, max_ko = 0, max_rv = 0, max_split_w = 0;
   bool any_split = false;
   for (int l = 0; l < d.n_layers; ++l) {
     LayerInfo& L = c->layers[l];
@@ -162,6 +163,21 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
     coff = align_up(coff + kv_rows * L.rk_p * 2, 256);
     L.v_off = coff;
     coff = align_up(coff + kv_rows * L.rv_p * 2, 256);
+    if (L.split) {
+      L.ku_off = coff;
+      coff = align_up(coff + kv_rows * L.rku_p * 2, 256);
+      L.vu_off = coff;
+      coff = align_up(coff + kv_rows * L.rvu_p * 2, 256);
+      L.posi_off = coff;
+      coff = align_up(coff + static_cast<int64_t>(max_batch) * max_seq * 4, 256);
+      L.posu_off = coff;
+      coff = align_up(coff + static_cast<int64_t>(max_batch) * max_seq * 4, 256);
+      L.ni_off = coff;
+      coff = align_up(coff + static_cast<int64_t>(max_batch) * 4, 256);
+      L.nu_off = coff;
+      coff = align_up(coff + static_cast<int64_t>(max_batch) * 4, 256);
+      if (L.rk_p > max_split_w) max_split_w = L.rk_p;
+    }
     if (L.split && L.rep == l) {
       L.cls_off = coff;
       coff = align_up(coff + static_cast<int64_t>(max_batch) * max_seq, 256);
@@ -176,10 +192,6 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
   }
   c->len_dev_off = coff;
   coff = align_up(coff + static_cast<int64_t>(d.n_layers) * 4, 256);
-  if (any_split) {
-    delete c;
-    return fail(ZDC_ERR_UNSUPPORTED, "token-level split (g_bp < 10000) is not implemented in this build");
-  }
   c->weight_bytes = woff;
   c->cache_bytes = coff;
   const int64_t rows = static_cast<int64_t>(max_batch) * max_seq;
@@ -192,6 +204,17 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
   s = align_up(s + rows * d.n_heads * 4, 256);
   c->s_part = s;
   s = align_up(s + static_cast<int64_t>(max_batch) * d.n_heads * 128 * (max_rv + 2) * 4, 256);
+  if (any_split) {  // staged K'/V' of a split layer before packing, compaction indices, new-row staging
+    const int64_t kv_rows = static_cast<int64_t>(max_batch) * d.n_kv_heads * max_seq;
+    c->s_ks = s;
+    s = align_up(s + kv_rows * max_split_w * 2, 256);
+    c->s_vs = s;
+    s = align_up(s + kv_rows * max_split_w * 2, 256);
+    c->s_didx = s;
+    s = align_up(s + rows * 4, 256);
+    c->s_new = s;
+    s = align_up(s + static_cast<int64_t>(max_batch) * d.n_kv_heads * max_split_w * 2 * 2, 256);
+  }
   c->ldq = max_nq;
   c->ldo = max_ko;
   c->scratch_bytes = s;
@@ -338,7 +361,6 @@ zdc_status zdc_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, ui
     for (int l = 0; l < c->dims.n_layers; ++l) all_empty &= c->len[l] == 0;
     if (!all_empty) return fail(ZDC_ERR_SHAPE, "zdc_prefill: batch %d differs from the cache batch %d", B, c->batch);
   }
-  (void)importance;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   g_launches = 0;
   const int d = c->dims.d_model, Nh = c->dims.n_heads, Nkv = c->dims.n_kv_heads;
@@ -346,18 +368,37 @@ zdc_status zdc_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, ui
   for (int l = l0; l < l1; ++l) {
     const LayerInfo& L = c->layers[l];
     const uint16_t* xin = l == l0 ? x : y;
-    // a1 + a2: [Q'|K'|V'] = x W_QKV^R; K'/V' written into the cache at positions [0, S)
+    const bool is_rep = L.rep == l;
+    if (L.split && !is_rep && c->len[L.rep] != S)
+      return fail(ZDC_ERR_STATE, "zdc_prefill: layer %d needs its representative layer %d prefilled first", l, L.rep);
+    // a1 + a2: [Q'|K'|V'] = x W_QKV^R; K'/V' written into the cache at positions [0, S) (uniform
+    // layers) or staged for the class-aware packing (token split)
     Epilogue e1;
     e1.mode = 1;
     e1.qkv = qkv_dest(c, L, S, 0, nullptr);
+    uint16_t* ks = reinterpret_cast<uint16_t*>(c->scratch + c->s_ks);
+    uint16_t* vs = reinterpret_cast<uint16_t*>(c->scratch + c->s_vs);
+    if (L.split) {
+      e1.qkv.k = ks;
+      e1.qkv.v = vs;
+    }
     g_prof_class = kProfGemmQkv;
     ZDC_CUDA_TRY(launch_gemm(xin, d, reinterpret_cast<const uint16_t*>(c->w + L.w_qkv), d, M, L.n_qkv, d, e1, s));
+    const LayerInfo& R = c->layers[L.rep];
+    uint8_t* rep_cls = reinterpret_cast<uint8_t*>(c->cache + R.cls_off);
+    g_prof_class = kProfOther;
+    if (L.split && !is_rep) {
+      // non-representative layer: the group's classes are known; unimportant key/value rows lose
+      // dims >= r^u BEFORE attention (P:774-776 DEL; reading c13)
+      ZDC_CUDA_TRY(launch_truncate(ks, L.rk_p, L.rku, B, Nkv, S, c->max_seq, rep_cls, c->max_seq, s));
+      ZDC_CUDA_TRY(launch_truncate(vs, L.rv_p, L.rvu, B, Nkv, S, c->max_seq, rep_cls, c->max_seq, s));
+    }
     // a3: causal attention at head dim r, O' and LSE
     PrefillAttnArgs a;
     a.q = reinterpret_cast<const uint16_t*>(c->scratch + c->s_q);
     a.ldq = L.nq;
-    a.k = reinterpret_cast<const uint16_t*>(c->cache + L.k_off);
-    a.v = reinterpret_cast<const uint16_t*>(c->cache + L.v_off);
+    a.k = L.split ? ks : reinterpret_cast<const uint16_t*>(c->cache + L.k_off);
+    a.v = L.split ? vs : reinterpret_cast<const uint16_t*>(c->cache + L.v_off);
     a.S_cap = c->max_seq;
     a.o = reinterpret_cast<uint16_t*>(c->scratch + c->s_o);
     a.ldo = L.ko_p;
@@ -373,6 +414,30 @@ zdc_status zdc_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, ui
     a.q_row0 = 0;
     a.n_q = S;
     ZDC_CUDA_TRY(launch_prefill_attention(a, s));
+    if (L.split) {
+      g_prof_class = kProfOther;
+      if (is_rep) {
+        // a4: importance from the reused softmax denominators, then the top-g selection
+        float* scores = reinterpret_cast<float*>(c->cache + L.score_off);
+        ZDC_CUDA_TRY(launch_importance(a.lse, S, Nh, B, 0, c->importance_mode, scores, c->max_seq,
+                                       importance ? importance + static_cast<int64_t>(l) * B * c->max_seq : nullptr,
+                                       c->max_seq, nullptr, s));
+        ZDC_CUDA_TRY(launch_select(scores, c->max_seq, S, L.g_bp, B, reinterpret_cast<uint8_t*>(c->cache + L.cls_off),
+                                   reinterpret_cast<float*>(c->cache + L.tau_off), s));
+      }
+      // a2 (split): stable class-aware compaction of the staged rows into pool_I / pool_U
+      int* didx = reinterpret_cast<int*>(c->scratch + c->s_didx);
+      ZDC_CUDA_TRY(launch_rank(rep_cls, c->max_seq, S, B, didx, c->max_seq,
+                               reinterpret_cast<int*>(c->cache + L.posi_off), reinterpret_cast<int*>(c->cache + L.posu_off),
+                               c->max_seq, reinterpret_cast<int*>(c->cache + L.ni_off),
+                               reinterpret_cast<int*>(c->cache + L.nu_off), s));
+      ZDC_CUDA_TRY(launch_pack(ks, L.rk_p, reinterpret_cast<uint16_t*>(c->cache + L.k_off),
+                               reinterpret_cast<uint16_t*>(c->cache + L.ku_off), L.rku_p, L.rku, B, Nkv, S, c->max_seq,
+                               didx, c->max_seq, s));
+      ZDC_CUDA_TRY(launch_pack(vs, L.rv_p, reinterpret_cast<uint16_t*>(c->cache + L.v_off),
+                               reinterpret_cast<uint16_t*>(c->cache + L.vu_off), L.rvu_p, L.rvu, B, Nkv, S, c->max_seq,
+                               didx, c->max_seq, s));
+    }
     // a5: y = O' W_O^R
     Epilogue e5;
     e5.mode = 0;
@@ -403,6 +468,18 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
     e1.mode = 1;
     e1.qkv = qkv_dest(c, L, 1, 0, nullptr);
     e1.qkv.pos_ptr = len_dev;
+    uint16_t* knew = reinterpret_cast<uint16_t*>(c->scratch + c->s_new);
+    uint16_t* vnew = knew + static_cast<int64_t>(B) * Nkv * L.rk_p;
+    if (L.split) {  // stage the new row; the class-aware append places it below
+      e1.qkv.k = knew;
+      e1.qkv.v = vnew;
+      e1.qkv.pos_ptr = nullptr;
+      e1.qkv.pos0 = 0;
+      e1.qkv.kg = L.rk_p;
+      e1.qkv.kb = static_cast<int64_t>(Nkv) * L.rk_p;
+      e1.qkv.vg = L.rv_p;
+      e1.qkv.vb = static_cast<int64_t>(Nkv) * L.rv_p;
+    }
     const uint16_t* wqkv = reinterpret_cast<const uint16_t*>(c->w + L.w_qkv);
     const uint16_t* wo = reinterpret_cast<const uint16_t*>(c->w + L.w_o);
     g_prof_class = kProfGemvQkv;
@@ -410,7 +487,21 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
       ZDC_CUDA_TRY(launch_gemv(wqkv, xin, d, B, L.n_qkv, d, e1, s));
     else
       ZDC_CUDA_TRY(launch_gemm(xin, d, wqkv, d, B, L.n_qkv, d, e1, s));
-    // a3: split-K attention over the *len_dev + 1 cached keys
+    const LayerInfo& R = c->layers[L.rep];
+    const bool is_rep = L.rep == l;
+    if (L.split) {
+      g_prof_class = kProfOther;
+      ZDC_CUDA_TRY(launch_append(knew, vnew, L.rk_p, Nkv, reinterpret_cast<uint16_t*>(c->cache + L.k_off),
+                                 reinterpret_cast<uint16_t*>(c->cache + L.v_off),
+                                 reinterpret_cast<uint16_t*>(c->cache + L.ku_off),
+                                 reinterpret_cast<uint16_t*>(c->cache + L.vu_off), L.rku_p, L.rku, c->max_seq,
+                                 reinterpret_cast<int*>(c->cache + L.ni_off), reinterpret_cast<int*>(c->cache + L.nu_off),
+                                 reinterpret_cast<int*>(c->cache + L.posi_off),
+                                 reinterpret_cast<int*>(c->cache + L.posu_off), c->max_seq, len_dev,
+                                 reinterpret_cast<const uint8_t*>(c->cache + R.cls_off), c->max_seq, is_rep ? 1 : 0, B,
+                                 s));
+    }
+    // a3: split-K attention over the *len_dev + 1 cached keys (two pools with a token split)
     DecodeAttnArgs a;
     a.q = reinterpret_cast<const uint16_t*>(c->scratch + c->s_q);
     a.ldq = L.nq;
@@ -430,7 +521,29 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
     a.rv = L.rv_p;
     a.scale = 1.0f / std::sqrt(static_cast<float>(c->dims.d_head));
     a.splits = decode_splits(B, Nkv, c->max_seq);
+    if (L.split) {
+      a.len_ptr = nullptr;
+      a.n0_ptr = reinterpret_cast<const int*>(c->cache + L.ni_off);
+      a.n1_ptr = reinterpret_cast<const int*>(c->cache + L.nu_off);
+      a.k1 = reinterpret_cast<const uint16_t*>(c->cache + L.ku_off);
+      a.v1 = reinterpret_cast<const uint16_t*>(c->cache + L.vu_off);
+      a.rk1 = L.rku_p;
+      a.rv1 = L.rvu_p;
+    }
     ZDC_CUDA_TRY(launch_decode_attention(a, s));
+    if (L.split && is_rep) {
+      g_prof_class = kProfOther;
+      ZDC_CUDA_TRY(launch_classify(a.lse, Nh, c->importance_mode, reinterpret_cast<const float*>(c->cache + L.tau_off),
+                                   reinterpret_cast<float*>(c->cache + L.score_off),
+                                   reinterpret_cast<uint8_t*>(c->cache + L.cls_off), c->max_seq, nullptr, 0, L.rk_p,
+                                   Nkv, reinterpret_cast<uint16_t*>(c->cache + L.k_off),
+                                   reinterpret_cast<uint16_t*>(c->cache + L.v_off),
+                                   reinterpret_cast<uint16_t*>(c->cache + L.ku_off),
+                                   reinterpret_cast<uint16_t*>(c->cache + L.vu_off), L.rku_p, L.rku, c->max_seq,
+                                   reinterpret_cast<int*>(c->cache + L.ni_off), reinterpret_cast<int*>(c->cache + L.nu_off),
+                                   reinterpret_cast<int*>(c->cache + L.posi_off),
+                                   reinterpret_cast<int*>(c->cache + L.posu_off), len_dev, B, s));
+    }
     // a5: y = O' W_O^R; this kernel also advances *len_dev (all readers of it have run)
     Epilogue e5;
     e5.mode = 0;
@@ -452,9 +565,18 @@ zdc_status zdc_decode(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, uin
   if (st != ZDC_OK) return st;
   if (B <= 0 || B > c->max_batch) return fail(ZDC_ERR_CAPACITY, "zdc_decode: B=%d (max_batch %d)", B, c->max_batch);
   if (c->batch != 0 && B != c->batch) return fail(ZDC_ERR_SHAPE, "zdc_decode: B=%d but cache batch is %d", B, c->batch);
-  for (int l = l0; l < l1; ++l)
+  for (int l = l0; l < l1; ++l) {
     if (c->len[l] + 1 > c->max_seq)
       return fail(ZDC_ERR_CAPACITY, "zdc_decode: layer %d len %d + 1 > max_seq %d", l, c->len[l], c->max_seq);
+    const LayerInfo& L = c->layers[l];
+    if (L.split && L.rep != l) {
+      // the representative must have classified this position (in this call or an earlier one)
+      const int rep_len = c->len[L.rep] + ((L.rep >= l0 && L.rep < l) ? 1 : 0);
+      if (rep_len <= c->len[l])
+        return fail(ZDC_ERR_STATE, "zdc_decode: layer %d: representative %d has not classified position %d", l, L.rep,
+                    c->len[l]);
+    }
+  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   g_launches = 0;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
@@ -529,33 +651,85 @@ zdc_status zdc_cache_export(const zdc_ctx* c, int32_t layer, float* k, float* v,
   if (!c->cache) return fail(ZDC_ERR_STATE, "zdc_cache_export: ctx not bound");
   if (layer < 0 || layer >= c->dims.n_layers) return fail(ZDC_ERR_SHAPE, "zdc_cache_export: layer %d", layer);
   const LayerInfo& L = c->layers[layer];
-  const int B = c->batch, len = c->len[layer], Nkv = c->dims.n_kv_heads;
+  const int B = c->batch, len = c->len[layer], Nkv = c->dims.n_kv_heads, S_cap = c->max_seq;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   ZDC_CUDA_TRY(cudaStreamSynchronize(st));
-  const int64_t rows = static_cast<int64_t>(c->max_batch) * Nkv * c->max_seq;
-  std::vector<uint16_t> hk, hv;
-  if (k) {
-    hk.resize(rows * L.rk_p);
-    ZDC_CUDA_TRY(cudaMemcpy(hk.data(), c->cache + L.k_off, hk.size() * 2, cudaMemcpyDeviceToHost));
+  const int64_t rows = static_cast<int64_t>(c->max_batch) * Nkv * S_cap;
+  auto fetch16 = [&](int64_t off, int64_t n, std::vector<uint16_t>& h) {
+    h.resize(n);
+    return cudaMemcpy(h.data(), c->cache + off, n * 2, cudaMemcpyDeviceToHost);
+  };
+  auto fetch32 = [&](int64_t off, int64_t n, std::vector<int>& h) {
+    h.resize(n);
+    return cudaMemcpy(h.data(), c->cache + off, n * 4, cudaMemcpyDeviceToHost);
+  };
+  std::vector<uint16_t> ki, vi, ku, vu;
+  std::vector<int> posi, posu, ni, nu;
+  ZDC_CUDA_TRY(fetch16(L.k_off, rows * L.rk_p, ki));
+  ZDC_CUDA_TRY(fetch16(L.v_off, rows * L.rv_p, vi));
+  if (L.split) {
+    ZDC_CUDA_TRY(fetch16(L.ku_off, rows * L.rku_p, ku));
+    ZDC_CUDA_TRY(fetch16(L.vu_off, rows * L.rvu_p, vu));
+    ZDC_CUDA_TRY(fetch32(L.posi_off, static_cast<int64_t>(c->max_batch) * S_cap, posi));
+    ZDC_CUDA_TRY(fetch32(L.posu_off, static_cast<int64_t>(c->max_batch) * S_cap, posu));
+    ZDC_CUDA_TRY(fetch32(L.ni_off, c->max_batch, ni));
+    ZDC_CUDA_TRY(fetch32(L.nu_off, c->max_batch, nu));
   }
-  if (v) {
-    hv.resize(rows * L.rv_p);
-    ZDC_CUDA_TRY(cudaMemcpy(hv.data(), c->cache + L.v_off, hv.size() * 2, cudaMemcpyDeviceToHost));
+  const int64_t nk_out = static_cast<int64_t>(B) * len * Nkv;
+  if (k) std::fill(k, k + nk_out * L.rk, 0.f);
+  if (v) std::fill(v, v + nk_out * L.rv, 0.f);
+  if (is_imp) std::memset(is_imp, L.split ? 0 : 1, static_cast<size_t>(B) * len);
+  // place pool row i of (b, g) at position t, zero-filled to the important widths
+  auto place = [&](int b, int t, int i, const std::vector<uint16_t>& K, const std::vector<uint16_t>& V, int wk, int wv,
+                   int rk_valid, int rv_valid) {
+    if (t < 0 || t >= len) return;
+    for (int g = 0; g < Nkv; ++g) {
+      const int64_t row = (static_cast<int64_t>(b) * Nkv + g) * S_cap + i;
+      const int64_t o = (static_cast<int64_t>(b) * len + t) * Nkv + g;
+      if (k)
+        for (int e = 0; e < rk_valid; ++e) k[o * L.rk + e] = bf16_to_f32(K[row * wk + e]);
+      if (v)
+        for (int e = 0; e < rv_valid; ++e) v[o * L.rv + e] = bf16_to_f32(V[row * wv + e]);
+    }
+  };
+  for (int b = 0; b < B; ++b) {
+    if (!L.split) {
+      for (int t = 0; t < len; ++t) place(b, t, t, ki, vi, L.rk_p, L.rv_p, L.rk, L.rv);
+      continue;
+    }
+    for (int i = 0; i < ni[b]; ++i) {
+      const int t = posi[static_cast<int64_t>(b) * S_cap + i];
+      place(b, t, i, ki, vi, L.rk_p, L.rv_p, L.rk, L.rv);
+      if (is_imp && t >= 0 && t < len) is_imp[static_cast<int64_t>(b) * len + t] = 1;
+    }
+    for (int i = 0; i < nu[b]; ++i) {
+      const int t = posu[static_cast<int64_t>(b) * S_cap + i];
+      place(b, t, i, ku, vu, L.rku_p, L.rvu_p, L.rku, L.rvu);
+    }
   }
+  if (tau) {
+    if (L.split) {
+      ZDC_CUDA_TRY(cudaMemcpy(tau, c->cache + c->layers[L.rep].tau_off, static_cast<size_t>(B) * 4,
+                              cudaMemcpyDeviceToHost));
+    } else {
+      for (int b = 0; b < B; ++b) tau[b] = INFINITY;
+    }
+  }
+  return ZDC_OK;
+}
+
+zdc_status zdc_scores_export(const zdc_ctx* c, int32_t layer, float* scores, void* stream) {
+  if (!c || !scores) return fail(ZDC_ERR_INVALID_ARG, "zdc_scores_export: null argument");
+  if (layer < 0 || layer >= c->dims.n_layers) return fail(ZDC_ERR_SHAPE, "zdc_scores_export: layer %d", layer);
+  const LayerInfo& L = c->layers[layer];
+  if (!L.split || L.rep != layer)
+    return fail(ZDC_ERR_STATE, "zdc_scores_export: layer %d is not the representative of a split group", layer);
+  ZDC_CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  const int B = c->batch, len = c->len[layer];
+  std::vector<float> h(static_cast<size_t>(c->max_batch) * c->max_seq);
+  ZDC_CUDA_TRY(cudaMemcpy(h.data(), c->cache + L.score_off, h.size() * 4, cudaMemcpyDeviceToHost));
   for (int b = 0; b < B; ++b)
-    for (int t = 0; t < len; ++t)
-      for (int g = 0; g < Nkv; ++g) {
-        const int64_t row = (static_cast<int64_t>(b) * Nkv + g) * c->max_seq + t;
-        if (k)
-          for (int e = 0; e < L.rk; ++e)
-            k[((static_cast<int64_t>(b) * len + t) * Nkv + g) * L.rk + e] = bf16_to_f32(hk[row * L.rk_p + e]);
-        if (v)
-          for (int e = 0; e < L.rv; ++e)
-            v[((static_cast<int64_t>(b) * len + t) * Nkv + g) * L.rv + e] = bf16_to_f32(hv[row * L.rv_p + e]);
-      }
-  if (is_imp) std::memset(is_imp, 1, static_cast<size_t>(B) * len);
-  if (tau)
-    for (int b = 0; b < B; ++b) tau[b] = INFINITY;
+    for (int t = 0; t < len; ++t) scores[static_cast<int64_t>(b) * len + t] = h[static_cast<size_t>(b) * c->max_seq + t];
   return ZDC_OK;
 }
 

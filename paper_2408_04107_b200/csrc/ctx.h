@@ -22,6 +22,8 @@ struct LayerInfo {
   int64_t w_qkv = 0, w_o = 0;                      // byte offsets in the weight region
   int64_t k_off = 0, v_off = 0;                    // byte offsets in the cache region
   int64_t cls_off = 0, tau_off = 0, score_off = 0;  // representative layers of split groups
+  // token split: pool_U (unimportant rows, truncated width), positions and per-sequence counts
+  int64_t ku_off = 0, vu_off = 0, posi_off = 0, posu_off = 0, ni_off = 0, nu_off = 0;
 };
 
 struct CommState;
@@ -36,6 +38,7 @@ struct zdc_ctx {
   std::vector<zdc::LayerInfo> layers;
   int64_t weight_bytes = 0, cache_bytes = 0, scratch_bytes = 0;
   int64_t s_q = 0, s_o = 0, s_lse = 0, s_part = 0;  // scratch offsets
+  int64_t s_ks = 0, s_vs = 0, s_didx = 0, s_new = 0;  // token-split staging
   int ldq = 0, ldo = 0;
   uint8_t* w = nullptr;
   uint8_t* cache = nullptr;

@@ -100,6 +100,26 @@ cudaError_t launch_pack_weights_bf16(const uint16_t* wq, const uint16_t* wk, con
                                      int Nkv, int dh, int rk, int rv, int rk_p, int rv_p, int ko_p,
                                      cudaStream_t stream);
 
+// ---- a4 selection + class-aware packing (select.cu)
+cudaError_t launch_importance(const float* lse, int T, int Nh, int B, int t0, int mode, float* scores, int64_t ld,
+                              float* out_copy, int64_t ld_copy, const int* pos_ptr, cudaStream_t s);
+cudaError_t launch_select(const float* scores, int64_t ld, int S, int g_bp, int B, uint8_t* cls, float* tau,
+                          cudaStream_t s);
+cudaError_t launch_truncate(uint16_t* kv, int width, int r_u, int B, int Nkv, int S, int S_cap, const uint8_t* cls,
+                            int64_t ld_cls, cudaStream_t s);
+cudaError_t launch_rank(const uint8_t* cls, int64_t ld_cls, int S, int B, int* didx, int64_t ld_didx, int* pos_i,
+                        int* pos_u, int64_t ld_pos, int* n_i, int* n_u, cudaStream_t s);
+cudaError_t launch_pack(const uint16_t* src, int w, uint16_t* pool_i, uint16_t* pool_u, int wu, int r_u, int B, int Nkv,
+                        int S, int S_cap, const int* didx, int64_t ld_didx, cudaStream_t s);
+cudaError_t launch_append(const uint16_t* knew, const uint16_t* vnew, int w, int Nkv, uint16_t* ki, uint16_t* vi,
+                          uint16_t* ku, uint16_t* vu, int wu, int r_u, int S_cap, int* n_i, int* n_u, int* pos_i,
+                          int* pos_u, int64_t ld_pos, const int* len_ptr, const uint8_t* rep_cls, int64_t ld_cls,
+                          int is_rep, int B, cudaStream_t s);
+cudaError_t launch_classify(const float* lse, int Nh, int mode, const float* tau, float* scores, uint8_t* cls,
+                            int64_t ld, float* out_copy, int64_t ld_copy, int w, int Nkv, uint16_t* ki, uint16_t* vi,
+                            uint16_t* ku, uint16_t* vu, int wu, int r_u, int S_cap, int* n_i, int* n_u, int* pos_i,
+                            int* pos_u, const int* len_ptr, int B, cudaStream_t s);
+
 extern int64_t g_launches;  // kernels enqueued by the last API call
 
 // ---- per-kernel-class timing (zdc_profile): CUDA events bracket each launch on its stream
