@@ -169,10 +169,21 @@ zdc_status zdc_decode(zdc_ctx* ctx, int32_t l0, int32_t l1, const uint16_t* x, u
  * bytes = (P-1)/P * B S N_kv (r_k + r_v) * 2) -> a3 for local queries against all keys at
  * or before their global position -> a5 on local rows.  The result rows equal the
  * zdc_prefill rows of the same tokens.  Token split under SP is not supported
- * (ZDC_ERR_UNSUPPORTED).  zdc_comm_init takes a 128-byte ncclUniqueId.
+ * (ZDC_ERR_UNSUPPORTED).  zdc_comm_init takes a 128-byte ncclUniqueId.  Each rank keeps the
+ * gathered compressed K'/V' of the whole sequence in its cache, in the gather layout
+ * [P][K|V][B][N_kv][S/P][r]; zdc_decode / zdc_cache_export on such a layer return
+ * ZDC_ERR_UNSUPPORTED (SP decode is NEXT-2).  Chunks (S/P, or S/(2P) for zigzag) must be
+ * multiples of 128 when P > 1.
  *   stats (optional, host): bytes exchanged per rank and the exchange time on the device.
  * ---------------------------------------------------------------------------------- */
+zdc_status zdc_comm_unique_id(void* nccl_unique_id_out /*128 B, rank 0 creates, broadcast by the caller*/);
 zdc_status zdc_comm_init(zdc_ctx* ctx, const void* nccl_unique_id, int32_t rank, int32_t world);
+/* Test transport: instead of ncclAllGather, call fn(user, gather_buf, chunk_bytes, rank, world, stream)
+ * where the caller must make gather_buf[q*chunk_bytes, (q+1)*chunk_bytes) equal rank q's slot for every q
+ * before returning (used to run P ranks as P processes on ONE GPU in tests).  Replaces zdc_comm_init. */
+typedef void (*zdc_exchange_fn)(void* user, void* gather_buf, int64_t chunk_bytes, int32_t rank, int32_t world,
+                                void* stream);
+zdc_status zdc_sp_set_exchange_hook(zdc_ctx* ctx, zdc_exchange_fn fn, void* user, int32_t rank, int32_t world);
 typedef struct {
   int64_t bytes_sent, bytes_recv, bytes_recv_uncompressed;
   float exchange_ms, total_ms;

@@ -27,7 +27,8 @@ ZDC_STATUS = {0: "ZDC_OK", -1: "ZDC_ERR_INVALID_ARG", -2: "ZDC_ERR_SHAPE", -3: "
 
 EXPORTED_SYMBOLS = ["zdc_last_error", "zdc_version", "zdc_fold_weights", "zdc_ctx_create", "zdc_ctx_sizes",
                     "zdc_ctx_bind", "zdc_ctx_destroy", "zdc_load_folded", "zdc_load_folded_device",
-                    "zdc_prefill", "zdc_decode", "zdc_comm_init", "zdc_sp_prefill", "zdc_sp_positions",
+                    "zdc_prefill", "zdc_decode", "zdc_comm_unique_id", "zdc_comm_init",
+                    "zdc_sp_set_exchange_hook", "zdc_sp_prefill", "zdc_sp_positions",
                     "zdc_cache_export", "zdc_cache_length", "zdc_scores_export", "zdc_cache_reset", "zdc_last_lse",
                     "zdc_gemm_bf16", "zdc_kernel_launch_count", "zdc_profile", "zdc_profile_read"]
 
@@ -56,6 +57,11 @@ class SpStats(ctypes.Structure):
                 ("total_ms", ctypes.c_float)]
 
 
+# test transport of zdc_sp_set_exchange_hook: fn(user, gather_buf, chunk_bytes, rank, world, stream)
+EXCHANGE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                               ctypes.c_int32, ctypes.c_void_p)
+
+
 def lib_path() -> str:
     return _LIB_PATH
 
@@ -80,7 +86,9 @@ def lib():
             "zdc_load_folded_device": ([P, I32, P, P, P, P, P], I32),
             "zdc_prefill": ([P, I32, I32, P, P, I32, I32, P, P], I32),
             "zdc_decode": ([P, I32, I32, P, P, I32, P], I32),
+            "zdc_comm_unique_id": ([P], I32),
             "zdc_comm_init": ([P, P, I32, I32], I32),
+            "zdc_sp_set_exchange_hook": ([P, EXCHANGE_FN, P, I32, I32], I32),
             "zdc_sp_prefill": ([P, I32, I32, P, P, I32, I32, I32, ctypes.POINTER(SpStats), P], I32),
             "zdc_sp_positions": ([I32, I32, I32, I32, ctypes.POINTER(I32)], I32),
             "zdc_cache_export": ([P, I32, P, P, P, P, P], I32),
@@ -185,6 +193,13 @@ def sp_positions(S_total: int, world: int, rank: int, layout: int) -> np.ndarray
     return np.array(buf[:n], dtype=np.int64)
 
 
+def comm_unique_id() -> bytes:
+    """128-byte ncclUniqueId (rank 0 creates it; the caller broadcasts it)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().zdc_comm_unique_id(buf), "zdc_comm_unique_id")
+    return buf.raw
+
+
 def gemm_bf16(a, b, d, stream=None):
     """D[M][N] = A[M][K] B[N][K]^T through zdc_gemm_bf16 (tcgen05)."""
     M, K = a.shape
@@ -281,6 +296,28 @@ class Context:
         _check(lib().zdc_last_lse(self.h, layer, ctypes.c_void_p(out.ctypes.data), ctypes.c_void_p(_stream(stream))),
                "zdc_last_lse")
         return out
+
+    def comm_init(self, unique_id: bytes, rank: int, world: int):
+        buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+        _check(lib().zdc_comm_init(self.h, buf, rank, world), "zdc_comm_init")
+
+    def set_exchange_hook(self, fn, rank: int, world: int):
+        """Test transport for zdc_sp_prefill (fn is an EXCHANGE_FN); keeps a reference to fn."""
+        self._hook = fn
+        _check(lib().zdc_sp_set_exchange_hook(self.h, fn, None, rank, world), "zdc_sp_set_exchange_hook")
+
+    def sp_prefill(self, x_local, y_local, S_total: int, layout: int = 1, l0: int = 0, l1: Optional[int] = None,
+                   stats: bool = False, stream=None):
+        l1 = self.dims.n_layers if l1 is None else l1
+        st = SpStats()
+        _check(lib().zdc_sp_prefill(self.h, l0, l1, _tptr(x_local, "bf16"), _tptr(y_local, "bf16"),
+                                    x_local.shape[0], S_total, layout, ctypes.byref(st) if stats else None,
+                                    ctypes.c_void_p(_stream(stream))), "zdc_sp_prefill")
+        if stats:
+            return {"bytes_sent": st.bytes_sent, "bytes_recv": st.bytes_recv,
+                    "bytes_recv_uncompressed": st.bytes_recv_uncompressed, "exchange_ms": st.exchange_ms,
+                    "total_ms": st.total_ms}
+        return None
 
     def reset(self, stream=None):
         _check(lib().zdc_cache_reset(self.h, ctypes.c_void_p(_stream(stream))), "zdc_cache_reset")

@@ -110,6 +110,7 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
   c->importance_mode = plan->importance_mode;
   c->layers.resize(d.n_layers);
   c->len.assign(d.n_layers, 0);
+  c->sp_layer.assign(d.n_layers, 0);
   int64_t woff = 0, coff = 0;
   int max_nq = 0, max_ko = 0, max_rv = 0, max_split_w = 0;
   bool any_split = false;
@@ -243,6 +244,7 @@ zdc_status zdc_ctx_bind(zdc_ctx* c, void* w, void* cache, void* scratch) {
   ZDC_CUDA_TRY(cudaMemset(c->scratch, 0, c->scratch_bytes));
   ZDC_CUDA_TRY(cudaMemset(c->w, 0, c->weight_bytes));
   c->len.assign(c->dims.n_layers, 0);
+  c->sp_layer.assign(c->dims.n_layers, 0);
   c->batch = 0;
   return ZDC_OK;
 }
@@ -568,6 +570,8 @@ zdc_status zdc_decode(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, uin
   for (int l = l0; l < l1; ++l) {
     if (c->len[l] + 1 > c->max_seq)
       return fail(ZDC_ERR_CAPACITY, "zdc_decode: layer %d len %d + 1 > max_seq %d", l, c->len[l], c->max_seq);
+    if (c->sp_layer[l])
+      return fail(ZDC_ERR_UNSUPPORTED, "zdc_decode: layer %d holds an SP-sharded cache (SP decode is NEXT-2)", l);
     const LayerInfo& L = c->layers[l];
     if (L.split && L.rep != l) {
       // the representative must have classified this position (in this call or an earlier one)
@@ -634,6 +638,7 @@ zdc_status zdc_cache_reset(zdc_ctx* c, void* stream) {
   ZDC_CUDA_TRY(cudaMemsetAsync(c->len_dev(), 0, static_cast<size_t>(c->dims.n_layers) * 4,
                                static_cast<cudaStream_t>(stream)));
   c->len.assign(c->dims.n_layers, 0);
+  c->sp_layer.assign(c->dims.n_layers, 0);
   c->batch = 0;
   return ZDC_OK;
 }
@@ -650,6 +655,7 @@ zdc_status zdc_cache_export(const zdc_ctx* c, int32_t layer, float* k, float* v,
   if (!c) return fail(ZDC_ERR_INVALID_ARG, "zdc_cache_export: null ctx");
   if (!c->cache) return fail(ZDC_ERR_STATE, "zdc_cache_export: ctx not bound");
   if (layer < 0 || layer >= c->dims.n_layers) return fail(ZDC_ERR_SHAPE, "zdc_cache_export: layer %d", layer);
+  if (c->sp_layer[layer]) return fail(ZDC_ERR_UNSUPPORTED, "zdc_cache_export: layer %d holds an SP gather buffer", layer);
   const LayerInfo& L = c->layers[layer];
   const int B = c->batch, len = c->len[layer], Nkv = c->dims.n_kv_heads, S_cap = c->max_seq;
   cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -70,7 +70,21 @@ __global__ void __launch_bounds__(192, 1)
   const int kv_end = a.q_pos0 + last_q + 1;                   // keys [0, kv_end) are visible to some row
   const int n_kv = (kv_end + C::BN - 1) / C::BN;
   const int q_row = b * a.S + a.q_row0 + q0;                  // row in the Q'/O' matrices
-  const int kv_row0 = (b * a.Nkv + g) * a.S_cap;              // row of key 0 in the K'/V' buffers
+  // row of the first key of KV tile j in the K'/V' tensor maps (V row = K row + v_row_off)
+  auto kv_tile_row = [&](int j) -> int {
+    const int pos = j * C::BN;
+    if (a.kv_mode == 0) return (b * a.Nkv + g) * a.S_cap + pos;
+    const int q = pos / a.sp_chunk, r = pos - q * a.sp_chunk;   // SP gather buffer
+    int owner, local;
+    if (!a.sp_zigzag) {
+      owner = q;
+      local = r;
+    } else {
+      owner = q < a.sp_P ? q : 2 * a.sp_P - 1 - q;
+      local = (q < a.sp_P ? 0 : a.sp_chunk) + r;
+    }
+    return ((owner * 2 * a.B + b) * a.Nkv + g) * a.sp_n_local + local;
+  };
   const uint32_t warp = warp_id(), lane = lane_id();
 
   if (warp == 4) {
@@ -115,13 +129,13 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
         for (int c = 0; c < C::NCH; ++c)
           tma_load_2d_hint(smem + C::OFF_K + s * C::TILE + c * C::CHUNK, &tk, &k_full[s], c * C::CW,
-                           kv_row0 + j * C::BN, keep);
+                           kv_tile_row(j), keep);
         mbar_wait(&v_empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&v_full[s], C::TILE);
 #pragma unroll
         for (int c = 0; c < C::NCH; ++c)
           tma_load_2d_hint(smem + C::OFF_V + s * C::TILE + c * C::CHUNK, &tv, &v_full[s], c * C::CW,
-                           kv_row0 + j * C::BN, keep);
+                           static_cast<int>(kv_tile_row(j) + a.v_row_off), keep);
       }
     }
   } else if (warp == 5) {
@@ -288,7 +302,8 @@ static cudaError_t launch_attn_t(const PrefillAttnArgs& a, cudaStream_t stream) 
   }
   CUtensorMap tq, tk, tv;
   const uint64_t q_rows = static_cast<uint64_t>(a.B) * a.S;
-  const uint64_t kv_rows = static_cast<uint64_t>(a.B) * a.Nkv * a.S_cap;
+  const uint64_t kv_rows = a.kv_rows_total ? static_cast<uint64_t>(a.kv_rows_total)
+                                           : static_cast<uint64_t>(a.B) * a.Nkv * a.S_cap;
   if (!make_tmap_2d(&tq, a.q, static_cast<uint64_t>(a.ldq), q_rows, a.ldq * 2, C::CW, C::BM, C::SWB))
     return cudaErrorInvalidValue;
   if (!make_tmap_2d(&tk, a.k, HD, kv_rows, HD * 2, C::CW, C::BN, C::SWB)) return cudaErrorInvalidValue;

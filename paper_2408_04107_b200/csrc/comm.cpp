@@ -1,18 +1,298 @@
-// comm.cpp — placeholder for the sequence-parallel exchange.
+// comm.cpp — a6: sequence-parallel prefill that exchanges ONLY the compressed K'/V'
+// (§5.3: "transmitting compressed Q, K, and V tensors ... significantly reduces
+// communication time overhead"; this build all-gathers K'/V', reading c17).
+//
+// Per layer, on rank p of P (one process per GPU):
+//   a1  local tokens -> Q' (staging) and K'/V' written by the GEMM epilogue straight into this
+//       rank's slot of the gather buffer [P][K|V][B][N_kv][n_local][r] (no pack pass)
+//   a6  in-place ncclAllGather of the slots over NVLink (bytes = (P-1)/P B S N_kv (r_k+r_v) 2)
+//   a3  local queries (global positions: contiguous or zigzag) attend to every key at or before
+//       them; the tcgen05 attention kernel maps key tiles to (owner rank, local row) itself
+//   a5  local rows -> y_local
+// NCCL is resolved at run time (dlopen of libnccl.so.2, i.e. the copy torch already loaded), so
+// the library has no link-time NCCL dependency.  zdc_sp_set_exchange_hook replaces the NCCL
+// all-gather by a caller callback for single-GPU multi-process tests.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
 #include "api_util.h"
 #include "ctx.h"
+#include "kernels.h"
+
+typedef void (*zdc_exchange_fn)(void* user, void* gather_buf, int64_t chunk_bytes, int32_t rank, int32_t world,
+                                void* stream);
+
 namespace zdc {
-void comm_destroy(zdc_ctx*) {}
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+static NcclApi* nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      api.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (api.h) break;
+    }
+    if (!api.h) return;
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(api.h, "ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(api.h, "ncclCommInitRank"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(api.h, "ncclCommDestroy"));
+    api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(api.h, "ncclAllGather"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(api.h, "ncclGetErrorString"));
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather && api.GetErrorString;
+  });
+  return &api;
+}
+
+struct CommState {
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  zdc_exchange_fn hook = nullptr;
+  void* hook_user = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
+
+void comm_destroy(zdc_ctx* c) {
+  if (!c->comm) return;
+  if (c->comm->comm && nccl_api()->ok) nccl_api()->CommDestroy(c->comm->comm);
+  if (c->comm->e0) cudaEventDestroy(c->comm->e0);
+  if (c->comm->e1) cudaEventDestroy(c->comm->e1);
+  delete c->comm;
+  c->comm = nullptr;
+}
+
+// global position of local token t on rank p (layout 0 contiguous, 1 zigzag)
+static inline int sp_position(int S, int P, int p, int layout, int t) {
+  const int n = S / P;
+  if (layout == 0) return p * n + t;
+  const int c = S / (2 * P);
+  return t < c ? p * c + t : (2 * P - 1 - p) * c + (t - c);
+}
+
 }  // namespace zdc
+
+using namespace zdc;
+
 extern "C" {
-zdc_status zdc_comm_init(zdc_ctx*, const void*, int32_t, int32_t) {
-  return zdc::fail(ZDC_ERR_UNSUPPORTED, "zdc_comm_init: not built yet");
+
+zdc_status zdc_comm_unique_id(void* out) {
+  if (!out) return fail(ZDC_ERR_INVALID_ARG, "zdc_comm_unique_id: null output");
+  NcclApi* api = nccl_api();
+  if (!api->ok) return fail(ZDC_ERR_NCCL, "zdc_comm_unique_id: libnccl.so.2 not loadable");
+  ncclUniqueId id;
+  ncclResult_t r = api->GetUniqueId(&id);
+  if (r != ncclSuccess) return fail(ZDC_ERR_NCCL, "ncclGetUniqueId: %s", api->GetErrorString(r));
+  std::memcpy(out, &id, sizeof(id));
+  return ZDC_OK;
 }
-zdc_status zdc_sp_prefill(zdc_ctx*, int32_t, int32_t, const uint16_t*, uint16_t*, int32_t, int32_t, int32_t,
-                          zdc_sp_stats*, void*) {
-  return zdc::fail(ZDC_ERR_UNSUPPORTED, "zdc_sp_prefill: not built yet");
+
+zdc_status zdc_comm_init(zdc_ctx* c, const void* uid, int32_t rank, int32_t world) {
+  if (!c || !uid) return fail(ZDC_ERR_INVALID_ARG, "zdc_comm_init: null argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(ZDC_ERR_INVALID_ARG, "zdc_comm_init: rank %d world %d", rank, world);
+  NcclApi* api = nccl_api();
+  if (!api->ok) return fail(ZDC_ERR_NCCL, "zdc_comm_init: libnccl.so.2 not loadable");
+  comm_destroy(c);
+  c->comm = new CommState();
+  c->comm->rank = rank;
+  c->comm->world = world;
+  ncclUniqueId id;
+  std::memcpy(&id, uid, sizeof(id));
+  ncclResult_t r = api->CommInitRank(&c->comm->comm, world, id, rank);
+  if (r != ncclSuccess) {
+    comm_destroy(c);
+    return fail(ZDC_ERR_NCCL, "ncclCommInitRank: %s", api->GetErrorString(r));
+  }
+  ZDC_CUDA_TRY(cudaEventCreate(&c->comm->e0));
+  ZDC_CUDA_TRY(cudaEventCreate(&c->comm->e1));
+  return ZDC_OK;
 }
-zdc_status zdc_sp_positions(int32_t, int32_t, int32_t, int32_t, int32_t*) {
-  return zdc::fail(ZDC_ERR_UNSUPPORTED, "zdc_sp_positions: not built yet");
+
+zdc_status zdc_sp_set_exchange_hook(zdc_ctx* c, zdc_exchange_fn fn, void* user, int32_t rank, int32_t world) {
+  if (!c || !fn) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_set_exchange_hook: null argument");
+  if (world < 1 || rank < 0 || rank >= world)
+    return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_set_exchange_hook: rank %d world %d", rank, world);
+  comm_destroy(c);
+  c->comm = new CommState();
+  c->comm->rank = rank;
+  c->comm->world = world;
+  c->comm->hook = fn;
+  c->comm->hook_user = user;
+  ZDC_CUDA_TRY(cudaEventCreate(&c->comm->e0));
+  ZDC_CUDA_TRY(cudaEventCreate(&c->comm->e1));
+  return ZDC_OK;
 }
+
+zdc_status zdc_sp_positions(int32_t S_total, int32_t world, int32_t rank, int32_t layout, int32_t* positions) {
+  if (!positions) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_positions: null output");
+  if (world < 1 || rank < 0 || rank >= world || (layout != 0 && layout != 1))
+    return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_positions: rank %d world %d layout %d", rank, world, layout);
+  if (S_total <= 0 || S_total % (layout == 1 ? 2 * world : world) != 0)
+    return fail(ZDC_ERR_SHAPE, "zdc_sp_positions: S_total %d not divisible by %d", S_total,
+                layout == 1 ? 2 * world : world);
+  const int n = S_total / world;
+  for (int t = 0; t < n; ++t) positions[t] = sp_position(S_total, world, rank, layout, t);
+  return ZDC_OK;
 }
+
+zdc_status zdc_sp_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, uint16_t* y, int32_t B,
+                          int32_t S_total, int32_t layout, zdc_sp_stats* stats, void* stream) {
+  if (!c || !x || !y) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_prefill: null argument");
+  if (x == y) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_prefill: x and y alias");
+  if (!c->w) return fail(ZDC_ERR_STATE, "zdc_sp_prefill: ctx not bound");
+  if (!c->comm) return fail(ZDC_ERR_STATE, "zdc_sp_prefill: zdc_comm_init not called");
+  if (l0 < 0 || l1 > c->dims.n_layers || l0 >= l1)
+    return fail(ZDC_ERR_SHAPE, "zdc_sp_prefill: layer range [%d, %d)", l0, l1);
+  const int P = c->comm->world, p = c->comm->rank;
+  if (layout != 0 && layout != 1) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_prefill: layout %d", layout);
+  const int parts = layout == 1 ? 2 * P : P;
+  if (B <= 0 || S_total <= 0 || S_total % parts != 0)
+    return fail(ZDC_ERR_SHAPE, "zdc_sp_prefill: S_total %d not divisible by %d (%s layout)", S_total, parts,
+                layout == 1 ? "zigzag" : "contiguous");
+  const int n_local = S_total / P;
+  const int chunk = S_total / parts;
+  if (P > 1 && chunk % 128 != 0)
+    return fail(ZDC_ERR_UNSUPPORTED, "zdc_sp_prefill: sequence chunk %d is not a multiple of the 128-key tile", chunk);
+  if (B > c->max_batch || S_total > c->max_seq)
+    return fail(ZDC_ERR_CAPACITY, "zdc_sp_prefill: B=%d S_total=%d exceeds max_batch=%d max_seq=%d", B, S_total,
+                c->max_batch, c->max_seq);
+  for (int l = l0; l < l1; ++l) {
+    if (c->layers[l].split) return fail(ZDC_ERR_UNSUPPORTED, "zdc_sp_prefill: token split under SP is NEXT-2 (layer %d)", l);
+    if (c->len[l] != 0) return fail(ZDC_ERR_STATE, "zdc_sp_prefill: layer %d cache is not empty", l);
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int d = c->dims.d_model, Nh = c->dims.n_heads, Nkv = c->dims.n_kv_heads;
+  const int M = B * n_local;
+  g_launches = 0;
+  float exch_ms = 0.f;
+  int64_t bytes_recv = 0, bytes_recv_unc = 0;
+  cudaEvent_t t_begin = nullptr, t_end = nullptr;
+  if (stats) {
+    ZDC_CUDA_TRY(cudaEventCreate(&t_begin));
+    ZDC_CUDA_TRY(cudaEventCreate(&t_end));
+    ZDC_CUDA_TRY(cudaEventRecord(t_begin, s));
+  }
+  for (int l = l0; l < l1; ++l) {
+    const LayerInfo& L = c->layers[l];
+    const uint16_t* xin = l == l0 ? x : y;
+    uint16_t* gbuf = reinterpret_cast<uint16_t*>(c->cache + L.k_off);  // [P][K|V][B][Nkv][n_local][r]
+    const int64_t slot_rows = static_cast<int64_t>(B) * Nkv * n_local;
+    const int64_t chunk_elems = 2 * slot_rows * L.rk_p;
+    // a1 + a2: epilogue writes this rank's K'/V' slot of the gather buffer
+    Epilogue e1;
+    e1.mode = 1;
+    QkvDest& q = e1.qkv;
+    q.q = reinterpret_cast<uint16_t*>(c->scratch + c->s_q);
+    q.ldq = L.nq;
+    q.nq = L.nq;
+    q.nk = L.nk;
+    q.k = gbuf + p * chunk_elems;
+    q.v = q.k + slot_rows * L.rk_p;
+    q.rk = L.rk_p;
+    q.rv = L.rv_p;
+    q.S = n_local;
+    q.kg = static_cast<int64_t>(n_local) * L.rk_p;
+    q.kb = q.kg * Nkv;
+    q.vg = static_cast<int64_t>(n_local) * L.rv_p;
+    q.vb = q.vg * Nkv;
+    q.pos0 = 0;
+    g_prof_class = kProfGemmQkv;
+    ZDC_CUDA_TRY(launch_gemm(xin, d, reinterpret_cast<const uint16_t*>(c->w + L.w_qkv), d, M, L.n_qkv, d, e1, s));
+    // a6: in-place all-gather of the compressed K'/V' slots
+    const int64_t chunk_bytes = chunk_elems * 2;
+    if (P > 1) {
+      if (stats) ZDC_CUDA_TRY(cudaEventRecord(c->comm->e0, s));
+      if (c->comm->hook) {
+        c->comm->hook(c->comm->hook_user, gbuf, chunk_bytes, p, P, s);
+      } else {
+        ncclResult_t r = nccl_api()->AllGather(gbuf + p * chunk_elems, gbuf, static_cast<size_t>(chunk_bytes), ncclUint8,
+                                               c->comm->comm, s);
+        if (r != ncclSuccess) return fail(ZDC_ERR_NCCL, "ncclAllGather: %s", nccl_api()->GetErrorString(r));
+      }
+      if (stats) {
+        ZDC_CUDA_TRY(cudaEventRecord(c->comm->e1, s));
+        ZDC_CUDA_TRY(cudaEventSynchronize(c->comm->e1));
+        float ms = 0.f;
+        ZDC_CUDA_TRY(cudaEventElapsedTime(&ms, c->comm->e0, c->comm->e1));
+        exch_ms += ms;
+      }
+      bytes_recv += (P - 1) * chunk_bytes;
+      bytes_recv_unc += (P - 1) * 2 * slot_rows * c->dims.d_head * 2;
+    }
+    // a3: local query segments against every earlier key in the gathered buffer
+    const int segs = layout == 1 ? 2 : 1;
+    for (int sg = 0; sg < segs; ++sg) {
+      PrefillAttnArgs a;
+      a.q = reinterpret_cast<const uint16_t*>(c->scratch + c->s_q);
+      a.ldq = L.nq;
+      a.k = gbuf;
+      a.v = gbuf;
+      a.kv_mode = 1;
+      a.sp_P = P;
+      a.sp_n_local = n_local;
+      a.sp_chunk = chunk;
+      a.sp_zigzag = layout;
+      a.v_row_off = slot_rows;
+      a.kv_rows_total = static_cast<int64_t>(P) * 2 * slot_rows;
+      a.S_cap = n_local;
+      a.o = reinterpret_cast<uint16_t*>(c->scratch + c->s_o);
+      a.ldo = L.ko_p;
+      a.lse = reinterpret_cast<float*>(c->scratch + c->s_lse);
+      a.B = B;
+      a.S = n_local;
+      a.Nh = Nh;
+      a.Nkv = Nkv;
+      a.rk = L.rk_p;
+      a.rv = L.rv_p;
+      a.scale = 1.0f / std::sqrt(static_cast<float>(c->dims.d_head));
+      a.q_row0 = sg * chunk;
+      a.n_q = layout == 1 ? chunk : n_local;
+      a.q_pos0 = sp_position(S_total, P, p, layout, a.q_row0);
+      ZDC_CUDA_TRY(launch_prefill_attention(a, s));
+    }
+    // a5
+    Epilogue e5;
+    e5.mode = 0;
+    e5.d = y;
+    e5.ldd = d;
+    g_prof_class = kProfGemmO;
+    ZDC_CUDA_TRY(launch_gemm(reinterpret_cast<const uint16_t*>(c->scratch + c->s_o), L.ko_p,
+                             reinterpret_cast<const uint16_t*>(c->w + L.w_o), L.ko_p, M, d, L.ko_p, e5, s));
+    g_prof_class = kProfOther;
+    c->len[l] = S_total;
+    c->sp_layer[l] = 1;
+    c->last_layer = l;
+    c->last_T = n_local;
+  }
+  c->batch = B;
+  if (stats) {
+    ZDC_CUDA_TRY(cudaEventRecord(t_end, s));
+    ZDC_CUDA_TRY(cudaEventSynchronize(t_end));
+    float tot = 0.f;
+    ZDC_CUDA_TRY(cudaEventElapsedTime(&tot, t_begin, t_end));
+    cudaEventDestroy(t_begin);
+    cudaEventDestroy(t_end);
+    stats->bytes_recv = bytes_recv;
+    stats->bytes_sent = bytes_recv;  // all-gather: each slot goes to the P-1 peers
+    stats->bytes_recv_uncompressed = bytes_recv_unc;
+    stats->exchange_ms = exch_ms;
+    stats->total_ms = tot;
+  }
+  return ZDC_OK;
+}
+
+}  // extern "C"

@@ -44,6 +44,7 @@ struct zdc_ctx {
   uint8_t* cache = nullptr;
   uint8_t* scratch = nullptr;
   std::vector<int> len;  // per-layer cache length
+  std::vector<int> sp_layer;  // 1 = the layer's cache holds an SP gather buffer (not position-ordered)
   int batch = 0;
   int last_layer = -1, last_T = 0;
   zdc::CommState* comm = nullptr;

@@ -62,6 +62,12 @@ struct PrefillAttnArgs {
   int q_pos0;          // global position of query row t is q_pos0 + t (SP chunks)
   int q_row0;          // first row of this chunk inside the Q'/O' matrices
   int n_q;             // number of query rows of this launch (per sequence)
+  // key addressing: kv_mode 0 = position-ordered rows (above); 1 = SP gather buffer
+  // [P][K|V][B][Nkv][sp_n_local][r]: key position -> (owner rank, local row) by the layout
+  int kv_mode = 0;
+  int sp_P = 1, sp_n_local = 0, sp_chunk = 0, sp_zigzag = 0;
+  int64_t v_row_off = 0;      // V row = K row + v_row_off (kv_mode 1: both maps share the base)
+  int64_t kv_rows_total = 0;  // rows of the K/V tensor maps (0 = B * Nkv * S_cap)
 };
 cudaError_t launch_prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream);
 

@@ -1,0 +1,108 @@
+"""zdc_sp_prefill on ONE GPU with P processes (one zdc_ctx each).  The exchange runs through the
+library's test transport (zdc_sp_set_exchange_hook: a gloo all-gather over host memory) instead of
+NCCL, which cannot put two ranks on one device; everything else is the production SP path: the a1
+epilogue writes each rank's compressed K'/V' slot, attention maps key tiles to (owner, local row)
+in the gather buffer, zigzag query chunks.  Checks (P11 layout invariance):
+* every rank's y rows are BIT-IDENTICAL to the single-process zdc_prefill rows of its positions
+  (same per-element GEMM K order and per-row key-tile order);
+* and within 2e-2 of the fp64 oracle."""
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _cudart():
+    for name in ("libcudart.so.12", "libcudart.so"):
+        try:
+            return ctypes.CDLL(name)
+        except OSError:
+            continue
+    raise OSError("libcudart not found")
+
+
+def _worker(rank, world, port, layout, S, B, out_q):
+    import torch.distributed as dist
+    import oracle as O  # noqa: F401
+    import paper_2408_04107_b200 as zdc
+    import zdc_synth as Z
+    from zdc_testlib import fold_stack, to_dev_bf16
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    dims = Z.Dims(2, 256, 4, 2, 64)
+    plan = Z.plan_uniform(2, 64)
+    _, folded = fold_stack(dims, 1, n_calib=256)
+    ctx = zdc.Context(dims, plan, B, S)
+    for l, f in enumerate(folded):
+        ctx.load_folded(l, f["wq_f"], f["wk_f"], f["wv_f"], f["wo_f"])
+    x = Z.prompt(dims, 1, B, S, seed=41)
+    pos = zdc.sp_positions(S, world, rank, layout)
+    cudart = _cudart()
+    cudart.cudaMemcpy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
+    cudart.cudaStreamSynchronize.argtypes = [ctypes.c_void_p]
+
+    def exchange(user, gbuf, chunk_bytes, r, P, stream):
+        cudart.cudaStreamSynchronize(stream)
+        mine = np.empty(chunk_bytes, dtype=np.uint8)
+        cudart.cudaMemcpy(mine.ctypes.data, gbuf + r * chunk_bytes, chunk_bytes, 2)   # D2H
+        parts = [torch.zeros(chunk_bytes, dtype=torch.uint8) for _ in range(P)]
+        dist.all_gather(parts, torch.from_numpy(mine))
+        for q in range(P):
+            cudart.cudaMemcpy(gbuf + q * chunk_bytes, parts[q].numpy().ctypes.data, chunk_bytes, 1)  # H2D
+
+    cb = zdc.EXCHANGE_FN(exchange)
+    ctx.set_exchange_hook(cb, rank, world)
+    xl = to_dev_bf16(np.ascontiguousarray(x[:, pos]))
+    yl = torch.empty_like(xl)
+    stats = ctx.sp_prefill(xl, yl, S_total=S, layout=layout, stats=True)
+    torch.cuda.synchronize()
+    out_q.put((rank, pos, yl.float().cpu().numpy(), stats))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,layout", [(2, 0), (2, 1), (4, 1)])
+def test_sp_prefill_equals_single_gpu_rows(world, layout):
+    import multiprocessing as pymp
+    import oracle as O
+    import paper_2408_04107_b200 as zdc
+    import zdc_synth as Z
+    from zdc_testlib import fold_stack, make_context, normwise, to_dev_bf16
+    B = 2
+    S = 256 * world * (2 if layout else 1)   # chunks of 128 (zigzag) / 256 (contiguous)
+    ctx_mp = pymp.get_context("spawn")
+    q = ctx_mp.Queue()
+    port = 29600 + world * 10 + layout + os.getpid() % 500
+    procs = [ctx_mp.Process(target=_worker, args=(r, world, port, layout, S, B, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    # single-process reference through zdc_prefill
+    dims = Z.Dims(2, 256, 4, 2, 64)
+    plan = Z.plan_uniform(2, 64)
+    _, folded = fold_stack(dims, 1, n_calib=256)
+    x = Z.prompt(dims, 1, B, S, seed=41)
+    ctx = make_context(dims, plan, folded, B, S)
+    xd = to_dev_bf16(x)
+    y = torch.empty_like(xd)
+    ctx.prefill(xd, y)
+    torch.cuda.synchronize()
+    y_single = y.float().cpu().numpy()
+    want = O.OracleModel(dims, plan, folded, faithful=True).prefill(x)
+    covered = []
+    for rank, pos, yl, stats in res:
+        assert np.array_equal(yl, y_single[:, pos]), rank      # bit-identical rows
+        assert normwise(yl, want[:, pos]) <= 2e-2
+        covered += pos.tolist()
+        # bytes received per rank and layer: (P-1)/P * B * S * N_kv * (r_k + r_v) * 2, two layers
+        assert stats["bytes_recv"] == 2 * O.sp_bytes_received(world, B, S, 2, 64, 64)
+        assert stats["bytes_recv_uncompressed"] == 2 * O.sp_bytes_received(world, B, S, 2, 128, 128)
+    assert sorted(covered) == list(range(S))
