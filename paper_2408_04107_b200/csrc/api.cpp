@@ -205,6 +205,8 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
   s = align_up(s + rows * d.n_heads * 4, 256);
   c->s_part = s;
   s = align_up(s + static_cast<int64_t>(max_batch) * d.n_heads * 128 * (max_rv + 2) * 4, 256);
+  c->s_cnt = s;  // decode-attention merge counters [max_batch][N_kv], kept at zero between launches
+  s = align_up(s + static_cast<int64_t>(max_batch) * d.n_kv_heads * 4, 256);
   if (any_split) {  // staged K'/V' of a split layer before packing, compaction indices, new-row staging
     const int64_t kv_rows = static_cast<int64_t>(max_batch) * d.n_kv_heads * max_seq;
     c->s_ks = s;
@@ -516,6 +518,7 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
     a.ldo = L.ko_p;
     a.lse = reinterpret_cast<float*>(c->scratch + c->s_lse);
     a.part = reinterpret_cast<float*>(c->scratch + c->s_part);
+    a.counters = reinterpret_cast<int*>(c->scratch + c->s_cnt);
     a.B = B;
     a.Nh = Nh;
     a.Nkv = Nkv;

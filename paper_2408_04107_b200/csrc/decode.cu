@@ -6,7 +6,8 @@
 //   decode_attn_partial    a3: split-K over the context ("flash decoding"); one CTA per
 //                          (chunk, KV head, sequence); the G = N_h/N_kv query heads of a KV
 //                          group share each K'/V' row load (GQA, reading c4).
-//   decode_attn_combine    LSE merge of the chunks -> O' (bf16) and the row LSE (f32).
+//                          The last CTA of each (sequence, KV head) LSE-merges the chunks -> O' (bf16)
+//                          and the row LSE (f32) (no separate combine launch).
 //   pack_weights_kernel    load-time truncation + zero padding + transposition of the folded
 //                          weights; never on the hot path.
 #include "common.cuh"
@@ -73,19 +74,29 @@ __device__ __forceinline__ uint16_t f32_to_bf16_bits(float f) {
 }
 
 // ------------------------------------------------------------------ skinny projection
+// pdl_mode bit 0: trigger the dependent launch only after this kernel's own wait (bounds the
+// look-ahead to one kernel); otherwise trigger at entry.  Weight rows are bulk-prefetched into L2
+// before the wait: they do not depend on the predecessor, so with PDL their HBM stream overlaps
+// the previous kernels of the decode step.
 template <int NB>
 __global__ void __launch_bounds__(256) gemv_kernel(const uint16_t* __restrict__ W, const uint16_t* __restrict__ x,
-                                                   int64_t ldx, int N, int K, const Epilogue epi) {
+                                                   int64_t ldx, int N, int K, const Epilogue epi, int pdl_mode) {
   extern __shared__ uint4 xs[];  // [NB][K/8] bf16 units
   const int kc = K >> 3;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (!(pdl_mode & 1)) pdl_trigger();
+  if (lane == 0)
+    for (int n = blockIdx.x * 8 + warp; n < N; n += gridDim.x * 8)
+      l2_prefetch(W + static_cast<int64_t>(n) * K, static_cast<uint32_t>(K) * 2u);
+  pdl_wait();
+  if (pdl_mode & 1) pdl_trigger();
   if (epi.len_inc && blockIdx.x == 0 && threadIdx.x == 0) *epi.len_inc += 1;
   for (int i = threadIdx.x; i < NB * kc; i += blockDim.x) {
     const int b = i / kc, c = i - b * kc;
     xs[i] = *reinterpret_cast<const uint4*>(x + b * ldx + c * 8);
   }
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int U = 8;
+  constexpr int U = 16;
   for (int n = blockIdx.x * 8 + warp; n < N; n += gridDim.x * 8) {
     const uint4* w = reinterpret_cast<const uint4*>(W + static_cast<int64_t>(n) * K);
     float acc[NB];
@@ -130,13 +141,15 @@ static cudaError_t launch_gemv_nb(const uint16_t* W, const uint16_t* x, int64_t 
     attr = true;
   }
   int blocks = (N + 7) / 8;
-  const int cap = num_sms() * 8;
+  const int cap = num_sms() * 2;
   if (blocks > cap) blocks = cap;
+  // the a1 projection (writes the staging read by attention) bounds the look-ahead
+  const int mode = epi.mode == 1 ? 1 : 0;
   prof_mark(stream, true, g_prof_class);
-  gemv_kernel<NB><<<blocks, 256, smem, stream>>>(W, x, ldx, N, K, epi);
+  cudaError_t e = launch_k(gemv_kernel<NB>, dim3(blocks), dim3(256), smem, stream, g_pdl, W, x, ldx, N, K, epi, mode);
   prof_mark(stream, false, g_prof_class);
   ++g_launches;
-  return cudaGetLastError();
+  return e;
 }
 
 cudaError_t launch_gemv(const uint16_t* W, const uint16_t* x, int64_t ldx, int B, int N, int K, const Epilogue& epi,
@@ -174,8 +187,24 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
   __shared__ float sc[G][kMaxChunk];
   __shared__ float red[4][G][RV];
   __shared__ float stat[2][4][G];
+  __shared__ int s_last;
   const int split = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row0 = (static_cast<int64_t>(b) * a.Nkv + g) * a.S_cap;
+  const float scl = a.scale * kLog2e;
+  pdl_trigger();
+  if (a.n0_ptr == nullptr && threadIdx.x == 0) {
+    // uniform cache: the length is final before the predecessor (the a1 projection) runs, so the
+    // chunk's cached rows can stream into L2 while it finishes (the new row is re-read after the wait)
+    const int len0 = a.len_ptr ? *a.len_ptr + 1 : a.len;
+    const int ch0 = (len0 + a.splits - 1) / a.splits;
+    const int p0 = split * ch0, p1 = min(len0 - 1, p0 + ch0);
+    if (p1 > p0) {
+      l2_prefetch(kp + (row0 + p0) * RK, static_cast<uint32_t>(p1 - p0) * RK * 2u);
+      l2_prefetch(vp + (row0 + p0) * RV, static_cast<uint32_t>(p1 - p0) * RV * 2u);
+    }
+  }
+  pdl_wait();
   int len;
   if (pool == 0)
     len = a.n0_ptr ? a.n0_ptr[b] : (a.len_ptr ? *a.len_ptr + 1 : a.len);
@@ -185,8 +214,6 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
   const int s0 = split * chunk;
   const int s1 = min(len, s0 + chunk);
   const int n = max(0, s1 - s0);
-  const float scl = a.scale * kLog2e;
-  const int64_t row0 = (static_cast<int64_t>(b) * a.Nkv + g) * a.S_cap;
 
   // ---- scores s = q . k * scale * log2(e), all G heads of the group per K' row load
   {
@@ -301,36 +328,48 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
       dst[RVO + 1] = n > 0 ? l : 0.f;
     }
   }
-}
-
-// Merge the partials of one (sequence, head): O' = sum_s o_s 2^(m_s - M) / sum_s l_s 2^(m_s - M),
-// LSE = (M + log2 L) ln 2 (natural log of the Eq. 3 denominator).
-__global__ void __launch_bounds__(128) decode_attn_combine(const DecodeAttnArgs a, int nslots) {
-  const int h = blockIdx.x, b = blockIdx.y;
-  const int RV = a.rv;
-  const float* part = a.part + (static_cast<int64_t>(b) * a.Nh + h) * nslots * (RV + 2);
-  __shared__ float w[128];
-  __shared__ float tot;
+  // ---- the last CTA of this (sequence, KV head) merges every partial (replaces a combine launch):
+  // O' = sum_s o_s 2^(m_s - M) / sum_s l_s 2^(m_s - M), LSE = (M + log2 L) ln 2
+  __threadfence();
+  __syncthreads();
   if (threadIdx.x == 0) {
-    float M = -INFINITY;
-    for (int s = 0; s < nslots; ++s) M = fmaxf(M, part[s * (RV + 2) + RV]);
-    float L = 0.f;
-    for (int s = 0; s < nslots; ++s) {
-      const float m = part[s * (RV + 2) + RV];
-      const float ws = m == -INFINITY ? 0.f : exp2f(m - M);
-      w[s] = ws;
-      L += ws * part[s * (RV + 2) + RV + 1];
-    }
-    tot = L;
-    if (a.lse) a.lse[b * a.Nh + h] = (M + log2f(L)) / kLog2e;
+    const int prev = atomicAdd(&a.counters[b * a.Nkv + g], 1);
+    s_last = prev == nslots - 1;
   }
   __syncthreads();
-  const float inv = 1.f / tot;
-  for (int c = threadIdx.x; c < RV; c += blockDim.x) {
-    float o = 0.f;
-    for (int s = 0; s < nslots; ++s) o = fmaf(w[s], part[s * (RV + 2) + c], o);
-    a.o[b * a.ldo + h * RV + c] = f32_to_bf16_bits(o * inv);
+  if (!s_last) return;
+  __threadfence();
+  float* wts = &sc[0][0];  // reuse: [G][nslots] merge weights (nslots <= 128 <= kMaxChunk)
+#pragma unroll 1
+  for (int gi = 0; gi < G; ++gi) {
+    const float* hp = a.part + ((static_cast<int64_t>(b) * a.Nh + g * G + gi) * nslots) * (RVO + 2);
+    float m = threadIdx.x < nslots ? __ldcg(hp + threadIdx.x * (RVO + 2) + RVO) : -INFINITY;
+    float mm = m;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, off));
+    if (lane == 0) stat[0][warp][gi] = mm;
+    __syncthreads();
+    const float M = fmaxf(fmaxf(stat[0][0][gi], stat[0][1][gi]), fmaxf(stat[0][2][gi], stat[0][3][gi]));
+    float wl = 0.f;
+    if (threadIdx.x < nslots) {
+      const float w = m == -INFINITY ? 0.f : exp2f(m - M);
+      wts[gi * 128 + threadIdx.x] = w;
+      wl = w * __ldcg(hp + threadIdx.x * (RVO + 2) + RVO + 1);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) wl += __shfl_xor_sync(0xffffffffu, wl, off);
+    if (lane == 0) stat[1][warp][gi] = wl;
+    __syncthreads();
+    const float L = stat[1][0][gi] + stat[1][1][gi] + stat[1][2][gi] + stat[1][3][gi];
+    const float inv = 1.f / L;
+    for (int c = threadIdx.x; c < RVO; c += 128) {
+      float o = 0.f;
+      for (int s2 = 0; s2 < nslots; ++s2) o = fmaf(wts[gi * 128 + s2], __ldcg(hp + s2 * (RVO + 2) + c), o);
+      a.o[b * a.ldo + (g * G + gi) * RVO + c] = f32_to_bf16_bits(o * inv);
+    }
+    if (threadIdx.x == 0 && a.lse) a.lse[b * a.Nh + g * G + gi] = (M + log2f(L)) / kLog2e;
   }
+  if (threadIdx.x == 0) a.counters[b * a.Nkv + g] = 0;
 }
 
 int decode_splits(int B, int Nkv, int len) {
@@ -349,7 +388,7 @@ template <int RK, int G>
 static void launch_partial_t(const DecodeAttnArgs& a, const uint16_t* kp, const uint16_t* vp, int pool, int slot0,
                              int nslots, cudaStream_t stream) {
   dim3 grid(a.splits, a.Nkv, a.B);
-  decode_attn_partial<RK, RK, G><<<grid, 128, 0, stream>>>(a, kp, vp, pool, slot0, nslots);
+  launch_k(decode_attn_partial<RK, RK, G>, grid, dim3(128), 0, stream, g_pdl, a, kp, vp, pool, slot0, nslots);
 }
 
 template <int G>
@@ -385,15 +424,13 @@ cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t stream
   if (a.splits > 64 || (a.len + a.splits - 1) / a.splits > kMaxChunk) return cudaErrorInvalidValue;
   if (a.rk != a.rv || (a.k1 && a.rk1 != a.rv1)) return cudaErrorInvalidValue;
   const int nslots = a.splits * (a.k1 ? 2 : 1);
+  if (nslots > 128 || !a.counters) return cudaErrorInvalidValue;
   prof_mark(stream, true, kProfAttnDecode);
   cudaError_t e = launch_partial(a, a.rk, a.k, a.v, 0, 0, nslots, stream);
   if (e == cudaSuccess && a.k1) e = launch_partial(a, a.rk1, a.k1, a.v1, 1, a.splits, nslots, stream);
   prof_mark(stream, false, kProfAttnDecode);
+  g_launches += a.k1 ? 2 : 1;
   if (e != cudaSuccess) return e;
-  prof_mark(stream, true, kProfAttnCombine);
-  decode_attn_combine<<<dim3(a.Nh, a.B), 128, 0, stream>>>(a, nslots);
-  prof_mark(stream, false, kProfAttnCombine);
-  g_launches += a.k1 ? 3 : 2;
   return cudaGetLastError();
 }
 

@@ -21,6 +21,7 @@
 namespace zdc {
 
 int64_t g_launches = 0;
+bool g_pdl = true;
 int g_prof_class = kProfOther;
 
 // ------------------------------------------------------------------ host: per-class event timing

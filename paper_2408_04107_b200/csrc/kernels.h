@@ -93,6 +93,7 @@ struct DecodeAttnArgs {
   int64_t ldo = 0;
   float* lse = nullptr;   // [B][Nh]
   float* part = nullptr;  // scratch [B][Nh][2 * splits][rv + 2]
+  int* counters = nullptr;  // scratch [B][Nkv] zero-initialised; the last CTA per (b, g) merges
   int B = 0, Nh = 0, Nkv = 0;
   float scale = 0.f;
   int splits = 1;
@@ -127,6 +128,25 @@ cudaError_t launch_classify(const float* lse, int Nh, int mode, const float* tau
                             int* pos_u, const int* len_ptr, int B, cudaStream_t s);
 
 extern int64_t g_launches;  // kernels enqueued by the last API call
+extern bool g_pdl;          // launch decode kernels with programmatic stream serialization
+
+// Launch with the programmatic-dependent-launch attribute (when pdl): the kernel may start while
+// its predecessor is still running; it must call pdl_wait() before reading the predecessor's output.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                     Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = pdl ? attr : nullptr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 // ---- per-kernel-class timing (zdc_profile): CUDA events bracket each launch on its stream
 enum ProfClass { kProfGemmQkv = 0, kProfAttnPrefill, kProfGemmO, kProfGemvQkv, kProfAttnDecode, kProfAttnCombine,

@@ -36,7 +36,7 @@ def _worker(rank, world, port, layout, S, B, out_q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     dims = Z.Dims(2, 256, 4, 2, 64)
-    plan = Z.plan_uniform(2, 64)
+    plan = Z.plan_uniform(2, 32)
     _, folded = fold_stack(dims, 1, n_calib=256)
     ctx = zdc.Context(dims, plan, B, S)
     for l, f in enumerate(folded):
@@ -87,7 +87,7 @@ def test_sp_prefill_equals_single_gpu_rows(world, layout):
         assert p.exitcode == 0
     # single-process reference through zdc_prefill
     dims = Z.Dims(2, 256, 4, 2, 64)
-    plan = Z.plan_uniform(2, 64)
+    plan = Z.plan_uniform(2, 32)
     _, folded = fold_stack(dims, 1, n_calib=256)
     x = Z.prompt(dims, 1, B, S, seed=41)
     ctx = make_context(dims, plan, folded, B, S)
@@ -103,6 +103,7 @@ def test_sp_prefill_equals_single_gpu_rows(world, layout):
         assert normwise(yl, want[:, pos]) <= 2e-2
         covered += pos.tolist()
         # bytes received per rank and layer: (P-1)/P * B * S * N_kv * (r_k + r_v) * 2, two layers
-        assert stats["bytes_recv"] == 2 * O.sp_bytes_received(world, B, S, 2, 64, 64)
-        assert stats["bytes_recv_uncompressed"] == 2 * O.sp_bytes_received(world, B, S, 2, 128, 128)
+        assert stats["bytes_recv"] == 2 * O.sp_bytes_received(world, B, S, 2, 32, 32)
+        # r / d_head = 32 / 64 of the uncompressed K/V bytes
+        assert stats["bytes_recv_uncompressed"] == 2 * O.sp_bytes_received(world, B, S, 2, 64, 64)
     assert sorted(covered) == list(range(S))
