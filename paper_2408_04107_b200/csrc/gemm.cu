@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -21,7 +22,7 @@
 namespace zdc {
 
 int64_t g_launches = 0;
-bool g_pdl = true;
+bool g_pdl = getenv("ZDC_NO_PDL") == nullptr;  // A/B switch for programmatic dependent launch
 int g_prof_class = kProfOther;
 
 // ------------------------------------------------------------------ host: per-class event timing
