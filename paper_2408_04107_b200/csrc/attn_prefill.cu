@@ -603,7 +603,9 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
-bool g_attn_v2 = getenv("ZDC_ATTN_V1") == nullptr;  // A/B switch: ZDC_ATTN_V1=1 selects the one-tile kernel
+// A/B switch: ZDC_ATTN_V2=1 selects the two-tile kernel (measured slower than v1 so far: 103 vs 80 us
+// per c2 layer, profiles/r01).
+bool g_attn_v2 = getenv("ZDC_ATTN_V2") != nullptr;
 
 template <int HD>
 static cudaError_t launch_attn2_t(const PrefillAttnArgs& a, cudaStream_t stream) {

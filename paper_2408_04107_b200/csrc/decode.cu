@@ -130,23 +130,110 @@ __global__ void __launch_bounds__(256) gemv_kernel(const uint16_t* __restrict__ 
   }
 }
 
+// TMA-staged version (the one launched): one CTA per SM owns a contiguous block of weight rows.
+// Warp 8 keeps a ring of row slots in shared memory full with cp.async.bulk copies; the first
+// `slots` rows are issued BEFORE the PDL wait (weights do not depend on the predecessor), so they
+// stream in while the previous decode kernels run.  Warps 0-7 wait for the predecessor, stage x,
+// and reduce one row per warp from shared memory.
+template <int NB>
+__global__ void __launch_bounds__(288, 1)
+    gemv_ring_kernel(const uint16_t* __restrict__ W, const uint16_t* __restrict__ x, int64_t ldx, int N, int K,
+                     const Epilogue epi, int pdl_mode, int slots) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  const int row_bytes = K * 2;
+  const int kc = K >> 3;
+  uint8_t* ring = smem_raw;
+  uint4* xs = reinterpret_cast<uint4*>(smem_raw + static_cast<size_t>(slots) * row_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + static_cast<size_t>(slots) * row_bytes +
+                                               static_cast<size_t>(NB) * row_bytes);
+  uint64_t* empty = full + slots;
+  const int per = (N + gridDim.x - 1) / gridDim.x;
+  const int r0 = blockIdx.x * per;
+  const int nrows = max(0, min(N, r0 + per) - r0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 256) {
+    for (int s = 0; s < slots; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (!(pdl_mode & 1)) pdl_trigger();
+  if (warp == 8) {
+    // ---- producer: weight rows HBM -> smem ring (independent of the predecessor: no wait)
+    if (lane == 0) {
+      for (int i = 0; i < nrows; ++i) {
+        const int s = i % slots;
+        if (i >= slots) mbar_wait(&empty[s], ((i / slots) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[s], row_bytes);
+        bulk_g2s(ring + static_cast<size_t>(s) * row_bytes, W + static_cast<int64_t>(r0 + i) * K, row_bytes,
+                 &full[s]);
+      }
+    }
+    return;
+  }
+  // ---- consumers
+  pdl_wait();
+  if (pdl_mode & 1) pdl_trigger();
+  if (epi.len_inc && blockIdx.x == 0 && threadIdx.x == 0) *epi.len_inc += 1;
+  for (int i = threadIdx.x; i < NB * kc; i += 256) {
+    const int b = i / kc, c = i - b * kc;
+    xs[i] = *reinterpret_cast<const uint4*>(x + b * ldx + c * 8);
+  }
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+  for (int i = warp; i < nrows; i += 8) {
+    const int s = i % slots;
+    mbar_wait(&full[s], (i / slots) & 1);
+    const uint4* w = reinterpret_cast<const uint4*>(ring + static_cast<size_t>(s) * row_bytes);
+    float acc[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc[b] = 0.f;
+#pragma unroll 4
+    for (int c = lane; c < kc; c += 32) {
+      const uint4 wv = w[c];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) acc[b] += dot8(wv, xs[b * kc + c]);
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], off);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&empty[s]);
+#pragma unroll
+      for (int b = 0; b < NB; ++b) store_scalar(epi, b, r0 + i, f32_to_bf16_bits(acc[b]));
+    }
+  }
+}
+
+static constexpr int kGemvRingBytes = 96 * 1024;  // leaves room for the next kernel's CTAs (PDL)
+
 template <int NB>
 static cudaError_t launch_gemv_nb(const uint16_t* W, const uint16_t* x, int64_t ldx, int N, int K, const Epilogue& epi,
                                   cudaStream_t stream) {
-  const size_t smem = static_cast<size_t>(NB) * K * 2;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemv_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaError_t e =
+        cudaFuncSetAttribute(gemv_ring_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   int blocks = (N + 7) / 8;
-  const int cap = num_sms() * 2;
-  if (blocks > cap) blocks = cap;
+  if (blocks > num_sms()) blocks = num_sms();
+  const int per = (N + blocks - 1) / blocks;
+  int slots = kGemvRingBytes / (K * 2);
+  if (slots > per) slots = per;
+  if (slots < 1) slots = 1;
+  const size_t smem = static_cast<size_t>(slots) * K * 2 + static_cast<size_t>(NB) * K * 2 + 16 * slots + 16;
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
   // the a1 projection (writes the staging read by attention) bounds the look-ahead
   const int mode = epi.mode == 1 ? 1 : 0;
   prof_mark(stream, true, g_prof_class);
-  cudaError_t e = launch_k(gemv_kernel<NB>, dim3(blocks), dim3(256), smem, stream, g_pdl, W, x, ldx, N, K, epi, mode);
+  cudaError_t e = launch_k(gemv_ring_kernel<NB>, dim3(blocks), dim3(288), smem, stream, g_pdl, W, x, ldx, N, K, epi,
+                           mode, slots);
   prof_mark(stream, false, g_prof_class);
   ++g_launches;
   return e;
@@ -192,16 +279,34 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row0 = (static_cast<int64_t>(b) * a.Nkv + g) * a.S_cap;
   const float scl = a.scale * kLog2e;
+  // the chunk's K'/V' rows (contiguous in the cache) are staged in shared memory by two bulk copies
+  extern __shared__ __align__(128) uint8_t dsm[];
+  const int cmax = (a.len + a.splits - 1) / a.splits;
+  uint16_t* Ks = reinterpret_cast<uint16_t*>(dsm);
+  uint16_t* Vs = Ks + static_cast<size_t>(cmax) * RK;
+  uint64_t* kvbar = reinterpret_cast<uint64_t*>(Vs + static_cast<size_t>(cmax) * RV);  // [0] cached, [1] rest
   pdl_trigger();
-  if (a.n0_ptr == nullptr && threadIdx.x == 0) {
-    // uniform cache: the length is final before the predecessor (the a1 projection) runs, so the
-    // chunk's cached rows can stream into L2 while it finishes (the new row is re-read after the wait)
+  if (threadIdx.x == 0) {
+    mbar_init(&kvbar[0], 1);
+    mbar_init(&kvbar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const bool uniform = a.n0_ptr == nullptr;
+  int pre = 0;  // rows staged before the dependency wait
+  if (uniform) {
+    // uniform cache: the length is final before the predecessor (the a1 projection) runs, so every
+    // cached row of the chunk streams in while it finishes; only the new row waits for it
     const int len0 = a.len_ptr ? *a.len_ptr + 1 : a.len;
     const int ch0 = (len0 + a.splits - 1) / a.splits;
-    const int p0 = split * ch0, p1 = min(len0 - 1, p0 + ch0);
-    if (p1 > p0) {
-      l2_prefetch(kp + (row0 + p0) * RK, static_cast<uint32_t>(p1 - p0) * RK * 2u);
-      l2_prefetch(vp + (row0 + p0) * RV, static_cast<uint32_t>(p1 - p0) * RV * 2u);
+    const int p0 = split * ch0;
+    pre = max(0, min(min(len0, p0 + ch0), len0 - 1) - p0);
+    if (threadIdx.x == 0) {
+      mbar_arrive_expect_tx(&kvbar[0], static_cast<uint32_t>(pre) * (RK + RV) * 2u);
+      if (pre > 0) {
+        bulk_g2s(Ks, kp + (row0 + p0) * RK, static_cast<uint32_t>(pre) * RK * 2u, &kvbar[0]);
+        bulk_g2s(Vs, vp + (row0 + p0) * RV, static_cast<uint32_t>(pre) * RV * 2u, &kvbar[0]);
+      }
     }
   }
   pdl_wait();
@@ -214,6 +319,19 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
   const int s0 = split * chunk;
   const int s1 = min(len, s0 + chunk);
   const int n = max(0, s1 - s0);
+  if (threadIdx.x == 0) {
+    if (!uniform) mbar_arrive_expect_tx(&kvbar[0], 0);
+    const int rest = n - pre;
+    mbar_arrive_expect_tx(&kvbar[1], static_cast<uint32_t>(max(rest, 0)) * (RK + RV) * 2u);
+    if (rest > 0) {
+      bulk_g2s(Ks + static_cast<size_t>(pre) * RK, kp + (row0 + s0 + pre) * RK, static_cast<uint32_t>(rest) * RK * 2u,
+               &kvbar[1]);
+      bulk_g2s(Vs + static_cast<size_t>(pre) * RV, vp + (row0 + s0 + pre) * RV, static_cast<uint32_t>(rest) * RV * 2u,
+               &kvbar[1]);
+    }
+  }
+  mbar_wait(&kvbar[0], 0);
+  mbar_wait(&kvbar[1], 0);
 
   // ---- scores s = q . k * scale * log2(e), all G heads of the group per K' row load
   {
@@ -230,7 +348,8 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
     for (int jb = warp * RPW; jb < n; jb += 4 * RPW) {  // warp-uniform trip count (shuffles inside)
       const int j = jb + sub;
       const bool valid = lane_on && j < n;
-      const uint4 kv = valid ? ldg_stream(kp + (row0 + s0 + j) * RK + u * 8) : make_uint4(0, 0, 0, 0);
+      const uint4 kv =
+          valid ? *reinterpret_cast<const uint4*>(Ks + static_cast<size_t>(j) * RK + u * 8) : make_uint4(0, 0, 0, 0);
       float kf[8];
       bf16x8_to_f32(kv, kf);
 #pragma unroll
@@ -285,7 +404,7 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
     for (int jb = warp * RPWV; jb < n; jb += 4 * RPWV) {
       const int j = jb + sub;
       if (lane_on && j < n) {
-        const uint4 vv = ldg_stream(vp + (row0 + s0 + j) * RV + u * 8);
+        const uint4 vv = *reinterpret_cast<const uint4*>(Vs + static_cast<size_t>(j) * RV + u * 8);
         float vf[8];
         bf16x8_to_f32(vv, vf);
 #pragma unroll
@@ -364,6 +483,7 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
     const float inv = 1.f / L;
     for (int c = threadIdx.x; c < RVO; c += 128) {
       float o = 0.f;
+#pragma unroll 8  // independent loads in flight (this merge sits on the decode critical path)
       for (int s2 = 0; s2 < nslots; ++s2) o = fmaf(wts[gi * 128 + s2], __ldcg(hp + s2 * (RVO + 2) + c), o);
       a.o[b * a.ldo + (g * G + gi) * RVO + c] = f32_to_bf16_bits(o * inv);
     }
@@ -374,8 +494,10 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
 
 int decode_splits(int B, int Nkv, int len) {
   const int pairs = B * Nkv;
-  int s = (4 * num_sms() + pairs - 1) / pairs;     // ~4 CTAs per SM
-  const int min_for_smem = (len + kMaxChunk - 1) / kMaxChunk;
+  int s = (2 * num_sms() + pairs - 1) / pairs;     // ~2 CTAs per SM
+  // a chunk's K'/V' rows are staged in shared memory: <= 300 rows (150 KB at width 128)
+  constexpr int kMaxStagedRows = 300;
+  const int min_for_smem = (len + kMaxStagedRows - 1) / kMaxStagedRows;
   const int max_useful = (len + 31) / 32;            // >= 32 keys per chunk
   if (s > max_useful) s = max_useful;
   if (s < min_for_smem) s = min_for_smem;
@@ -388,7 +510,14 @@ template <int RK, int G>
 static void launch_partial_t(const DecodeAttnArgs& a, const uint16_t* kp, const uint16_t* vp, int pool, int slot0,
                              int nslots, cudaStream_t stream) {
   dim3 grid(a.splits, a.Nkv, a.B);
-  launch_k(decode_attn_partial<RK, RK, G>, grid, dim3(128), 0, stream, g_pdl, a, kp, vp, pool, slot0, nslots);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(decode_attn_partial<RK, RK, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    attr = true;
+  }
+  const int cmax = (a.len + a.splits - 1) / a.splits;
+  const size_t smem = static_cast<size_t>(cmax) * (RK + RK) * 2 + 16;
+  launch_k(decode_attn_partial<RK, RK, G>, grid, dim3(128), smem, stream, g_pdl, a, kp, vp, pool, slot0, nslots);
 }
 
 template <int G>
