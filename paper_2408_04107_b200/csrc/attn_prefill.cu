@@ -203,30 +203,36 @@ __global__ void __launch_bounds__(192, 1)
       mbar_arrive(&s_empty[s]);
       const int key0 = j * C::BN;
       const bool diag = key0 + C::BN - 1 > qpos;             // some key of this tile is in the future
-      float tmax = -INFINITY;
+      // 4 independent max / sum chains (one warp per SMSP: latency, not throughput, limits it)
+      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
       for (int c = 0; c < 4; ++c)
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
-          float x = __uint_as_float(sv[c][e]) * sl;
-          if (diag && key0 + c * 32 + e > qpos) x = -INFINITY;
-          sv[c][e] = __float_as_uint(x);
-          tmax = fmaxf(tmax, x);
+          float x = __uint_as_float(sv[c][e]);
+          if (diag && key0 + c * 32 + e > qpos) {
+            x = -INFINITY;
+            sv[c][e] = __float_as_uint(x);
+          }
+          mx4[e & 3] = fmaxf(mx4[e & 3], x);
         }
+      // scale > 0: max(s) * scale = max(s * scale)
+      const float tmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sl;
       const float m_new = fmaxf(m_run, tmax);
       const float alpha = exp2f(m_run - m_new);              // 0 on the first tile
-      float psum = 0.f;
+      float ps4[4] = {0.f, 0.f, 0.f, 0.f};
       uint32_t pk[4][16];
 #pragma unroll
       for (int c = 0; c < 4; ++c)
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          const float p0 = fast_exp2(__uint_as_float(sv[c][2 * e]) - m_new);
-          const float p1 = fast_exp2(__uint_as_float(sv[c][2 * e + 1]) - m_new);
-          psum += p0 + p1;
+          // 2^(s * scale*log2e - m): one FFMA + MUFU.EX2 per score (masked scores are -inf -> 0)
+          const float p0 = fast_exp2(fmaf(__uint_as_float(sv[c][2 * e]), sl, -m_new));
+          const float p1 = fast_exp2(fmaf(__uint_as_float(sv[c][2 * e + 1]), sl, -m_new));
+          ps4[e & 3] += p0 + p1;
           pk[c][e] = pack_bf16x2(p0, p1);
         }
-      l_run = l_run * alpha + psum;
+      l_run = l_run * alpha + ((ps4[0] + ps4[1]) + (ps4[2] + ps4[3]));
       m_run = m_new;
       // O (TMEM) and the P buffer (smem) are free once PV_{j-1} has completed
       if (j > 0) {

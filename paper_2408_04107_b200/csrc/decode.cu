@@ -333,34 +333,46 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
   mbar_wait(&kvbar[0], 0);
   mbar_wait(&kvbar[1], 0);
 
-  // ---- scores s = q . k * scale * log2(e), all G heads of the group per K' row load
+  // ---- scores s = q . k * scale * log2(e): one thread per key row, all G heads of the group
+  // per row.  q sits in shared memory as f32; each thread visits the 16-byte chunks of its row in
+  // a rotated order ((k + j) mod UK), so the 32 rows a warp reads hit distinct banks.
   {
-    const int sub = lane / UKP, u = lane % UKP;
-    const bool lane_on = sub < RPW && u < UK;
-    float qf[G][8];
+    __shared__ __align__(16) float qsf[G][RK];
+    for (int i = threadIdx.x; i < G * UK; i += 128) {
+      const int gi = i / UK, u = i - gi * UK;
+      float f[8];
+      bf16x8_to_f32(*reinterpret_cast<const uint4*>(a.q + b * a.ldq + (g * G + gi) * a.rk + u * 8), f);
 #pragma unroll
-    for (int gi = 0; gi < G; ++gi) {
-      uint4 qv = make_uint4(0, 0, 0, 0);
-      if (lane_on) qv = *reinterpret_cast<const uint4*>(a.q + b * a.ldq + (g * G + gi) * a.rk + u * 8);
-      bf16x8_to_f32(qv, qf[gi]);
+      for (int e = 0; e < 8; ++e) qsf[gi][u * 8 + e] = f[e];
     }
-#pragma unroll 4
-    for (int jb = warp * RPW; jb < n; jb += 4 * RPW) {  // warp-uniform trip count (shuffles inside)
-      const int j = jb + sub;
-      const bool valid = lane_on && j < n;
-      const uint4 kv =
-          valid ? *reinterpret_cast<const uint4*>(Ks + static_cast<size_t>(j) * RK + u * 8) : make_uint4(0, 0, 0, 0);
-      float kf[8];
-      bf16x8_to_f32(kv, kf);
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += 128) {
+      float acc[G];
 #pragma unroll
-      for (int gi = 0; gi < G; ++gi) {
-        float p = 0.f;
+      for (int gi = 0; gi < G; ++gi) acc[gi] = 0.f;
+      const int rot = j % UK;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) p = fmaf(qf[gi][e], kf[e], p);
+      for (int k = 0; k < UK; ++k) {
+        int kc = k + rot;
+        if (kc >= UK) kc -= UK;
+        float kf[8];
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(Ks + static_cast<size_t>(j) * RK + kc * 8), kf);
 #pragma unroll
-        for (int off = UKP / 2; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
-        if (u == 0 && valid) sc[gi][j] = p * scl;
+        for (int gi = 0; gi < G; ++gi) {
+          const float4 q0 = *reinterpret_cast<const float4*>(&qsf[gi][kc * 8]);
+          const float4 q1 = *reinterpret_cast<const float4*>(&qsf[gi][kc * 8 + 4]);
+          acc[gi] = fmaf(q0.x, kf[0], acc[gi]);
+          acc[gi] = fmaf(q0.y, kf[1], acc[gi]);
+          acc[gi] = fmaf(q0.z, kf[2], acc[gi]);
+          acc[gi] = fmaf(q0.w, kf[3], acc[gi]);
+          acc[gi] = fmaf(q1.x, kf[4], acc[gi]);
+          acc[gi] = fmaf(q1.y, kf[5], acc[gi]);
+          acc[gi] = fmaf(q1.z, kf[6], acc[gi]);
+          acc[gi] = fmaf(q1.w, kf[7], acc[gi]);
+        }
       }
+#pragma unroll
+      for (int gi = 0; gi < G; ++gi) sc[gi][j] = acc[gi] * scl;
     }
   }
   __syncthreads();
