@@ -10,7 +10,8 @@
 //   O   += P_j V'_j    tcgen05.mma M=128 N=r  K=128  (A = P smem K-major,  B = V' smem MN-major)
 // S is double-buffered in TMEM so the MMA of S_{j+1} overlaps the softmax of S_j; O stays in
 // TMEM for the whole KV loop and is rescaled in place when the running max moves.
-// Warps 0-3: softmax (thread = query row = TMEM lane); warp 4: TMA producer; warp 5: MMA issuer.
+// Warps 0-7: softmax (thread = query row = TMEM lane; warps w and w+4 split the 128 keys of a
+// tile); warp 8: TMA producer; warp 9: MMA issuer.
 // Rounding points: P = exp(s - m) rounded to bf16 before PV, l from the
 // unrounded P; O' rounded to bf16 after the division by l.
 #include "common.cuh"
@@ -44,7 +45,7 @@ struct AttnCfg {
 };
 
 template <int HD>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     prefill_attn_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                         const __grid_constant__ CUtensorMap tv, const PrefillAttnArgs a) {
   using C = AttnCfg<HD>;
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(192, 1)
   };
   const uint32_t warp = warp_id(), lane = lane_id();
 
-  if (warp == 4) {
+  if (warp == 8) {
     if (lane == 0) {
       tma_prefetch_desc(&tq);
       tma_prefetch_desc(&tk);
@@ -101,9 +102,9 @@ __global__ void __launch_bounds__(192, 1)
         mbar_init(&v_full[i], 1);
         mbar_init(&v_empty[i], 1);
         mbar_init(&s_full[i], 1);
-        mbar_init(&s_empty[i], 128);
+        mbar_init(&s_empty[i], 256);
       }
-      mbar_init(p_full, 128);
+      mbar_init(p_full, 256);
       mbar_init(pv_done, 1);
       fence_barrier_init();
     }
@@ -115,7 +116,7 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 4) {
+  if (warp == 8) {
     // ------------------------------------------------ TMA producer
     if (elect_one()) {
       const uint64_t keep = policy_evict_last();
@@ -140,7 +141,7 @@ __global__ void __launch_bounds__(192, 1)
                            static_cast<int>(kv_tile_row(j) + a.v_row_off), keep);
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     // ------------------------------------------------ MMA issuer
     if (elect_one()) {
       constexpr uint32_t idesc_s = make_idesc_bf16(C::BM, C::BN, 0, 0);
@@ -184,29 +185,34 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    // ------------------------------------------------ softmax warps 0..3: thread = query row
-    const int r = warp * 32 + lane;
+    // ------------------------------------------------ softmax warps 0..7: thread = query row;
+    // warps w and w+4 share TMEM lane quarter w%4 and split the 128 keys of a tile (64 each), so
+    // every scheduler runs two softmax warps.  Only the row max is exchanged per tile; each half
+    // keeps its own partial row sum until the epilogue.
+    __shared__ float xmax[2][2][128];  // [tile parity][half][row]
+    __shared__ float xsum[2][128];
+    const int hw = warp >> 2, qq = warp & 3;
+    const int r = qq * 32 + lane;
     const int qpos = a.q_pos0 + q0 + r;                      // global position of this query row
-    const uint32_t lane_base = (warp * 32) << 16;
+    const uint32_t lane_base = (qq * 32) << 16;
     const float sl = a.scale * kLog2eF;
-    float m_run = -INFINITY, l_run = 0.f;
-    uint8_t* p_smem = smem + C::OFF_P;
+    float m_run = -INFINITY, l_half = 0.f;
+    uint8_t* p_smem = smem + C::OFF_P + hw * 16384;          // this half's [128][64] SW128 chunk
     for (int j = 0; j < n_kv; ++j) {
       const int s = j & 1;
       mbar_wait(&s_full[s], (j >> 1) & 1);
       tc_fence_after();
-      uint32_t sv[4][32];
+      uint32_t sv[2][32];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(tmem + lane_base + s * 128 + c * 32, sv[c]);
+      for (int c = 0; c < 2; ++c) tmem_ld32(tmem + lane_base + s * 128 + hw * 64 + c * 32, sv[c]);
       tc_wait_ld();
       tc_fence_before();
       mbar_arrive(&s_empty[s]);
-      const int key0 = j * C::BN;
-      const bool diag = key0 + C::BN - 1 > qpos;             // some key of this tile is in the future
-      // 4 independent max / sum chains (one warp per SMSP: latency, not throughput, limits it)
+      const int key0 = j * C::BN + hw * 64;
+      const bool diag = key0 + 63 > qpos;                    // some key of this half is in the future
       float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+      for (int c = 0; c < 2; ++c)
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
           float x = __uint_as_float(sv[c][e]);
@@ -216,14 +222,16 @@ __global__ void __launch_bounds__(192, 1)
           }
           mx4[e & 3] = fmaxf(mx4[e & 3], x);
         }
+      xmax[s][hw][r] = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+      asm volatile("bar.sync 1, 256;" ::: "memory");
       // scale > 0: max(s) * scale = max(s * scale)
-      const float tmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sl;
+      const float tmax = fmaxf(xmax[s][0][r], xmax[s][1][r]) * sl;
       const float m_new = fmaxf(m_run, tmax);
       const float alpha = exp2f(m_run - m_new);              // 0 on the first tile
       float ps4[4] = {0.f, 0.f, 0.f, 0.f};
-      uint32_t pk[4][16];
+      uint32_t pk[2][16];
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+      for (int c = 0; c < 2; ++c)
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           // 2^(s * scale*log2e - m): one FFMA + MUFU.EX2 per score (masked scores are -inf -> 0)
@@ -232,7 +240,7 @@ __global__ void __launch_bounds__(192, 1)
           ps4[e & 3] += p0 + p1;
           pk[c][e] = pack_bf16x2(p0, p1);
         }
-      l_run = l_run * alpha + ((ps4[0] + ps4[1]) + (ps4[2] + ps4[3]));
+      l_half = l_half * alpha + ((ps4[0] + ps4[1]) + (ps4[2] + ps4[3]));
       m_run = m_new;
       // O (TMEM) and the P buffer (smem) are free once PV_{j-1} has completed
       if (j > 0) {
@@ -240,7 +248,7 @@ __global__ void __launch_bounds__(192, 1)
         tc_fence_after();
         if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
-          for (int c0 = 0; c0 < HD; c0 += 16) {
+          for (int c0 = hw * 16; c0 < HD; c0 += 32) {        // this half's 16-column chunks of O
             uint32_t ov[16];
             tmem_ld16(tmem + lane_base + C::O_COL + c0, ov);
             tc_wait_ld();
@@ -251,26 +259,28 @@ __global__ void __launch_bounds__(192, 1)
           tc_wait_st();
         }
       }
-      // P row r -> two [128][64] K-major SW128 chunks
+      // P row r, keys [hw*64, hw*64+64) -> this half's K-major SW128 chunk
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const int c = u >> 3, uu = u & 7;
+      for (int u = 0; u < 8; ++u) {
         uint4 val = make_uint4(pk[u >> 2][(u & 3) * 4 + 0], pk[u >> 2][(u & 3) * 4 + 1],
                                pk[u >> 2][(u & 3) * 4 + 2], pk[u >> 2][(u & 3) * 4 + 3]);
-        *reinterpret_cast<uint4*>(p_smem + c * 16384 + sw128_off(r, uu)) = val;
+        *reinterpret_cast<uint4*>(p_smem + sw128_off(r, u)) = val;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
       mbar_arrive(p_full);
     }
-    // ---- epilogue: O / l -> bf16, LSE
+    // ---- epilogue: O / l -> bf16, LSE (l = sum of the two halves' partial sums)
+    xsum[hw][r] = l_half;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    const float l_run = xsum[0][r] + xsum[1][r];
     mbar_wait(pv_done, (n_kv - 1) & 1);
     tc_fence_after();
     const float inv_l = 1.f / l_run;
     const bool valid = q0 + r < a.n_q;
     uint16_t* orow = a.o + static_cast<int64_t>(q_row + r) * a.ldo + h * HD;
 #pragma unroll
-    for (int c0 = 0; c0 < HD; c0 += 16) {
+    for (int c0 = hw * 16; c0 < HD; c0 += 32) {
       uint32_t ov[16];
       tmem_ld16(tmem + lane_base + C::O_COL + c0, ov);
       tc_wait_ld();
@@ -288,11 +298,12 @@ __global__ void __launch_bounds__(192, 1)
         *reinterpret_cast<uint4*>(orow + c0 + 8) = w1;
       }
     }
-    if (valid && a.lse) a.lse[(static_cast<int64_t>(b) * a.Nh + h) * a.S + a.q_row0 + q0 + r] = (m_run + log2f(l_run)) * kLn2F;
+    if (hw == 0 && valid && a.lse)
+      a.lse[(static_cast<int64_t>(b) * a.Nh + h) * a.S + a.q_row0 + q0 + r] = (m_run + log2f(l_run)) * kLn2F;
     tc_fence_before();
   }
   __syncthreads();
-  if (warp == 4) {
+  if (warp == 8) {
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
   }
@@ -662,7 +673,7 @@ static cudaError_t launch_attn_t(const PrefillAttnArgs& a, cudaStream_t stream) 
   if (!make_tmap_2d(&tv, a.v, HD, kv_rows, HD * 2, C::CW, C::BN, C::SWB)) return cudaErrorInvalidValue;
   dim3 grid((a.n_q + C::BM - 1) / C::BM, a.Nh, a.B);
   prof_mark(stream, true, kProfAttnPrefill);
-  prefill_attn_kernel<HD><<<grid, 192, C::SMEM, stream>>>(tq, tk, tv, a);
+  prefill_attn_kernel<HD><<<grid, 320, C::SMEM, stream>>>(tq, tk, tv, a);
   prof_mark(stream, false, kProfAttnPrefill);
   ++g_launches;
   return cudaGetLastError();
