@@ -519,6 +519,7 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
     a.lse = reinterpret_cast<float*>(c->scratch + c->s_lse);
     a.part = reinterpret_cast<float*>(c->scratch + c->s_part);
     a.counters = reinterpret_cast<int*>(c->scratch + c->s_cnt);
+    a.prefetch_before_wait = getenv("ZDC_NO_PREWAIT") == nullptr ? 1 : 0;
     a.B = B;
     a.Nh = Nh;
     a.Nkv = Nkv;

@@ -2,6 +2,7 @@
 #pragma once
 #include <stdint.h>
 
+#include <cstdlib>
 #include <map>
 #include <tuple>
 #include <vector>
@@ -56,7 +57,7 @@ struct zdc_ctx {
     int64_t kernels = 0;
   };
   std::map<std::tuple<int, int, int, const void*, void*, cudaStream_t>, GraphEntry> graphs;
-  bool use_graphs = true;
+  bool use_graphs = getenv("ZDC_NO_GRAPH") == nullptr;  // zdc_decode replays one CUDA graph per call shape
   int* len_dev() { return reinterpret_cast<int*>(cache + len_dev_off); }
 };
 

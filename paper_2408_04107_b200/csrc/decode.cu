@@ -232,7 +232,8 @@ static cudaError_t launch_gemv_nb(const uint16_t* W, const uint16_t* x, int64_t 
   // the a1 projection (writes the staging read by attention) bounds the look-ahead
   const int mode = epi.mode == 1 ? 1 : 0;
   prof_mark(stream, true, g_prof_class);
-  cudaError_t e = launch_k(gemv_ring_kernel<NB>, dim3(blocks), dim3(288), smem, stream, g_pdl, W, x, ldx, N, K, epi,
+  cudaError_t e = launch_k(gemv_ring_kernel<NB>, dim3(blocks), dim3(288), smem, stream, g_pdl && (g_pdl_mask & 1), W,
+                           x, ldx, N, K, epi,
                            mode, slots);
   prof_mark(stream, false, g_prof_class);
   ++g_launches;
@@ -293,20 +294,19 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
   }
   __syncthreads();
   const bool uniform = a.n0_ptr == nullptr;
-  int pre = 0;  // rows staged before the dependency wait
-  if (uniform) {
+  const int pre = 0;  // rows staged in shared memory before the dependency wait (none, see below)
+  if (uniform && a.prefetch_before_wait && threadIdx.x == 0) {
     // uniform cache: the length is final before the predecessor (the a1 projection) runs, so every
-    // cached row of the chunk streams in while it finishes; only the new row waits for it
+    // cached row of the chunk streams HBM -> L2 while it finishes (the new row is excluded).
+    // (Staging them straight into shared memory with cp.async.bulk before griddepcontrol.wait
+    // faulted under PDL on B200 — profiles/r01/NOTES.md — so the smem copy follows the wait.)
     const int len0 = a.len_ptr ? *a.len_ptr + 1 : a.len;
     const int ch0 = (len0 + a.splits - 1) / a.splits;
     const int p0 = split * ch0;
-    pre = max(0, min(min(len0, p0 + ch0), len0 - 1) - p0);
-    if (threadIdx.x == 0) {
-      mbar_arrive_expect_tx(&kvbar[0], static_cast<uint32_t>(pre) * (RK + RV) * 2u);
-      if (pre > 0) {
-        bulk_g2s(Ks, kp + (row0 + p0) * RK, static_cast<uint32_t>(pre) * RK * 2u, &kvbar[0]);
-        bulk_g2s(Vs, vp + (row0 + p0) * RV, static_cast<uint32_t>(pre) * RV * 2u, &kvbar[0]);
-      }
+    const int np = max(0, min(min(len0, p0 + ch0), len0 - 1) - p0);
+    if (np > 0) {
+      l2_prefetch(kp + (row0 + p0) * RK, static_cast<uint32_t>(np) * RK * 2u);
+      l2_prefetch(vp + (row0 + p0) * RV, static_cast<uint32_t>(np) * RV * 2u);
     }
   }
   pdl_wait();
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
   const int s1 = min(len, s0 + chunk);
   const int n = max(0, s1 - s0);
   if (threadIdx.x == 0) {
-    if (!uniform) mbar_arrive_expect_tx(&kvbar[0], 0);
+    mbar_arrive_expect_tx(&kvbar[0], 0);
     const int rest = n - pre;
     mbar_arrive_expect_tx(&kvbar[1], static_cast<uint32_t>(max(rest, 0)) * (RK + RV) * 2u);
     if (rest > 0) {
@@ -529,7 +529,8 @@ static void launch_partial_t(const DecodeAttnArgs& a, const uint16_t* kp, const 
   }
   const int cmax = (a.len + a.splits - 1) / a.splits;
   const size_t smem = static_cast<size_t>(cmax) * (RK + RK) * 2 + 16;
-  launch_k(decode_attn_partial<RK, RK, G>, grid, dim3(128), smem, stream, g_pdl, a, kp, vp, pool, slot0, nslots);
+  launch_k(decode_attn_partial<RK, RK, G>, grid, dim3(128), smem, stream, g_pdl && (g_pdl_mask & 2), a, kp, vp, pool,
+           slot0, nslots);
 }
 
 template <int G>

@@ -94,6 +94,7 @@ struct DecodeAttnArgs {
   float* lse = nullptr;   // [B][Nh]
   float* part = nullptr;  // scratch [B][Nh][2 * splits][rv + 2]
   int* counters = nullptr;  // scratch [B][Nkv] zero-initialised; the last CTA per (b, g) merges
+  int prefetch_before_wait = 1;  // stage cached rows before the PDL dependency wait
   int B = 0, Nh = 0, Nkv = 0;
   float scale = 0.f;
   int splits = 1;
@@ -129,6 +130,7 @@ cudaError_t launch_classify(const float* lse, int Nh, int mode, const float* tau
 
 extern int64_t g_launches;  // kernels enqueued by the last API call
 extern bool g_pdl;          // launch decode kernels with programmatic stream serialization
+extern int g_pdl_mask;      // bit 0: projections, bit 1: attention
 
 // Launch with the programmatic-dependent-launch attribute (when pdl): the kernel may start while
 // its predecessor is still running; it must call pdl_wait() before reading the predecessor's output.
