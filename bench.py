@@ -33,6 +33,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "compressed-attn prefill tok/s & decode tok/s per B200 (% roofline); SP K/V exchange GB/s"
+_T0 = time.time()
+
+
+def log(msg):
+    sys.stderr.write("[bench %7.1fs] %s\n" % (time.time() - _T0, msg))
+    sys.stderr.flush()
 CONFIG_NAME = "c2_llama2_7b"
 
 
@@ -235,8 +241,10 @@ def run_zdc(args):
             y_all[t].copy_(y_dec)
 
     # warm-up eagerly (kernel attributes, decode graphs of the library), then capture the step
+    log("weights loaded; eager warm-up step")
     eager_step()
     torch.cuda.synchronize()
+    log("eager step done")
     if args.profile_only:
         eager_step()
         torch.cuda.synchronize()
@@ -255,6 +263,7 @@ def run_zdc(args):
             ctx.decode(x_buf, y_dec, l, l + 1)
             launches["decode"] += zdc.last_launch_count()
     torch.cuda.synchronize()
+    log("graphs captured")
     kernels_per_step = launches["prefill"] + T * launches["decode"]
 
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
@@ -276,6 +285,7 @@ def run_zdc(args):
     for _ in range(args.warmup):
         graph_step()
     torch.cuda.synchronize()
+    log("graph warm-up done")
     if world > 1:
         dist.barrier()
     clk = ClockSampler(local)

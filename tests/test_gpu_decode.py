@@ -75,3 +75,42 @@ def test_decode_c2_layer_long_context():
     rows = np.array([0, 1, 63, 64, 127, 128, 255, 299])
     want = m.prefill_rows(0, x, rows)
     assert normwise(y[:, rows], want) <= TOL
+
+
+def test_decode_side_stream_graphs_pdl():
+    """The production decode path: a non-default stream makes zdc_decode capture each call shape
+    into a CUDA graph (device-side lengths) whose kernels use programmatic dependent launch.
+    Per-layer calls (as bench.py issues them), 8 layers x 24 steps, parity with the oracle."""
+    dims = Dims(8, 256, 4, 4, 64)
+    plan = plan_uniform(8, 32)
+    _, folded = fold_stack(dims, 1, n_calib=256)
+    T = 24
+    x = Z.prompt(dims, 1, 1, T, seed=9)
+    ctx = make_context(dims, plan, folded, 1, T + 4)
+    s = torch.cuda.Stream()
+    want = O.OracleModel(dims, plan, folded, faithful=True).prefill(x)
+    # (a) per-layer calls, buffer l feeds layer l: one graph per (layer, x, y, stream) shape
+    with torch.cuda.stream(s):
+        bufs = [torch.empty(1, 256, device="cuda", dtype=torch.bfloat16) for _ in range(9)]
+        ys = []
+        for t in range(T):
+            bufs[0].copy_(to_dev_bf16(x[:, t]))
+            for l in range(8):
+                ctx.decode(bufs[l], bufs[l + 1], l, l + 1)
+            ys.append(bufs[8].clone())
+    s.synchronize()
+    got = np.stack([from_dev(v) for v in ys], 1)
+    assert normwise(got, want) <= TOL
+    # (b) one chained call per step over the 8 layers (a single graph)
+    ctx.reset()
+    with torch.cuda.stream(s):
+        xb = torch.empty(1, 256, device="cuda", dtype=torch.bfloat16)
+        yb = torch.empty_like(xb)
+        ys = []
+        for t in range(T):
+            xb.copy_(to_dev_bf16(x[:, t]))
+            ctx.decode(xb, yb, 0, 8)
+            ys.append(yb.clone())
+    s.synchronize()
+    got = np.stack([from_dev(v) for v in ys], 1)
+    assert normwise(got, want) <= TOL
