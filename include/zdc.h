@@ -219,6 +219,10 @@ zdc_status zdc_last_lse(const zdc_ctx* ctx, int32_t layer, float* lse_host, void
  * a, b, d: device; K % 64 == 0; rows 16-byte aligned. */
 zdc_status zdc_gemm_bf16(const uint16_t* a, const uint16_t* b, uint16_t* d,
                          int32_t M, int32_t N, int32_t K, void* stream);
+/* Kernel-level entry of the decode projection (a1 / a5 for B <= 8 rows, HBM-bound):
+ * y[b][n] = sum_k x[b][k] w[n][k]; w [N][K], x [B][K], y [B][N] bf16 (f32 accumulate). */
+zdc_status zdc_gemv_bf16(const uint16_t* w, const uint16_t* x, uint16_t* y, int32_t B, int32_t N, int32_t K,
+                         void* stream);
 
 /* Number of kernels the last prefill / decode call enqueued (for bench.py's gpu_launches). */
 int64_t zdc_kernel_launch_count(void);

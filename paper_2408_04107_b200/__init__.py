@@ -30,7 +30,8 @@ EXPORTED_SYMBOLS = ["zdc_last_error", "zdc_version", "zdc_fold_weights", "zdc_ct
                     "zdc_prefill", "zdc_decode", "zdc_comm_unique_id", "zdc_comm_init",
                     "zdc_sp_set_exchange_hook", "zdc_sp_prefill", "zdc_sp_positions",
                     "zdc_cache_export", "zdc_cache_length", "zdc_scores_export", "zdc_cache_reset", "zdc_last_lse",
-                    "zdc_gemm_bf16", "zdc_kernel_launch_count", "zdc_profile", "zdc_profile_read"]
+                    "zdc_gemm_bf16", "zdc_gemv_bf16", "zdc_kernel_launch_count", "zdc_profile",
+                    "zdc_profile_read"]
 
 
 class ZdcError(RuntimeError):
@@ -97,6 +98,7 @@ def lib():
             "zdc_cache_reset": ([P, P], I32),
             "zdc_last_lse": ([P, I32, P, P], I32),
             "zdc_gemm_bf16": ([P, P, P, I32, I32, I32, P], I32),
+            "zdc_gemv_bf16": ([P, P, P, I32, I32, I32, P], I32),
             "zdc_kernel_launch_count": ([], I64),
             "zdc_profile": ([ctypes.c_int], None),
             "zdc_profile_read": ([ctypes.POINTER(F), ctypes.POINTER(I64), ctypes.c_int], ctypes.c_int),
@@ -206,6 +208,13 @@ def gemm_bf16(a, b, d, stream=None):
     N = b.shape[0]
     _check(lib().zdc_gemm_bf16(_tptr(a, "bf16"), _tptr(b, "bf16"), _tptr(d, "bf16"), M, N, K, _stream(stream)),
            "zdc_gemm_bf16")
+
+
+def gemv_bf16(w, x, y, stream=None):
+    """y[B][N] = x[B][K] w[N][K]^T through zdc_gemv_bf16 (decode projection kernel, B <= 8)."""
+    N, K = w.shape
+    _check(lib().zdc_gemv_bf16(_tptr(w, "bf16"), _tptr(x, "bf16"), _tptr(y, "bf16"), x.shape[0], N, K,
+                               _stream(stream)), "zdc_gemv_bf16")
 
 
 class Context:

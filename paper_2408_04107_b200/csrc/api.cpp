@@ -770,4 +770,20 @@ zdc_status zdc_gemm_bf16(const uint16_t* a, const uint16_t* b, uint16_t* d, int3
   return ZDC_OK;
 }
 
+zdc_status zdc_gemv_bf16(const uint16_t* w, const uint16_t* x, uint16_t* y, int32_t B, int32_t N, int32_t K,
+                         void* stream) {
+  if (!w || !x || !y) return fail(ZDC_ERR_INVALID_ARG, "zdc_gemv_bf16: null pointer");
+  if (B <= 0 || B > 8 || N <= 0 || K <= 0 || K % 8 != 0)
+    return fail(ZDC_ERR_SHAPE, "zdc_gemv_bf16: B=%d N=%d K=%d (need 1 <= B <= 8, K %% 8 == 0)", B, N, K);
+  zdc_status st = check_sticky();
+  if (st != ZDC_OK) return st;
+  g_launches = 0;
+  Epilogue e;
+  e.mode = 0;
+  e.d = y;
+  e.ldd = N;
+  ZDC_CUDA_TRY(launch_gemv(w, x, K, B, N, K, e, static_cast<cudaStream_t>(stream)));
+  return ZDC_OK;
+}
+
 }  // extern "C"

@@ -13,6 +13,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace zdc {
 
 __device__ __forceinline__ uint4 ldg_stream(const void* p) {
@@ -209,7 +211,10 @@ __global__ void __launch_bounds__(288, 1)
   }
 }
 
-static constexpr int kGemvRingBytes = 96 * 1024;  // leaves room for the next kernel's CTAs (PDL)
+// ring bytes per CTA (tunable with ZDC_GEMV_RING_KB); 96 KB leaves room for the next kernel's CTAs
+static const int kGemvRingBytes = getenv("ZDC_GEMV_RING_KB") ? atoi(getenv("ZDC_GEMV_RING_KB")) * 1024 : 96 * 1024;
+// CTAs per SM for the projection GEMV (tunable with ZDC_GEMV_CTAS)
+static const int kGemvCtasPerSm = getenv("ZDC_GEMV_CTAS") ? atoi(getenv("ZDC_GEMV_CTAS")) : 1;
 
 template <int NB>
 static cudaError_t launch_gemv_nb(const uint16_t* W, const uint16_t* x, int64_t ldx, int N, int K, const Epilogue& epi,
@@ -222,7 +227,7 @@ static cudaError_t launch_gemv_nb(const uint16_t* W, const uint16_t* x, int64_t 
     attr = true;
   }
   int blocks = (N + 7) / 8;
-  if (blocks > num_sms()) blocks = num_sms();
+  if (blocks > num_sms() * kGemvCtasPerSm) blocks = num_sms() * kGemvCtasPerSm;
   const int per = (N + blocks - 1) / blocks;
   int slots = kGemvRingBytes / (K * 2);
   if (slots > per) slots = per;
