@@ -162,12 +162,18 @@ __global__ void __launch_bounds__(288, 1)
   }
   __syncthreads();
   if (!(pdl_mode & 1)) pdl_trigger();
+  // Row i is reduced by warp i % 8; warp w owns the slots [w*spw, (w+1)*spw) and uses them in order,
+  // so every mbarrier wait is for the phase right after the one last observed (a shared ring let a
+  // warp wait two phases ahead, where the parity test aliases: profiles/r01/NOTES.md).
+  const int spw = slots / 8;
   if (warp == 8) {
     // ---- producer: weight rows HBM -> smem ring (independent of the predecessor: no wait)
     if (lane == 0) {
+      if (pdl_mode & 2) pdl_wait();  // debug knob: issue the copies only after the dependency
       for (int i = 0; i < nrows; ++i) {
-        const int s = i % slots;
-        if (i >= slots) mbar_wait(&empty[s], ((i / slots) & 1) ^ 1);
+        const int k = i >> 3;
+        const int s = (i & 7) * spw + k % spw;
+        if (k >= spw) mbar_wait(&empty[s], ((k / spw) & 1) ^ 1);
         mbar_arrive_expect_tx(&full[s], row_bytes);
         bulk_g2s(ring + static_cast<size_t>(s) * row_bytes, W + static_cast<int64_t>(r0 + i) * K, row_bytes,
                  &full[s]);
@@ -185,8 +191,9 @@ __global__ void __launch_bounds__(288, 1)
   }
   asm volatile("bar.sync 1, 256;" ::: "memory");
   for (int i = warp; i < nrows; i += 8) {
-    const int s = i % slots;
-    mbar_wait(&full[s], (i / slots) & 1);
+    const int k = i >> 3;
+    const int s = warp * spw + k % spw;
+    mbar_wait(&full[s], (k / spw) & 1);
     const uint4* w = reinterpret_cast<const uint4*>(ring + static_cast<size_t>(s) * row_bytes);
     float acc[NB];
 #pragma unroll
@@ -212,7 +219,7 @@ __global__ void __launch_bounds__(288, 1)
 }
 
 // ring bytes per CTA (tunable with ZDC_GEMV_RING_KB); 96 KB leaves room for the next kernel's CTAs
-static const int kGemvRingBytes = getenv("ZDC_GEMV_RING_KB") ? atoi(getenv("ZDC_GEMV_RING_KB")) * 1024 : 96 * 1024;
+static const int kGemvRingBytes = getenv("ZDC_GEMV_RING_KB") ? atoi(getenv("ZDC_GEMV_RING_KB")) * 1024 : 128 * 1024;
 // CTAs per SM for the projection GEMV (tunable with ZDC_GEMV_CTAS)
 static const int kGemvCtasPerSm = getenv("ZDC_GEMV_CTAS") ? atoi(getenv("ZDC_GEMV_CTAS")) : 1;
 
@@ -229,13 +236,14 @@ static cudaError_t launch_gemv_nb(const uint16_t* W, const uint16_t* x, int64_t 
   int blocks = (N + 7) / 8;
   if (blocks > num_sms() * kGemvCtasPerSm) blocks = num_sms() * kGemvCtasPerSm;
   const int per = (N + blocks - 1) / blocks;
-  int slots = kGemvRingBytes / (K * 2);
-  if (slots > per) slots = per;
-  if (slots < 1) slots = 1;
+  int spw = kGemvRingBytes / (8 * K * 2);  // slots per consumer warp
+  if (spw > (per + 7) / 8) spw = (per + 7) / 8;
+  if (spw < 1) spw = 1;
+  const int slots = 8 * spw;
   const size_t smem = static_cast<size_t>(slots) * K * 2 + static_cast<size_t>(NB) * K * 2 + 16 * slots + 16;
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   // the a1 projection (writes the staging read by attention) bounds the look-ahead
-  const int mode = epi.mode == 1 ? 1 : 0;
+  const int mode = (epi.mode == 1 ? 1 : 0) | (getenv("ZDC_GEMV_NO_PREWAIT") ? 2 : 0);
   prof_mark(stream, true, g_prof_class);
   cudaError_t e = launch_k(gemv_ring_kernel<NB>, dim3(blocks), dim3(288), smem, stream, g_pdl && (g_pdl_mask & 1), W,
                            x, ldx, N, K, epi,
