@@ -519,7 +519,8 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
     a.lse = reinterpret_cast<float*>(c->scratch + c->s_lse);
     a.part = reinterpret_cast<float*>(c->scratch + c->s_part);
     a.counters = reinterpret_cast<int*>(c->scratch + c->s_cnt);
-    a.prefetch_before_wait = getenv("ZDC_NO_PREWAIT") == nullptr ? 1 : 0;
+    // cached K'/V' rows before the PDL wait: 2 = into shared memory, 1 = into L2, 0 = none
+    a.prefetch_before_wait = getenv("ZDC_ATTN_PREWAIT") ? atoi(getenv("ZDC_ATTN_PREWAIT")) : 2;
     a.B = B;
     a.Nh = Nh;
     a.Nkv = Nkv;

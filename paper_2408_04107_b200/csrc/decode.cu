@@ -307,17 +307,25 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
   }
   __syncthreads();
   const bool uniform = a.n0_ptr == nullptr;
-  const int pre = 0;  // rows staged in shared memory before the dependency wait (none, see below)
-  if (uniform && a.prefetch_before_wait && threadIdx.x == 0) {
+  int pre = 0;  // rows staged in shared memory before the dependency wait
+  if (uniform && a.prefetch_before_wait) {
     // uniform cache: the length is final before the predecessor (the a1 projection) runs, so every
-    // cached row of the chunk streams HBM -> L2 while it finishes (the new row is excluded).
-    // (Staging them straight into shared memory with cp.async.bulk before griddepcontrol.wait
-    // faulted under PDL on B200 — profiles/r01/NOTES.md — so the smem copy follows the wait.)
+    // cached row of the chunk can stream in while it finishes (the new row is excluded):
+    // mode 2 stages them straight into shared memory, mode 1 only into L2.
     const int len0 = a.len_ptr ? *a.len_ptr + 1 : a.len;
     const int ch0 = (len0 + a.splits - 1) / a.splits;
     const int p0 = split * ch0;
     const int np = max(0, min(min(len0, p0 + ch0), len0 - 1) - p0);
-    if (np > 0) {
+    if (a.prefetch_before_wait == 2) {
+      pre = np;
+      if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(&kvbar[0], static_cast<uint32_t>(np) * (RK + RV) * 2u);
+        if (np > 0) {
+          bulk_g2s(Ks, kp + (row0 + p0) * RK, static_cast<uint32_t>(np) * RK * 2u, &kvbar[0]);
+          bulk_g2s(Vs, vp + (row0 + p0) * RV, static_cast<uint32_t>(np) * RV * 2u, &kvbar[0]);
+        }
+      }
+    } else if (threadIdx.x == 0 && np > 0) {
       l2_prefetch(kp + (row0 + p0) * RK, static_cast<uint32_t>(np) * RK * 2u);
       l2_prefetch(vp + (row0 + p0) * RV, static_cast<uint32_t>(np) * RV * 2u);
     }
@@ -333,7 +341,7 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
   const int s1 = min(len, s0 + chunk);
   const int n = max(0, s1 - s0);
   if (threadIdx.x == 0) {
-    mbar_arrive_expect_tx(&kvbar[0], 0);
+    if (!(uniform && a.prefetch_before_wait == 2)) mbar_arrive_expect_tx(&kvbar[0], 0);
     const int rest = n - pre;
     mbar_arrive_expect_tx(&kvbar[1], static_cast<uint32_t>(max(rest, 0)) * (RK + RV) * 2u);
     if (rest > 0) {

@@ -24,8 +24,7 @@ namespace zdc {
 int64_t g_launches = 0;
 bool g_pdl = getenv("ZDC_NO_PDL") == nullptr;  // A/B switch for programmatic dependent launch
 // which decode kernels launch with PDL: bit 0 projections (GEMV), bit 1 attention
-// (attention under PDL hung / faulted on B200 in round 1, profiles/r01/NOTES.md: projections only)
-int g_pdl_mask = getenv("ZDC_PDL_MASK") ? atoi(getenv("ZDC_PDL_MASK")) : 1;
+int g_pdl_mask = getenv("ZDC_PDL_MASK") ? atoi(getenv("ZDC_PDL_MASK")) : 3;
 int g_prof_class = kProfOther;
 
 // ------------------------------------------------------------------ host: per-class event timing
