@@ -219,6 +219,20 @@ zdc_status zdc_last_lse(const zdc_ctx* ctx, int32_t layer, float* lse_host, void
  * a, b, d: device; K % 64 == 0; rows 16-byte aligned. */
 zdc_status zdc_gemm_bf16(const uint16_t* a, const uint16_t* b, uint16_t* d,
                          int32_t M, int32_t N, int32_t K, void* stream);
+/* Kernel-level entries of a3 (tests and roofline measurements), Eqs. 2-3 with the
+ * given scale (1/sqrt(d_h), reading c2), bf16 in / out, f32 softmax and accumulation:
+ * prefill (causal): q, o [B*S][N_h*r] (head h at cols h*r), k, v [B][N_kv][S][r], lse [B][N_h][S]
+ *   (may be NULL); r % 16 == 0, r <= 128.
+ * decode (the query attends to positions [0, len)): q, o [B][N_h*r], k, v [B][N_kv][S_cap][r],
+ *   lse [B][N_h] (may be NULL); workspace: zdc_decode_attention_workspace(...) bytes, zeroed by the
+ *   caller once (the kernel leaves its merge counters at zero). */
+zdc_status zdc_prefill_attention_bf16(const uint16_t* q, const uint16_t* k, const uint16_t* v, uint16_t* o,
+                                      float* lse, int32_t B, int32_t S, int32_t Nh, int32_t Nkv, int32_t r,
+                                      float scale, void* stream);
+int64_t zdc_decode_attention_workspace(int32_t B, int32_t Nh, int32_t Nkv, int32_t r);
+zdc_status zdc_decode_attention_bf16(const uint16_t* q, const uint16_t* k, const uint16_t* v, uint16_t* o,
+                                     float* lse, int32_t B, int32_t Nh, int32_t Nkv, int32_t r, int32_t len,
+                                     int32_t S_cap, float scale, void* workspace, void* stream);
 /* Kernel-level entry of the decode projection (a1 / a5 for B <= 8 rows, HBM-bound):
  * y[b][n] = sum_k x[b][k] w[n][k]; w [N][K], x [B][K], y [B][N] bf16 (f32 accumulate). */
 zdc_status zdc_gemv_bf16(const uint16_t* w, const uint16_t* x, uint16_t* y, int32_t B, int32_t N, int32_t K,

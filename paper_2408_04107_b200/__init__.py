@@ -30,8 +30,9 @@ EXPORTED_SYMBOLS = ["zdc_last_error", "zdc_version", "zdc_fold_weights", "zdc_ct
                     "zdc_prefill", "zdc_decode", "zdc_comm_unique_id", "zdc_comm_init",
                     "zdc_sp_set_exchange_hook", "zdc_sp_prefill", "zdc_sp_positions",
                     "zdc_cache_export", "zdc_cache_length", "zdc_scores_export", "zdc_cache_reset", "zdc_last_lse",
-                    "zdc_gemm_bf16", "zdc_gemv_bf16", "zdc_kernel_launch_count", "zdc_profile",
-                    "zdc_profile_read"]
+                    "zdc_gemm_bf16", "zdc_gemv_bf16", "zdc_prefill_attention_bf16",
+                    "zdc_decode_attention_workspace", "zdc_decode_attention_bf16",
+                    "zdc_kernel_launch_count", "zdc_profile", "zdc_profile_read"]
 
 
 class ZdcError(RuntimeError):
@@ -99,6 +100,9 @@ def lib():
             "zdc_last_lse": ([P, I32, P, P], I32),
             "zdc_gemm_bf16": ([P, P, P, I32, I32, I32, P], I32),
             "zdc_gemv_bf16": ([P, P, P, I32, I32, I32, P], I32),
+            "zdc_prefill_attention_bf16": ([P, P, P, P, P, I32, I32, I32, I32, I32, F, P], I32),
+            "zdc_decode_attention_workspace": ([I32, I32, I32, I32], I64),
+            "zdc_decode_attention_bf16": ([P, P, P, P, P, I32, I32, I32, I32, I32, I32, F, P, P], I32),
             "zdc_kernel_launch_count": ([], I64),
             "zdc_profile": ([ctypes.c_int], None),
             "zdc_profile_read": ([ctypes.POINTER(F), ctypes.POINTER(I64), ctypes.c_int], ctypes.c_int),
@@ -215,6 +219,34 @@ def gemv_bf16(w, x, y, stream=None):
     N, K = w.shape
     _check(lib().zdc_gemv_bf16(_tptr(w, "bf16"), _tptr(x, "bf16"), _tptr(y, "bf16"), x.shape[0], N, K,
                                _stream(stream)), "zdc_gemv_bf16")
+
+
+def prefill_attention_bf16(q, k, v, o, lse=None, scale=None, stream=None):
+    """Causal attention kernel alone: q, o [B][S][Nh*r]; k, v [B][Nkv][S][r]; lse [B][Nh][S] f32."""
+    B, S, nhr = q.shape
+    Nkv, r = k.shape[1], k.shape[3]
+    Nh = nhr // r
+    scale = 1.0 / r ** 0.5 if scale is None else scale
+    _check(lib().zdc_prefill_attention_bf16(_tptr(q, "bf16"), _tptr(k, "bf16"), _tptr(v, "bf16"), _tptr(o, "bf16"),
+                                            _tptr(lse, "f32") if lse is not None else None, B, S, Nh, Nkv, r,
+                                            float(scale), _stream(stream)), "zdc_prefill_attention_bf16")
+
+
+def decode_attention_bf16(q, k, v, o, length, lse=None, scale=None, workspace=None, stream=None):
+    """Decode attention kernel alone: q, o [B][Nh*r]; k, v [B][Nkv][S_cap][r]; keys [0, length)."""
+    import torch
+    B, nhr = q.shape
+    Nkv, S_cap, r = k.shape[1], k.shape[2], k.shape[3]
+    Nh = nhr // r
+    scale = 1.0 / r ** 0.5 if scale is None else scale
+    if workspace is None:
+        workspace = torch.zeros(int(lib().zdc_decode_attention_workspace(B, Nh, Nkv, r)), dtype=torch.uint8,
+                                device=q.device)
+    _check(lib().zdc_decode_attention_bf16(_tptr(q, "bf16"), _tptr(k, "bf16"), _tptr(v, "bf16"), _tptr(o, "bf16"),
+                                           _tptr(lse, "f32") if lse is not None else None, B, Nh, Nkv, r,
+                                           int(length), S_cap, float(scale), ctypes.c_void_p(workspace.data_ptr()),
+                                           _stream(stream)), "zdc_decode_attention_bf16")
+    return workspace
 
 
 class Context:

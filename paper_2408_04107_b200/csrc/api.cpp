@@ -771,6 +771,80 @@ zdc_status zdc_gemm_bf16(const uint16_t* a, const uint16_t* b, uint16_t* d, int3
   return ZDC_OK;
 }
 
+zdc_status zdc_prefill_attention_bf16(const uint16_t* q, const uint16_t* k, const uint16_t* v, uint16_t* o,
+                                      float* lse, int32_t B, int32_t S, int32_t Nh, int32_t Nkv, int32_t r,
+                                      float scale, void* stream) {
+  if (!q || !k || !v || !o) return fail(ZDC_ERR_INVALID_ARG, "zdc_prefill_attention_bf16: null pointer");
+  if (B <= 0 || S <= 0 || Nh <= 0 || Nkv <= 0 || Nh % Nkv != 0 || r <= 0 || r > 128 || r % 16 != 0)
+    return fail(ZDC_ERR_SHAPE, "zdc_prefill_attention_bf16: B=%d S=%d Nh=%d Nkv=%d r=%d", B, S, Nh, Nkv, r);
+  const int G = Nh / Nkv;
+  if (G != 1 && G != 2 && G != 4 && G != 8) return fail(ZDC_ERR_UNSUPPORTED, "group size %d", G);
+  zdc_status st = check_sticky();
+  if (st != ZDC_OK) return st;
+  g_launches = 0;
+  PrefillAttnArgs a;
+  a.q = q;
+  a.ldq = static_cast<int64_t>(Nh) * r;
+  a.k = k;
+  a.v = v;
+  a.S_cap = S;
+  a.o = o;
+  a.ldo = static_cast<int64_t>(Nh) * r;
+  a.lse = lse;
+  a.B = B;
+  a.S = S;
+  a.Nh = Nh;
+  a.Nkv = Nkv;
+  a.rk = r;
+  a.rv = r;
+  a.scale = scale;
+  a.q_pos0 = 0;
+  a.q_row0 = 0;
+  a.n_q = S;
+  ZDC_CUDA_TRY(launch_prefill_attention(a, static_cast<cudaStream_t>(stream)));
+  return ZDC_OK;
+}
+
+int64_t zdc_decode_attention_workspace(int32_t B, int32_t Nh, int32_t Nkv, int32_t r) {
+  return static_cast<int64_t>(B) * Nh * 128 * (r + 2) * 4 + static_cast<int64_t>(B) * Nkv * 4 + 256;
+}
+
+zdc_status zdc_decode_attention_bf16(const uint16_t* q, const uint16_t* k, const uint16_t* v, uint16_t* o,
+                                     float* lse, int32_t B, int32_t Nh, int32_t Nkv, int32_t r, int32_t len,
+                                     int32_t S_cap, float scale, void* workspace, void* stream) {
+  if (!q || !k || !v || !o || !workspace) return fail(ZDC_ERR_INVALID_ARG, "zdc_decode_attention_bf16: null pointer");
+  if (B <= 0 || Nh <= 0 || Nkv <= 0 || Nh % Nkv != 0 || r <= 0 || r > 128 || r % 16 != 0 || len <= 0 ||
+      len > S_cap)
+    return fail(ZDC_ERR_SHAPE, "zdc_decode_attention_bf16: B=%d Nh=%d Nkv=%d r=%d len=%d S_cap=%d", B, Nh, Nkv, r,
+                len, S_cap);
+  zdc_status st = check_sticky();
+  if (st != ZDC_OK) return st;
+  g_launches = 0;
+  DecodeAttnArgs a;
+  a.q = q;
+  a.ldq = static_cast<int64_t>(Nh) * r;
+  a.k = k;
+  a.v = v;
+  a.rk = r;
+  a.rv = r;
+  a.S_cap = S_cap;
+  a.len = len;
+  a.o = o;
+  a.ldo = static_cast<int64_t>(Nh) * r;
+  a.lse = lse;
+  a.part = static_cast<float*>(workspace);
+  a.counters = reinterpret_cast<int*>(static_cast<uint8_t*>(workspace) +
+                                      static_cast<int64_t>(B) * Nh * 128 * (r + 2) * 4);
+  a.B = B;
+  a.Nh = Nh;
+  a.Nkv = Nkv;
+  a.scale = scale;
+  a.splits = decode_splits(B, Nkv, len);
+  a.prefetch_before_wait = 0;
+  ZDC_CUDA_TRY(launch_decode_attention(a, static_cast<cudaStream_t>(stream)));
+  return ZDC_OK;
+}
+
 zdc_status zdc_gemv_bf16(const uint16_t* w, const uint16_t* x, uint16_t* y, int32_t B, int32_t N, int32_t K,
                          void* stream) {
   if (!w || !x || !y) return fail(ZDC_ERR_INVALID_ARG, "zdc_gemv_bf16: null pointer");
