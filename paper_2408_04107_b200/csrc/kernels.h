@@ -70,6 +70,7 @@ struct PrefillAttnArgs {
   int64_t kv_rows_total = 0;  // rows of the K/V tensor maps (0 = B * Nkv * S_cap)
 };
 cudaError_t launch_prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream);
+cudaError_t launch_prefill_attention_v3(const PrefillAttnArgs& a, cudaStream_t stream);
 
 // ---- a3 decode attention: split-K over the context (one or two pools) + LSE-merge combine
 struct DecodeAttnArgs {
