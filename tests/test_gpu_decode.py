@@ -114,3 +114,17 @@ def test_decode_side_stream_graphs_pdl():
     s.synchronize()
     got = np.stack([from_dev(v) for v in ys], 1)
     assert normwise(got, want) <= TOL
+
+
+@pytest.mark.parametrize("B", [9, 16])
+def test_decode_batch_above_gemv_limit(B):
+    """B > 8 decode rows take the tcgen05 GEMM path for a1 / a5 (with the fused append and the
+    device-side length advance in its epilogue / prologue)."""
+    dims = Dims(2, 256, 4, 2, 64)
+    plan = plan_uniform(2, 32)
+    _, folded = fold_stack(dims, 1, n_calib=256)
+    T = 12
+    x = Z.prompt(dims, 1, B, T, seed=10)
+    _, y = _run_decode(dims, plan, folded, x, B)
+    want = O.OracleModel(dims, plan, folded, faithful=True).prefill(x)
+    assert normwise(y, want) <= TOL
