@@ -582,7 +582,26 @@ static cudaError_t launch_partial(const DecodeAttnArgs& a, int width, const uint
   }
 }
 
-cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t stream) {
+static const bool g_dec_attn_v2 = getenv("ZDC_DEC_ATTN_V1") == nullptr;
+static bool v2_width(int w) { return w == 32 || w == 64 || w == 96 || w == 128; }
+
+cudaError_t launch_decode_attention(const DecodeAttnArgs& a_in, cudaStream_t stream) {
+  if (g_dec_attn_v2 && v2_width(a_in.rk) && (!a_in.k1 || v2_width(a_in.rk1)) && a_in.rk == a_in.rv &&
+      (!a_in.k1 || a_in.rk1 == a_in.rv1) && a_in.counters) {
+    // v2 (decode_attn2.cu): 8-warp CTAs, per-warp pipelined tiles; its own split count
+    DecodeAttnArgs a = a_in;
+    a.splits = decode2_splits(a.B, a.Nkv, a.len);
+    const int nslots = a.splits * (a.k1 ? 2 : 1);
+    if (nslots > 128) return cudaErrorInvalidValue;
+    prof_mark(stream, true, kProfAttnDecode);
+    cudaError_t e = launch_decode2_partial(a, a.rk, a.k, a.v, 0, 0, nslots, stream);
+    if (e == cudaSuccess && a.k1) e = launch_decode2_partial(a, a.rk1, a.k1, a.v1, 1, a.splits, nslots, stream);
+    prof_mark(stream, false, kProfAttnDecode);
+    g_launches += a.k1 ? 2 : 1;
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+  }
+  const DecodeAttnArgs& a = a_in;
   // a.len bounds the rows of either pool (graph replays may see any length up to it)
   if (a.splits > 64 || (a.len + a.splits - 1) / a.splits > kMaxChunk) return cudaErrorInvalidValue;
   if (a.rk != a.rv || (a.k1 && a.rk1 != a.rv1)) return cudaErrorInvalidValue;
