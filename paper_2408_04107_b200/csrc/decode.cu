@@ -590,7 +590,7 @@ cudaError_t launch_decode_attention(const DecodeAttnArgs& a_in, cudaStream_t str
       (!a_in.k1 || a_in.rk1 == a_in.rv1) && a_in.counters) {
     // v2 (decode_attn2.cu): 8-warp CTAs, per-warp pipelined tiles; its own split count
     DecodeAttnArgs a = a_in;
-    a.splits = decode2_splits(a.B, a.Nkv, a.len);
+    a.splits = decode2_splits(a.B, a.Nkv, a.len, a.rk, a.Nh / a.Nkv);
     const int nslots = a.splits * (a.k1 ? 2 : 1);
     if (nslots > 128) return cudaErrorInvalidValue;
     prof_mark(stream, true, kProfAttnDecode);

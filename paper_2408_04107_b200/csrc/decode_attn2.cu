@@ -1,7 +1,8 @@
 // decode_attn2.cu — a3 for token generation, v2 (the default): split-K "flash decoding" over the
 // compressed cache, restructured after the round-1 measurement (v1: 24% of HBM, one long serial
 // chain of phases per CTA):
-//   * one CTA (8 warps) per (split, KV head, sequence); each warp streams its own slice of rows in
+//   * one CTA (kNW = 4 warps) per (split, KV head, sequence), as many splits as fill ONE wave of
+//     the occupancy-limited CTA slots; each warp streams its own slice of rows in
 //     32-row tiles through a private 2-stage shared-memory ring filled by cp.async.bulk (per-warp
 //     mbarriers: no block-wide syncs in the main loop), so load and compute overlap per warp;
 //   * lane j scores row j of the tile for all G query heads of the KV group (GQA, reading c4);
@@ -16,6 +17,7 @@
 namespace zdc {
 
 static constexpr float kLog2eD = 1.4426950408889634f;
+static constexpr int kNW = 4;  // warps per CTA
 
 __device__ __forceinline__ void bf16x8_f32(uint4 v, float (&f)[8]) {
   f[0] = __uint_as_float(v.x << 16);
@@ -40,16 +42,16 @@ struct DA2 {
 };
 
 template <int RK, int RV, int G>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kNW * 32)
     decode_attn2_kernel(const DecodeAttnArgs a, const uint16_t* __restrict__ kp, const uint16_t* __restrict__ vp,
                         int pool, int slot0, int nslots) {
   using C = DA2<RK, RV>;
   static_assert(RV % 32 == 0 || RV == 16, "RV must be a multiple of 32 (or 16)");
   extern __shared__ __align__(128) uint8_t dsm[];
   __shared__ __align__(16) float qsf[G][RK];
-  __shared__ float wm[8][G], wl[8][G];
-  __shared__ float wo[8][G][RV];
-  __shared__ uint64_t bars[8][2];
+  __shared__ float wm[kNW][G], wl[kNW][G];
+  __shared__ float wo[kNW][G][RV];
+  __shared__ uint64_t bars[kNW][2];
   __shared__ int s_last;
   const int split = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -70,7 +72,7 @@ __global__ void __launch_bounds__(256, 1)
   auto ranges = [&](int len, int& w0, int& w1) {
     const int chunk = (len + a.splits - 1) / a.splits;
     const int c0 = split * chunk, c1 = min(len, c0 + chunk);
-    const int per = (max(0, c1 - c0) + 7) / 8;
+    const int per = (max(0, c1 - c0) + kNW - 1) / kNW;
     w0 = c0 + warp * per;
     w1 = min(c1, w0 + per);
     if (w1 < w0) w1 = w0;
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(256, 1)
   if (lane == 0)
     for (int t = pre_tiles; t < min(ntile, C::NST); ++t) issue(t, w0, w1, t);
   // q of the G heads of this KV group, as f32 in shared memory
-  for (int i = threadIdx.x; i < G * C::UK; i += 256) {
+  for (int i = threadIdx.x; i < G * C::UK; i += kNW * 32) {
     const int gi = i / C::UK, u = i - gi * C::UK;
     float f[8];
     bf16x8_f32(*reinterpret_cast<const uint4*>(a.q + b * a.ldq + (g * G + gi) * a.rk + u * 8), f);
@@ -221,14 +223,14 @@ __global__ void __launch_bounds__(256, 1)
   }
   __syncthreads();
   const int RVO = a.rv;
-  for (int i = threadIdx.x; i < G * RVO; i += 256) {
+  for (int i = threadIdx.x; i < G * RVO; i += kNW * 32) {
     const int gi = i / RVO, c = i - gi * RVO;
     float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) M = fmaxf(M, wm[w][gi]);
+    for (int w = 0; w < kNW; ++w) M = fmaxf(M, wm[w][gi]);
     float L = 0.f, O = 0.f;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) {
+    for (int w = 0; w < kNW; ++w) {
       const float f = wm[w][gi] == -INFINITY ? 0.f : exp2f(wm[w][gi] - M);
       L += f * wl[w][gi];
       if (c < RV) O += f * wo[w][gi][c];
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  for (int i = threadIdx.x; i < G * RVO; i += 256) {
+  for (int i = threadIdx.x; i < G * RVO; i += kNW * 32) {
     const int gi = i / RVO, c = i - gi * RVO;
     const float* hp = a.part + ((static_cast<int64_t>(b) * a.Nh + g * G + gi) * nslots) * (RVO + 2);
     float M = -INFINITY;
@@ -270,10 +272,42 @@ __global__ void __launch_bounds__(256, 1)
   if (threadIdx.x == 0) a.counters[b * a.Nkv + g] = 0;
 }
 
-int decode2_splits(int B, int Nkv, int len) {
+template <int RK, int G>
+static int ctas_per_sm_t() {
+  using C = DA2<RK, RK>;
+  static int n = 0;
+  if (n == 0) {
+    cudaFuncSetAttribute(decode_attn2_kernel<RK, RK, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kNW * C::WARP_BYTES));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_attn2_kernel<RK, RK, G>, kNW * 32,
+                                                  static_cast<size_t>(kNW * C::WARP_BYTES));
+    if (n < 1) n = 1;
+  }
+  return n;
+}
+
+template <int G>
+static int ctas_per_sm_g(int width) {
+  switch (width) {
+    case 32: return ctas_per_sm_t<32, G>();
+    case 64: return ctas_per_sm_t<64, G>();
+    case 96: return ctas_per_sm_t<96, G>();
+    default: return ctas_per_sm_t<128, G>();
+  }
+}
+
+// Split count: as many CTAs as fit in ONE wave (occupancy x SMs), >= 32 rows per warp.
+int decode2_splits(int B, int Nkv, int len, int width, int G) {
+  int fit = 1;
+  switch (G) {
+    case 1: fit = ctas_per_sm_g<1>(width); break;
+    case 2: fit = ctas_per_sm_g<2>(width); break;
+    case 4: fit = ctas_per_sm_g<4>(width); break;
+    default: fit = ctas_per_sm_g<8>(width); break;
+  }
   const int pairs = B * Nkv;
-  int s = (num_sms() + pairs - 1) / pairs;  // ~1 CTA (8 warps) per SM
-  const int max_useful = (len + 255) / 256; // >= 32 rows per warp
+  int s = fit * num_sms() / pairs;
+  const int max_useful = (len + kNW * 32 - 1) / (kNW * 32);
   if (s > max_useful) s = max_useful;
   if (s > 64) s = 64;
   if (s < 1) s = 1;
@@ -287,12 +321,12 @@ static cudaError_t launch2_t(const DecodeAttnArgs& a, const uint16_t* kp, const 
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(decode_attn2_kernel<RK, RK, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(8 * C::WARP_BYTES));
+                                         static_cast<int>(kNW * C::WARP_BYTES));
     if (e != cudaSuccess) return e;
     attr = true;
   }
   dim3 grid(a.splits, a.Nkv, a.B);
-  return launch_k(decode_attn2_kernel<RK, RK, G>, grid, dim3(256), static_cast<size_t>(8 * C::WARP_BYTES), stream,
+  return launch_k(decode_attn2_kernel<RK, RK, G>, grid, dim3(kNW * 32), static_cast<size_t>(kNW * C::WARP_BYTES), stream,
                   g_pdl && (g_pdl_mask & 2), a, kp, vp, pool, slot0, nslots);
 }
 

@@ -103,7 +103,7 @@ struct DecodeAttnArgs {
 cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t stream);
 cudaError_t launch_decode2_partial(const DecodeAttnArgs& a, int width, const uint16_t* kp, const uint16_t* vp,
                                    int pool, int slot0, int nslots, cudaStream_t s);
-int decode2_splits(int B, int Nkv, int len);
+int decode2_splits(int B, int Nkv, int len, int width, int G);
 int decode_splits(int B, int Nkv, int len);
 
 // ---- weight packing (load time): f32/bf16 full-rank folded -> truncated, padded, bf16
