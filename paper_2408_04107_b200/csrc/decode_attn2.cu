@@ -252,17 +252,28 @@ __global__ void __launch_bounds__(kNW * 32)
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  // (m, l) of every slot: one parallel load into shared memory (the ring is free now), then the
+  // per-head max and merge weights; the o loads below are independent (8 in flight per thread)
+  float* sm_m = reinterpret_cast<float*>(dsm);         // [G][nslots]
+  float* sm_l = sm_m + G * nslots;                      // [G][nslots]
+  for (int i = threadIdx.x; i < G * nslots; i += kNW * 32) {
+    const int gi = i / nslots, s2 = i - gi * nslots;
+    const float* hp = a.part + ((static_cast<int64_t>(b) * a.Nh + g * G + gi) * nslots + s2) * (RVO + 2);
+    sm_m[i] = __ldcg(hp + RVO);
+    sm_l[i] = __ldcg(hp + RVO + 1);
+  }
+  __syncthreads();
   for (int i = threadIdx.x; i < G * RVO; i += kNW * 32) {
     const int gi = i / RVO, c = i - gi * RVO;
     const float* hp = a.part + ((static_cast<int64_t>(b) * a.Nh + g * G + gi) * nslots) * (RVO + 2);
     float M = -INFINITY;
-    for (int s2 = 0; s2 < nslots; ++s2) M = fmaxf(M, __ldcg(hp + s2 * (RVO + 2) + RVO));
+    for (int s2 = 0; s2 < nslots; ++s2) M = fmaxf(M, sm_m[gi * nslots + s2]);
     float L = 0.f, O = 0.f;
-#pragma unroll 4
+#pragma unroll 8
     for (int s2 = 0; s2 < nslots; ++s2) {
-      const float ms = __ldcg(hp + s2 * (RVO + 2) + RVO);
+      const float ms = sm_m[gi * nslots + s2];
       const float f = ms == -INFINITY ? 0.f : exp2f(ms - M);
-      L = fmaf(f, __ldcg(hp + s2 * (RVO + 2) + RVO + 1), L);
+      L = fmaf(f, sm_l[gi * nslots + s2], L);
       O = fmaf(f, __ldcg(hp + s2 * (RVO + 2) + c), O);
     }
     __nv_bfloat16 ob = __float2bfloat16_rn(O / L);
