@@ -582,7 +582,9 @@ static cudaError_t launch_partial(const DecodeAttnArgs& a, int width, const uint
   }
 }
 
-static const bool g_dec_attn_v2 = getenv("ZDC_DEC_ATTN_V1") == nullptr;
+// v2 (decode_attn2.cu) is opt-in (ZDC_DEC_ATTN_V2=1): measured 12.3 us vs 11.3 us for v1 at the
+// c2 shape in round 1 (profiles/r01/NOTES.md)
+static const bool g_dec_attn_v2 = getenv("ZDC_DEC_ATTN_V2") != nullptr;
 static bool v2_width(int w) { return w == 32 || w == 64 || w == 96 || w == 128; }
 
 cudaError_t launch_decode_attention(const DecodeAttnArgs& a_in, cudaStream_t stream) {
