@@ -246,9 +246,16 @@ int64_t zdc_kernel_launch_count(void);
  * graph); zdc_profile_read synchronises, writes per class the summed milliseconds and launch
  * counts since the previous read, clears them, and returns the number of classes:
  * 0 a1 prefill GEMM, 1 a3 prefill attention, 2 a5 prefill GEMM, 3 a1 decode GEMV,
- * 4 a3 decode attention (partial), 5 a3 decode combine, 6 a5 decode GEMV, 7 other. */
+ * 4 a3 decode attention (partial), 5 a3 decode combine, 6 a5 decode GEMV, 7 other,
+ * 8 fused decode layer-step (a1+a2+a3+a5 in one kernel, B <= 8 uniform-rank layers). */
 void zdc_profile(int enable);
 int zdc_profile_read(float* ms, int64_t* count, int n);
+/* Diagnostics: with ZDC_FUSED_TRACE set in the environment, the fused decode kernel records
+ * per-CTA %globaltimer stamps (ns) of its last launch, [CTA][16]: 0 start, 1 input staged,
+ * 2 phase-1 done, 3 after grid barrier 1, 4 phase-2 done, 5 after grid barrier 2, 6 merge done,
+ * 7 end, 8/9/10 producer finished issuing phase 1/2/3.  Copies n values (synchronising the
+ * device); returns the count copied, 0 when tracing is off, -1 on a CUDA error. */
+int zdc_trace_read(unsigned long long* out, int n);
 
 #ifdef __cplusplus
 }

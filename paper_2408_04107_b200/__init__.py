@@ -32,7 +32,7 @@ EXPORTED_SYMBOLS = ["zdc_last_error", "zdc_version", "zdc_fold_weights", "zdc_ct
                     "zdc_cache_export", "zdc_cache_length", "zdc_scores_export", "zdc_cache_reset", "zdc_last_lse",
                     "zdc_gemm_bf16", "zdc_gemv_bf16", "zdc_prefill_attention_bf16",
                     "zdc_decode_attention_workspace", "zdc_decode_attention_bf16",
-                    "zdc_kernel_launch_count", "zdc_profile", "zdc_profile_read"]
+                    "zdc_kernel_launch_count", "zdc_profile", "zdc_profile_read", "zdc_trace_read"]
 
 
 class ZdcError(RuntimeError):
@@ -106,6 +106,7 @@ def lib():
             "zdc_kernel_launch_count": ([], I64),
             "zdc_profile": ([ctypes.c_int], None),
             "zdc_profile_read": ([ctypes.POINTER(F), ctypes.POINTER(I64), ctypes.c_int], ctypes.c_int),
+            "zdc_trace_read": ([ctypes.POINTER(ctypes.c_uint64), ctypes.c_int], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -132,6 +133,16 @@ PROFILE_CLASSES = ["a1_prefill_gemm", "a3_prefill_attention", "a5_prefill_gemm",
 def profile(enable: bool):
     """Per-kernel-class CUDA-event timing inside the library (zdc_profile)."""
     lib().zdc_profile(1 if enable else 0)
+
+
+def trace_read(n_cta: int = 148):
+    """Fused decode kernel timeline of its last launch (ZDC_FUSED_TRACE): uint64 [n_cta][16] ns."""
+    import numpy as np
+    buf = (ctypes.c_uint64 * (n_cta * 16))()
+    got = lib().zdc_trace_read(buf, n_cta * 16)
+    if got <= 0:
+        return None
+    return np.frombuffer(buf, dtype=np.uint64).reshape(n_cta, 16).copy()
 
 
 def profile_read():

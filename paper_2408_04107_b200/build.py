@@ -4,6 +4,7 @@ python -m paper_2408_04107_b200.build        # or __graft_entry__.build()
 """
 from __future__ import annotations
 
+import concurrent.futures
 import glob
 import os
 import subprocess
@@ -42,19 +43,22 @@ def build(verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     headers = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
         glob.glob(os.path.join(INCLUDE, "*.h"))
-    objs = []
+    objs, jobs = [], []
     for src in sorted(glob.glob(os.path.join(CSRC, "*.cu"))):
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
         if _stale(obj, [src] + headers):
-            out = _run([NVCC] + CUDA_FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-c", src, "-o", obj])
-            if verbose:
-                print(out)
+            jobs.append([NVCC] + CUDA_FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-c", src, "-o", obj])
         objs.append(obj)
     for src in sorted(glob.glob(os.path.join(CSRC, "*.cpp"))):
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
         if _stale(obj, [src] + headers):
-            _run(["g++"] + CXX_FLAGS + ["-c", src, "-o", obj])
+            jobs.append(["g++"] + CXX_FLAGS + ["-c", src, "-o", obj])
         objs.append(obj)
+    # translation units compile in parallel (the fused decode kernel alone has 80 template instances)
+    with concurrent.futures.ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        for out in ex.map(_run, jobs):
+            if verbose:
+                print(out)
     if _stale(LIB, objs):
         _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs +
              ["-Xcompiler", "-fopenmp", "-lgomp", "-ldl", "-lpthread"])

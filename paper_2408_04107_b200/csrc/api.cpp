@@ -207,6 +207,8 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
   s = align_up(s + static_cast<int64_t>(max_batch) * d.n_heads * 128 * (max_rv + 2) * 4, 256);
   c->s_cnt = s;  // decode-attention merge counters [max_batch][N_kv], kept at zero between launches
   s = align_up(s + static_cast<int64_t>(max_batch) * d.n_kv_heads * 4, 256);
+  c->s_gbar = s;  // fused decode grid barrier, kept self-resetting between launches
+  s = align_up(s + 64, 256);
   if (any_split) {  // staged K'/V' of a split layer before packing, compaction indices, new-row staging
     const int64_t kv_rows = static_cast<int64_t>(max_batch) * d.n_kv_heads * max_seq;
     c->s_ks = s;
@@ -245,6 +247,7 @@ zdc_status zdc_ctx_bind(zdc_ctx* c, void* w, void* cache, void* scratch) {
   ZDC_CUDA_TRY(cudaMemset(c->cache, 0, c->cache_bytes));
   ZDC_CUDA_TRY(cudaMemset(c->scratch, 0, c->scratch_bytes));
   ZDC_CUDA_TRY(cudaMemset(c->w, 0, c->weight_bytes));
+  fused_trace_buffer();  // allocated here (if ZDC_FUSED_TRACE is set), never inside a graph capture
   c->len.assign(c->dims.n_layers, 0);
   c->sp_layer.assign(c->dims.n_layers, 0);
   c->batch = 0;
@@ -486,6 +489,45 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
     }
     const uint16_t* wqkv = reinterpret_cast<const uint16_t*>(c->w + L.w_qkv);
     const uint16_t* wo = reinterpret_cast<const uint16_t*>(c->w + L.w_o);
+    static const bool fused_on = !(getenv("ZDC_DEC_FUSED") && atoi(getenv("ZDC_DEC_FUSED")) == 0);
+    if (fused_on && !L.split && decode_fused_supported(B, L.rk_p, c->G)) {
+      // the whole layer-step in one persistent kernel (decode_fused.cu)
+      DecFusedArgs f;
+      f.wqkv = wqkv;
+      f.wo = wo;
+      f.x = xin;
+      f.ldx = d;
+      f.y = y;
+      f.ldy = d;
+      f.q = reinterpret_cast<uint16_t*>(c->scratch + c->s_q);
+      f.ldq = L.nq;
+      f.kc = reinterpret_cast<uint16_t*>(c->cache + L.k_off);
+      f.vc = reinterpret_cast<uint16_t*>(c->cache + L.v_off);
+      f.len_ptr = len_dev;
+      f.part = reinterpret_cast<float*>(c->scratch + c->s_part);
+      f.lse = reinterpret_cast<float*>(c->scratch + c->s_lse);
+      f.gbar = reinterpret_cast<unsigned long long*>(c->scratch + c->s_gbar);
+      f.o = reinterpret_cast<uint16_t*>(c->scratch + c->s_o);
+      f.counters = reinterpret_cast<int*>(c->scratch + c->s_cnt);
+      f.trace = fused_trace_buffer();
+      f.B = B;
+      f.d = d;
+      f.n_qkv = L.n_qkv;
+      f.nq = L.nq;
+      f.nk = L.nk;
+      f.Nh = Nh;
+      f.Nkv = Nkv;
+      f.S_cap = c->max_seq;
+      f.splits = decode_fused_splits(B, Nkv);
+      f.ko_p = L.ko_p;
+      f.scale = 1.0f / std::sqrt(static_cast<float>(c->dims.d_head));
+      g_prof_class = kProfDecodeLayer;
+      cudaError_t e = launch_decode_fused(f, L.rk_p, s);
+      g_prof_class = kProfOther;
+      if (e == cudaSuccess) continue;
+      if (e != cudaErrorNotSupported) return fail(ZDC_ERR_CUDA, "fused decode layer %d: %s", l, cudaGetErrorString(e));
+      cudaGetLastError();
+    }
     g_prof_class = kProfGemvQkv;
     if (B <= 8)
       ZDC_CUDA_TRY(launch_gemv(wqkv, xin, d, B, L.n_qkv, d, e1, s));
@@ -528,6 +570,24 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
     a.rv = L.rv_p;
     a.scale = 1.0f / std::sqrt(static_cast<float>(c->dims.d_head));
     a.splits = decode_splits(B, Nkv, c->max_seq);
+    {
+      // L2 prefetch of the weights read next (bit 0: this layer's W_O^R, bit 1: the next layer's
+      // W_QKV^R, wrapping to layer 0 for the next step); off by default (ZDC_DEC_L2PF=3 enables it):
+      // measured slower in round 1, the prefetches delay the attention's own bulk copies
+      static const int pf_mode = getenv("ZDC_DEC_L2PF") ? atoi(getenv("ZDC_DEC_L2PF")) : 0;
+      const LayerInfo& N = c->layers[(l + 1) % c->dims.n_layers];
+      if (pf_mode & 1) {
+        a.pf_ptr[0] = wo;
+        a.pf_bytes[0] = static_cast<int64_t>(d) * L.ko_p * 2;
+      }
+      if (pf_mode & 2) {
+        a.pf_ptr[1] = c->w + N.w_qkv;
+        a.pf_bytes[1] = static_cast<int64_t>(N.n_qkv) * d * 2;
+      }
+      // only while the working set stays well inside the 126 MB L2 (the KV rows stream through too)
+      if (a.pf_bytes[0] > (64ll << 20)) a.pf_bytes[0] = 0;
+      if (a.pf_bytes[0] + a.pf_bytes[1] > (64ll << 20)) a.pf_bytes[1] = 0;
+    }
     if (L.split) {
       a.len_ptr = nullptr;
       a.n0_ptr = reinterpret_cast<const int*>(c->cache + L.ni_off);

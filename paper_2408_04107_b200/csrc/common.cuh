@@ -204,4 +204,31 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+// ---- bf16 <-> f32 helpers of the CUDA-core (decode) kernels
+__device__ __forceinline__ void bf16x8_to_f32(uint4 v, float (&f)[8]) {
+  f[0] = __uint_as_float(v.x << 16);
+  f[1] = __uint_as_float(v.x & 0xFFFF0000u);
+  f[2] = __uint_as_float(v.y << 16);
+  f[3] = __uint_as_float(v.y & 0xFFFF0000u);
+  f[4] = __uint_as_float(v.z << 16);
+  f[5] = __uint_as_float(v.z & 0xFFFF0000u);
+  f[6] = __uint_as_float(v.w << 16);
+  f[7] = __uint_as_float(v.w & 0xFFFF0000u);
+}
+
+__device__ __forceinline__ float dot8(uint4 w, uint4 x) {
+  float a[8], b[8];
+  bf16x8_to_f32(w, a);
+  bf16x8_to_f32(x, b);
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s = fmaf(a[i], b[i], s);
+  return s;
+}
+
+__device__ __forceinline__ uint16_t f32_to_bf16_bits(float f) {
+  __nv_bfloat16 h = __float2bfloat16_rn(f);
+  return *reinterpret_cast<uint16_t*>(&h);
+}
+
 }  // namespace zdc

@@ -25,27 +25,6 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
   return r;
 }
 
-__device__ __forceinline__ void bf16x8_to_f32(uint4 v, float (&f)[8]) {
-  f[0] = __uint_as_float(v.x << 16);
-  f[1] = __uint_as_float(v.x & 0xFFFF0000u);
-  f[2] = __uint_as_float(v.y << 16);
-  f[3] = __uint_as_float(v.y & 0xFFFF0000u);
-  f[4] = __uint_as_float(v.z << 16);
-  f[5] = __uint_as_float(v.z & 0xFFFF0000u);
-  f[6] = __uint_as_float(v.w << 16);
-  f[7] = __uint_as_float(v.w & 0xFFFF0000u);
-}
-
-__device__ __forceinline__ float dot8(uint4 w, uint4 x) {
-  float a[8], b[8];
-  bf16x8_to_f32(w, a);
-  bf16x8_to_f32(x, b);
-  float s = 0.f;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) s = fmaf(a[i], b[i], s);
-  return s;
-}
-
 // one bf16 output element (m, n) through the same destination map as the GEMM epilogue
 __device__ __forceinline__ void store_scalar(const Epilogue& e, int m, int n, uint16_t val) {
   uint16_t* dst;
@@ -70,10 +49,6 @@ __device__ __forceinline__ void store_scalar(const Epilogue& e, int m, int n, ui
   *dst = val;
 }
 
-__device__ __forceinline__ uint16_t f32_to_bf16_bits(float f) {
-  __nv_bfloat16 h = __float2bfloat16_rn(f);
-  return *reinterpret_cast<uint16_t*>(&h);
-}
 
 // ------------------------------------------------------------------ skinny projection
 // pdl_mode bit 0: trigger the dependent launch only after this kernel's own wait (bounds the
@@ -328,6 +303,19 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
     } else if (threadIdx.x == 0 && np > 0) {
       l2_prefetch(kp + (row0 + p0) * RK, static_cast<uint32_t>(np) * RK * 2u);
       l2_prefetch(vp + (row0 + p0) * RV, static_cast<uint32_t>(np) * RV * 2u);
+    }
+  }
+  if (threadIdx.x == 32 && pool == 0) {
+    // read-only weights of the following kernels -> L2 (this kernel's own rows were issued first)
+    const int64_t ncta = static_cast<int64_t>(gridDim.x) * gridDim.y * gridDim.z;
+    const int64_t cta = (static_cast<int64_t>(b) * gridDim.y + g) * gridDim.x + split;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      if (a.pf_bytes[i] <= 0) continue;
+      const int64_t per = ((a.pf_bytes[i] + ncta - 1) / ncta + 15) & ~int64_t(15);
+      const int64_t lo = cta * per, hi = min(a.pf_bytes[i], lo + per);
+      for (int64_t o = lo; o < hi; o += 32768)
+        l2_prefetch(static_cast<const uint8_t*>(a.pf_ptr[i]) + o, static_cast<uint32_t>(min(static_cast<int64_t>(32768), hi - o)));
     }
   }
   pdl_wait();

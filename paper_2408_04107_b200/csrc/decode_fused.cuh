@@ -1,0 +1,633 @@
+// decode_fused.cuh — the whole decode layer-step (SURVEY.md §8(a) a1, a2, a3, a5 for one new token
+// per sequence, "Q^h is obtained from the input token, while K^h and V^h of all previous
+// tokens are retrieved from the KVC") as ONE persistent kernel, one CTA per SM:
+//
+//   phase 1  a1 + a2   [Q'|K'|V'] = x W_QKV^R (Eq. 1 on the folded, truncated weights); Q' to
+//                      staging, K'/V' of the new token straight into the cache at position len
+//   grid barrier
+//   phase 2  a3        split-K attention over the cached rows and the new row at head dim r
+//                      (Eqs. 2-3, scale 1/sqrt(d_h)); one unnormalised partial (m, l, o) per
+//                      (sequence, KV head, chunk) item; the last CTA to finish a chunk of a
+//                      (sequence, KV head) LSE-merges its chunks -> O' (bf16) and the row LSE
+//   grid barrier
+//   phase 3  a5        y = O' W_O^R (Eq. 4 with the folded W_L), O' staged in shared memory
+//
+// Why one kernel: at B <= 8 a decode layer reads ~85 MB (c2) and the three separate kernels are
+// each latency-bound at their start and tail.  Here a single producer thread per CTA streams
+// every byte the CTA will read — its W_QKV rows, its K'/V' chunk rows, its W_O rows — through one
+// ring of shared-memory slots with cp.async.bulk, in consumption order.  It never waits for the
+// grid barriers (weights and cached rows do not depend on them), so HBM stays busy across the
+// phase boundaries; only the consumers wait.
+//
+// Consumers: warps 0..kNW-1; ring slot sequence number k is consumed by warp k % kNW, which owns
+// the sub-ring slots [w*spw, (w+1)*spw) (every mbarrier wait is for the phase right after the last one
+// the waiter observed; see profiles/r01/NOTES.md on parity aliasing).
+//
+// Rounding points (DESIGN.md §4 faithful mode): Q'/K'/V' to bf16 in phase 1; P = exp(s - m)
+// rounded to bf16 before PV with l taken from the unrounded P; O' to bf16 after the merge; y to bf16.
+#pragma once
+#include "common.cuh"
+#include "kernels.h"
+
+#include <algorithm>
+#include <cstdlib>
+
+namespace zdc {
+
+static constexpr float kLog2eF = 1.4426950408889634f;
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Grid barrier on a monotonic 64-bit arrival counter, called by ONE thread per CTA after a
+// CTA-level barrier (the release is cumulative over the CTA's writes ordered by it, as in
+// CUTLASS's generic barrier).  The arrival is a fire-and-forget red.release; the thread then
+// polls with ld.acquire until the counter reaches `target` = base + k * n for the k-th barrier of
+// this launch, where base (a multiple of n) is read after the PDL wait (every earlier launch has
+// completed, and no CTA of this launch can have passed barrier 1 yet).  No reset is needed.
+__device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned long long target) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
+  while (ld_acquire_u64(bar) < target) {
+  }
+}
+
+__device__ __forceinline__ int atomic_add_acq_rel(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define ZDC_STAMP(i)                                                        \
+  do {                                                                      \
+    if (a.trace) a.trace[static_cast<int64_t>(blockIdx.x) * 16 + (i)] = globaltimer(); \
+  } while (0)
+
+// consumer warps per CTA (one more warp is the producer)
+static constexpr int kNW = 8;
+static constexpr int kNC = kNW * 32;  // consumer threads
+
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kNC) : "memory"); }
+
+// ring slot of sequence number k (8 consumer warps, spw slots each)
+__device__ __forceinline__ int ring_slot(int k, int spw) { return (k % kNW) * spw + (k / kNW) % spw; }
+__device__ __forceinline__ uint32_t ring_parity(int k, int spw) { return ((k / kNW) / spw) & 1; }
+
+template <int RK>
+struct Dims2 {
+  // V'/O' dims a lane owns: RK >= 32: [lane*DPL, lane*DPL + DPL); RK == 16: dim lane (lanes < 16)
+  static constexpr int DPL = RK >= 32 ? RK / 32 : 1;
+};
+
+// o[gi][:] += P[j][gi] V'[j][lane-owned dims] (P broadcast from lane j)
+template <int RK, int G>
+__device__ __forceinline__ void pv_row(const uint16_t* Vs, int j, int lane, const float (&pb)[G],
+                                       float (&o)[G][Dims2<RK>::DPL]) {
+  constexpr int DPL = Dims2<RK>::DPL;
+  {
+    float v[DPL];
+    if constexpr (RK >= 32) {
+      const uint16_t* vr = Vs + j * RK + lane * DPL;
+      if constexpr (DPL == 4) {
+        const uint2 u = *reinterpret_cast<const uint2*>(vr);
+        v[0] = __uint_as_float(u.x << 16);
+        v[1] = __uint_as_float(u.x & 0xFFFF0000u);
+        v[2] = __uint_as_float(u.y << 16);
+        v[3] = __uint_as_float(u.y & 0xFFFF0000u);
+      } else if constexpr (DPL == 2) {
+        const uint32_t u = *reinterpret_cast<const uint32_t*>(vr);
+        v[0] = __uint_as_float(u << 16);
+        v[1] = __uint_as_float(u & 0xFFFF0000u);
+      } else {
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) v[i] = __uint_as_float(static_cast<uint32_t>(vr[i]) << 16);
+      }
+    } else {
+      v[0] = lane < RK ? __uint_as_float(static_cast<uint32_t>(Vs[j * RK + lane]) << 16) : 0.f;
+    }
+#pragma unroll
+    for (int gi = 0; gi < G; ++gi) {
+      const float pj = __shfl_sync(0xffffffffu, pb[gi], j);
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) o[gi][i] = fmaf(pj, v[i], o[gi][i]);
+    }
+  }
+}
+
+// One warp folds up to 32 key rows (lane j = row j) into its running softmax state for the G
+// query heads of the KV group: s = q.k * scale * log2(e); m, l, o rescaled online.
+template <int RK, int G>
+__device__ __forceinline__ void attn_rows(const uint16_t* Ks, const uint16_t* Vs, int np, const float* qf, float scl,
+                                          float (&m)[G], float (&l)[G], float (&o)[G][Dims2<RK>::DPL], int lane) {
+  constexpr int UK = RK / 8, DPL = Dims2<RK>::DPL;
+  float s[G], s2[G];
+#pragma unroll
+  for (int gi = 0; gi < G; ++gi) s[gi] = s2[gi] = 0.f;
+  if (lane < np) {
+    const int rot = lane % UK;  // rotated chunk order: the 32 rows of a warp hit distinct banks
+#pragma unroll
+    for (int kk = 0; kk < UK; ++kk) {
+      int kc = kk + rot;
+      if (kc >= UK) kc -= UK;
+      float kf[8];
+      bf16x8_to_f32(*reinterpret_cast<const uint4*>(Ks + lane * RK + kc * 8), kf);
+#pragma unroll
+      for (int gi = 0; gi < G; ++gi) {
+        const float4 q0 = *reinterpret_cast<const float4*>(qf + gi * RK + kc * 8);
+        const float4 q1 = *reinterpret_cast<const float4*>(qf + gi * RK + kc * 8 + 4);
+        float x0 = s[gi], x1 = s2[gi];  // two independent FMA chains
+        x0 = fmaf(q0.x, kf[0], x0);
+        x1 = fmaf(q0.y, kf[1], x1);
+        x0 = fmaf(q0.z, kf[2], x0);
+        x1 = fmaf(q0.w, kf[3], x1);
+        x0 = fmaf(q1.x, kf[4], x0);
+        x1 = fmaf(q1.y, kf[5], x1);
+        x0 = fmaf(q1.z, kf[6], x0);
+        x1 = fmaf(q1.w, kf[7], x1);
+        s[gi] = x0;
+        s2[gi] = x1;
+      }
+    }
+  }
+#pragma unroll
+  for (int gi = 0; gi < G; ++gi) s[gi] += s2[gi];
+  float pb[G];
+#pragma unroll
+  for (int gi = 0; gi < G; ++gi) {
+    const float sv = lane < np ? s[gi] * scl : -INFINITY;
+    float mx = sv;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    const float mn = fmaxf(m[gi], mx);  // finite: np >= 1
+    const float alpha = exp2f(m[gi] - mn);
+    const float p = lane < np ? exp2f(sv - mn) : 0.f;
+    float ps = p;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
+    l[gi] = l[gi] * alpha + ps;
+    m[gi] = mn;
+    pb[gi] = __bfloat162float(__float2bfloat16_rn(p));
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) o[gi][i] *= alpha;
+  }
+  // o += P V' (lane-owned dims); full slots take the unrolled path
+  if (np == 32) {
+#pragma unroll 8
+    for (int j = 0; j < 32; ++j) pv_row<RK, G>(Vs, j, lane, pb, o);
+    return;
+  }
+  for (int j = 0; j < np; ++j) pv_row<RK, G>(Vs, j, lane, pb, o);
+}
+
+// GEMV rows of one ring slot: out[b][row] = W[row] . xs[b] for NB input rows (B valid).
+template <int NB>
+__device__ __forceinline__ void gemv_rows(const uint8_t* slot, int nrows, int K, const uint4* xs4, int xw8,
+                                          int lane, float (&acc)[NB], int r) {
+  const uint4* w = reinterpret_cast<const uint4*>(slot) + static_cast<size_t>(r) * (K >> 3);
+#pragma unroll
+  for (int b = 0; b < NB; ++b) acc[b] = 0.f;
+  const int kc = K >> 3;
+#pragma unroll 4
+  for (int c = lane; c < kc; c += 32) {
+    const uint4 wv = w[c];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc[b] += dot8(wv, xs4[b * xw8 + c]);
+  }
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], off);
+  }
+}
+
+template <int NB, int RK, int G>
+__global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFusedArgs a) {
+  constexpr int DPL = Dims2<RK>::DPL;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int SB = a.slot_bytes, spw = a.spw, nslot = kNW * spw;
+  const int xw = a.xw, xw8 = xw >> 3;
+  uint8_t* ring = smem;
+  uint16_t* xs = reinterpret_cast<uint16_t*>(smem + static_cast<size_t>(nslot) * SB);  // [NB][xw]
+  float* qf = reinterpret_cast<float*>(xs + NB * xw);                                  // [G][RK]
+  float* wst = qf + G * RK;                                                            // [kNW][G][RK+2]
+  uint16_t* nrow = reinterpret_cast<uint16_t*>(wst + kNW * G * (RK + 2));             // [2][RK]
+  float* pst = reinterpret_cast<float*>(nrow + 2 * RK);  // staged partials [B*Nh][splits][RK+2] (stage_part)
+  float* wts = pst + a.pst_floats;                       // merge weights [B*Nh][splits] (stage_part)
+  uint64_t* full = reinterpret_cast<uint64_t*>(wts + a.wts_floats);
+  uint64_t* empty = full + nslot;
+  uint64_t* lenbar = empty + nslot;
+  uint64_t* pbar = lenbar + 1;
+  unsigned long long* s_base = reinterpret_cast<unsigned long long*>(pbar + 1);
+  int* s_len = reinterpret_cast<int*>(s_base + 1);
+  int* s_flag = s_len + 1;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const int cta = blockIdx.x, ncta = gridDim.x;
+  if (tid == kNC) {
+    for (int s = 0; s < nslot; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(lenbar, 1);
+    mbar_init(pbar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid == 0) ZDC_STAMP(0);
+
+  // ---- static work split (identical in producer and consumers)
+  const int d = a.d, ko = a.ko_p;
+  const int per1 = (a.n_qkv + ncta - 1) / ncta;
+  const int r1a = min(a.n_qkv, cta * per1), r1b = min(a.n_qkv, r1a + per1);
+  const int rps1 = SB / (d * 2);
+  const int n1 = (r1b - r1a + rps1 - 1) / rps1;
+  const int per3 = (d + ncta - 1) / ncta;
+  const int r3a = min(d, cta * per3), r3b = min(d, r3a + per3);
+  const int rps3 = SB / (ko * 2);
+  const int n3 = (r3b - r3a + rps3 - 1) / rps3;
+  const int nitems = a.B * a.Nkv * a.splits;
+  const int RPS = 32;  // K'/V' rows per slot: [32][RK] K' then [32][RK] V'
+
+  if (warp == kNW) {
+    // ================= producer (one thread): every HBM byte of this CTA, in consumption order
+    if (lane == 0) {
+      int k = 0;
+      // phase 1 weights: static, issued before the dependency wait
+      for (int r = r1a; r < r1b; r += rps1, ++k) {
+        const int nr = min(rps1, r1b - r);
+        const int s = ring_slot(k, spw);
+        if ((k / kNW) >= spw) mbar_wait(&empty[s], ring_parity(k, spw) ^ 1);
+        const uint32_t bytes = static_cast<uint32_t>(nr) * d * 2u;
+        mbar_arrive_expect_tx(&full[s], bytes);
+        bulk_g2s(ring + static_cast<size_t>(s) * SB, a.wqkv + static_cast<int64_t>(r) * d, bytes, &full[s]);
+      }
+      ZDC_STAMP(8);
+      // the cache length is read by a consumer after the PDL wait (the previous step of this
+      // layer may be the predecessor kernel)
+      mbar_wait(lenbar, 0);
+      const int L = *s_len, L1 = L + 1;
+      const int chunk = (L1 + a.splits - 1) / a.splits;
+      for (int it = cta; it < nitems; it += ncta) {
+        const int sp = it % a.splits, g = (it / a.splits) % a.Nkv, b = it / (a.splits * a.Nkv);
+        const int s0 = sp * chunk, e0 = min(min(L1, s0 + chunk), L);  // cached rows only
+        const int64_t row0 = (static_cast<int64_t>(b) * a.Nkv + g) * a.S_cap;
+        for (int p = s0; p < e0; p += RPS, ++k) {
+          const int np = min(RPS, e0 - p);
+          const int s = ring_slot(k, spw);
+          if ((k / kNW) >= spw) mbar_wait(&empty[s], ring_parity(k, spw) ^ 1);
+          const uint32_t bytes = static_cast<uint32_t>(np) * RK * 2u;
+          mbar_arrive_expect_tx(&full[s], 2 * bytes);
+          uint8_t* dst = ring + static_cast<size_t>(s) * SB;
+          bulk_g2s(dst, a.kc + (row0 + p) * RK, bytes, &full[s]);
+          bulk_g2s(dst + RPS * RK * 2, a.vc + (row0 + p) * RK, bytes, &full[s]);
+        }
+      }
+      ZDC_STAMP(9);
+      // phase 3 weights
+      for (int r = r3a; r < r3b; r += rps3, ++k) {
+        const int nr = min(rps3, r3b - r);
+        const int s = ring_slot(k, spw);
+        if ((k / kNW) >= spw) mbar_wait(&empty[s], ring_parity(k, spw) ^ 1);
+        const uint32_t bytes = static_cast<uint32_t>(nr) * ko * 2u;
+        mbar_arrive_expect_tx(&full[s], bytes);
+        bulk_g2s(ring + static_cast<size_t>(s) * SB, a.wo + static_cast<int64_t>(r) * ko, bytes, &full[s]);
+      }
+      ZDC_STAMP(10);
+    }
+    return;
+  }
+
+  // ================= consumers (warps 0..kNW-1)
+  pdl_wait();
+  pdl_trigger();
+  if (tid == 0) {
+    *s_len = *a.len_ptr;
+    *s_base = ld_acquire_u64(a.gbar) / ncta * ncta;
+    mbar_arrive(lenbar);
+  }
+  {
+    const int kcx = d >> 3;
+    uint4* xs4 = reinterpret_cast<uint4*>(xs);
+    for (int i = tid; i < NB * kcx; i += kNC) {
+      const int b = i / kcx, c = i - b * kcx;
+      xs4[b * xw8 + c] = b < a.B ? *reinterpret_cast<const uint4*>(a.x + b * a.ldx + c * 8) : make_uint4(0, 0, 0, 0);
+    }
+  }
+  consumer_sync();
+  if (tid == 0) ZDC_STAMP(1);
+  const int L = *s_len, L1 = L + 1;
+  const uint4* xs4 = reinterpret_cast<const uint4*>(xs);
+
+  // ---- phase 1: a1 + a2
+  for (int k = warp; k < n1; k += kNW) {
+    const int s = ring_slot(k, spw);
+    mbar_wait(&full[s], ring_parity(k, spw));
+    const int rb = r1a + k * rps1, nr = min(rps1, r1b - rb);
+    for (int r = 0; r < nr; ++r) {
+      float acc[NB];
+      gemv_rows<NB>(ring + static_cast<size_t>(s) * SB, nr, d, xs4, xw8, lane, acc, r);
+      const int n = rb + r;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        if (lane == b && b < a.B) {
+          const uint16_t v = f32_to_bf16_bits(acc[b]);
+          if (n < a.nq) {
+            a.q[b * a.ldq + n] = v;
+          } else if (n < a.nq + a.nk) {
+            const int nn = n - a.nq, g = nn / RK, c = nn - g * RK;
+            a.kc[((static_cast<int64_t>(b) * a.Nkv + g) * a.S_cap + L) * RK + c] = v;
+          } else {
+            const int nn = n - a.nq - a.nk, g = nn / RK, c = nn - g * RK;
+            a.vc[((static_cast<int64_t>(b) * a.Nkv + g) * a.S_cap + L) * RK + c] = v;
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  consumer_sync();
+  if (tid == 0) {
+    ZDC_STAMP(2);
+    grid_barrier(a.gbar, *s_base + ncta);
+    ZDC_STAMP(3);
+  }
+  consumer_sync();
+
+  // ---- phase 2: a3 partials
+  const float scl = a.scale * kLog2eF;
+  const int chunk = (L1 + a.splits - 1) / a.splits;
+  int kb = n1;
+  for (int it = cta; it < nitems; it += ncta) {
+    const int sp = it % a.splits, g = (it / a.splits) % a.Nkv, b = it / (a.splits * a.Nkv);
+    const int s0 = sp * chunk, s1 = min(L1, s0 + chunk), e0 = min(s1, L);
+    const int ns = e0 > s0 ? (e0 - s0 + RPS - 1) / RPS : 0;
+    const bool has_new = s0 <= L && L < s1;
+    for (int i = tid; i < G * RK; i += kNC) {
+      const int gi = i / RK, c = i - gi * RK;
+      const uint16_t u = __ldcg(reinterpret_cast<const unsigned short*>(a.q) + b * a.ldq + (g * G + gi) * RK + c);
+      qf[i] = __uint_as_float(static_cast<uint32_t>(u) << 16);
+    }
+    if (has_new && warp == 0) {
+      const int64_t row = ((static_cast<int64_t>(b) * a.Nkv + g) * a.S_cap + L) * RK;
+      for (int c = lane; c < RK; c += 32) {
+        nrow[c] = __ldcg(reinterpret_cast<const unsigned short*>(a.kc) + row + c);
+        nrow[RK + c] = __ldcg(reinterpret_cast<const unsigned short*>(a.vc) + row + c);
+      }
+    }
+    consumer_sync();
+    float m[G], l[G], o[G][DPL];
+#pragma unroll
+    for (int gi = 0; gi < G; ++gi) {
+      m[gi] = -INFINITY;
+      l[gi] = 0.f;
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) o[gi][i] = 0.f;
+    }
+    for (int t = (warp - kb % kNW + kNW) % kNW; t < ns; t += kNW) {
+      const int k = kb + t;
+      const int s = ring_slot(k, spw);
+      mbar_wait(&full[s], ring_parity(k, spw));
+      const uint16_t* Ks = reinterpret_cast<const uint16_t*>(ring + static_cast<size_t>(s) * SB);
+      attn_rows<RK, G>(Ks, Ks + RPS * RK, min(RPS, e0 - (s0 + t * RPS)), qf, scl, m, l, o, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if (has_new && warp == 0) attn_rows<RK, G>(nrow, nrow + RK, 1, qf, scl, m, l, o, lane);
+    // warp states -> shared memory, then the CTA merges them into this item's partial
+    float* ws = wst + warp * G * (RK + 2);
+#pragma unroll
+    for (int gi = 0; gi < G; ++gi) {
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) {
+        const int c = RK >= 32 ? lane * DPL + i : lane;
+        if (c < RK) ws[gi * (RK + 2) + c] = o[gi][i];
+      }
+      if (lane == 0) {
+        ws[gi * (RK + 2) + RK] = m[gi];
+        ws[gi * (RK + 2) + RK + 1] = l[gi];
+      }
+    }
+    consumer_sync();
+    if (tid == 0) ZDC_STAMP(11);
+    for (int i = tid; i < G * RK; i += kNC) {
+      const int gi = i / RK, c = i - gi * RK;
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < kNW; ++w) M = fmaxf(M, wst[(w * G + gi) * (RK + 2) + RK]);
+      float O = 0.f, Ls = 0.f;
+      if (M != -INFINITY) {
+#pragma unroll
+        for (int w = 0; w < kNW; ++w) {
+          const float* e = wst + (w * G + gi) * (RK + 2);
+          const float f = exp2f(e[RK] - M);  // 0 for warps without rows (m = -inf)
+          O = fmaf(e[c], f, O);
+          Ls = fmaf(e[RK + 1], f, Ls);
+        }
+      }
+      float* dst = a.part + ((static_cast<int64_t>(b) * a.Nh + g * G + gi) * a.splits + sp) * (RK + 2);
+      dst[c] = O;
+      if (c == 0) {
+        dst[RK] = M;
+        dst[RK + 1] = Ls;
+      }
+    }
+    // without staging (large partial sets) the last CTA to finish a chunk of (b, g) merges them:
+    // O' = sum_s o_s 2^(m_s - M) / sum_s l_s 2^(m_s - M), LSE = (M + log2 L) ln 2
+    consumer_sync();
+    if (!a.stage_part && tid == 0) {
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      *s_flag = atomic_add_acq_rel(a.counters + b * a.Nkv + g, 1) == a.splits - 1;
+    }
+    consumer_sync();
+    if (!a.stage_part && *s_flag) {
+      for (int i = tid; i < G * RK; i += kNC) {
+        const int gi = i / RK, c = i - gi * RK;
+        const float* hp = a.part + (static_cast<int64_t>(b) * a.Nh + g * G + gi) * a.splits * (RK + 2);
+        float M = -INFINITY;
+        for (int s2 = 0; s2 < a.splits; ++s2) M = fmaxf(M, __ldcg(hp + s2 * (RK + 2) + RK));
+        float O = 0.f, Ls = 0.f;
+        for (int s2 = 0; s2 < a.splits; ++s2) {
+          const float ms = __ldcg(hp + s2 * (RK + 2) + RK);
+          const float f = ms == -INFINITY ? 0.f : exp2f(ms - M);
+          O = fmaf(f, __ldcg(hp + s2 * (RK + 2) + c), O);
+          Ls = fmaf(f, __ldcg(hp + s2 * (RK + 2) + RK + 1), Ls);
+        }
+        a.o[b * ko + (g * G + gi) * RK + c] = f32_to_bf16_bits(O / Ls);
+        if (c == 0 && a.lse) a.lse[b * a.Nh + g * G + gi] = (M + log2f(Ls)) / kLog2eF;
+      }
+      if (tid == 0) a.counters[b * a.Nkv + g] = 0;
+    }
+    consumer_sync();
+    kb += ns;
+  }
+  consumer_sync();
+  if (tid == 0) {
+    ZDC_STAMP(4);
+    grid_barrier(a.gbar, *s_base + 2 * static_cast<unsigned long long>(ncta));
+    ZDC_STAMP(5);
+  }
+  consumer_sync();
+  if (cta == 0 && tid == 0) *a.len_ptr = L1;  // every reader of the length has passed barrier 1
+
+  if (tid == 0) ZDC_STAMP(14);
+  if (a.stage_part) {
+    // ---- every CTA merges all heads from ONE bulk copy of the partials (one round trip
+    // instead of the atomic + merge + reload chain): the same LSE merge as above
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> async-proxy reads
+      mbar_arrive_expect_tx(pbar, static_cast<uint32_t>(a.pst_bytes));
+      bulk_g2s(pst, a.part, static_cast<uint32_t>(a.pst_bytes), pbar);
+    }
+    mbar_wait(pbar, 0);
+    if (tid == 0) ZDC_STAMP(12);
+    const int S2 = a.splits;
+    for (int i = tid; i < a.B * a.Nh * S2; i += kNC) {
+      // merge weight of split s2 of head (b, h): 2^(m_s - M) / L, thread per (bh, s2)
+      const int bh = i / S2;
+      const float* hp = pst + bh * S2 * (RK + 2);
+      float M = -INFINITY;
+      for (int s2 = 0; s2 < S2; ++s2) M = fmaxf(M, hp[s2 * (RK + 2) + RK]);
+      float Ls = 0.f;
+      for (int s2 = 0; s2 < S2; ++s2) {
+        const float ms = hp[s2 * (RK + 2) + RK];
+        Ls += ms == -INFINITY ? 0.f : exp2f(ms - M) * hp[s2 * (RK + 2) + RK + 1];
+      }
+      const float ms = hp[(i - bh * S2) * (RK + 2) + RK];
+      wts[i] = ms == -INFINITY ? 0.f : exp2f(ms - M) / Ls;
+      if (i == bh * S2 && cta == 0 && a.lse) a.lse[bh] = (M + log2f(Ls)) / kLog2eF;
+    }
+    consumer_sync();
+    if (tid == 0) ZDC_STAMP(13);
+    {
+      // O' chunks of 8 columns (one head never straddles a chunk: RK % 16 == 0)
+      const int ko8 = ko >> 3, hk8 = (a.Nh * RK) >> 3;
+      uint4* xo = reinterpret_cast<uint4*>(xs);
+      for (int i = tid; i < NB * ko8; i += kNC) {
+        const int b = i / ko8, c8 = i - b * ko8;
+        float v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = 0.f;
+        if (b < a.B && c8 < hk8) {
+          const int h = (c8 * 8) / RK, cc = c8 * 8 - h * RK;
+          const int bh = b * a.Nh + h;
+          for (int s2 = 0; s2 < S2; ++s2) {
+            const float w = wts[bh * S2 + s2];
+            const float* hp = pst + (bh * S2 + s2) * (RK + 2) + cc;  // 8-byte aligned ((RK+2) even)
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+              const float2 f = *reinterpret_cast<const float2*>(hp + e);
+              v[e] = fmaf(w, f.x, v[e]);
+              v[e + 1] = fmaf(w, f.y, v[e + 1]);
+            }
+          }
+        }
+        xo[b * xw8 + c8] = make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
+                                      pack_bf16x2(v[6], v[7]));
+      }
+    }
+  } else {
+    // ---- O' (merged by the last CTA of each (b, g), published by barrier 2) -> shared memory
+    const int ko8 = ko >> 3, hk8 = (a.Nh * RK) >> 3;
+    uint4* xo = reinterpret_cast<uint4*>(xs);
+    for (int i = tid; i < NB * ko8; i += kNC) {
+      const int b = i / ko8, c = i - b * ko8;
+      xo[b * xw8 + c] = b < a.B && c < hk8 ? __ldcg(reinterpret_cast<const uint4*>(a.o + b * ko) + c)
+                                           : make_uint4(0, 0, 0, 0);
+    }
+  }
+  consumer_sync();
+  if (tid == 0) ZDC_STAMP(6);
+
+  // ---- phase 3: a5
+  for (int t = (warp - kb % kNW + kNW) % kNW; t < n3; t += kNW) {
+    const int k = kb + t;
+    const int s = ring_slot(k, spw);
+    mbar_wait(&full[s], ring_parity(k, spw));
+    const int rb = r3a + t * rps3, nr = min(rps3, r3b - rb);
+    for (int r = 0; r < nr; ++r) {
+      float acc[NB];
+      gemv_rows<NB>(ring + static_cast<size_t>(s) * SB, nr, ko, xs4, xw8, lane, acc, r);
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+        if (lane == b && b < a.B) a.y[b * a.ldy + rb + r] = f32_to_bf16_bits(acc[b]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  if (a.trace) {
+    consumer_sync();
+    if (tid == 0) ZDC_STAMP(7);
+  }
+}
+
+// ------------------------------------------------------------------ host
+// ring cap (ZDC_FUSED_RING_KB); the launcher fits as many slots as the 227 KB of shared memory allow
+static const int kFusedRingBytes = getenv("ZDC_FUSED_RING_KB") ? atoi(getenv("ZDC_FUSED_RING_KB")) * 1024 : 192 * 1024;
+
+template <int NB, int RK, int G>
+inline cudaError_t launch_fused_t(DecFusedArgs a, cudaStream_t stream) {
+  const int slot = std::max(std::max(a.d * 2, 4 * 32 * RK), a.ko_p * 2);  // a1 row | 32 K'+V' rows | a5 row
+  a.slot_bytes = slot;
+  a.xw = std::max(a.d, a.ko_p);
+  constexpr size_t kSmemMax = 227 * 1024;
+  const size_t fixed = static_cast<size_t>(NB) * a.xw * 2 + G * RK * 4 + kNW * G * (RK + 2) * 4 + 2 * RK * 2 + 48;
+  // the partials of every head staged by one bulk copy after barrier 2 when they fit (<= 48 KB)
+  const int64_t pbytes = (static_cast<int64_t>(a.B) * a.Nh * a.splits * (RK + 2) * 4 + 15) / 16 * 16;
+  const int64_t wfl = (static_cast<int64_t>(a.B) * a.Nh * a.splits + 3) / 4 * 4;
+  const size_t per_slot = static_cast<size_t>(slot) + 16;  // slot + its two mbarriers
+  a.stage_part = pbytes <= 48 * 1024 && fixed + pbytes + wfl * 4 + kNW * per_slot <= kSmemMax ? 1 : 0;
+  a.pst_floats = a.stage_part ? pbytes / 4 : 0;
+  a.pst_bytes = a.stage_part ? pbytes : 0;
+  a.wts_floats = a.stage_part ? wfl : 0;
+  const size_t base = fixed + static_cast<size_t>(a.pst_floats + a.wts_floats) * 4;
+  int spw = static_cast<int>(std::min<size_t>(kFusedRingBytes / (kNW * slot), (kSmemMax - std::min(base, kSmemMax)) / (kNW * per_slot)));
+  if (spw < 1) return cudaErrorNotSupported;
+  a.spw = spw;
+  const size_t smem = base + static_cast<size_t>(kNW * spw) * per_slot;
+  if (smem > kSmemMax) return cudaErrorNotSupported;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(decode_fused_kernel<NB, RK, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  prof_mark(stream, true, g_prof_class);
+  cudaError_t e = launch_k(decode_fused_kernel<NB, RK, G>, dim3(num_sms()), dim3(kNC + 32), smem, stream, g_pdl, a);
+  prof_mark(stream, false, g_prof_class);
+  ++g_launches;
+  return e;
+}
+
+template <int NB, int RK>
+inline cudaError_t launch_fused_g(const DecFusedArgs& a, int G, cudaStream_t s) {
+  switch (G) {
+    case 1: return launch_fused_t<NB, RK, 1>(a, s);
+    case 2: return launch_fused_t<NB, RK, 2>(a, s);
+    case 4: return launch_fused_t<NB, RK, 4>(a, s);
+    case 8: return launch_fused_t<NB, RK, 8>(a, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+template <int NB>
+inline cudaError_t launch_fused_r(const DecFusedArgs& a, int RK, int G, cudaStream_t s) {
+  switch (RK) {
+    case 16: return launch_fused_g<NB, 16>(a, G, s);
+    case 32: return launch_fused_g<NB, 32>(a, G, s);
+    case 64: return launch_fused_g<NB, 64>(a, G, s);
+    case 96: return launch_fused_g<NB, 96>(a, G, s);
+    case 128: return launch_fused_g<NB, 128>(a, G, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+}  // namespace zdc

@@ -96,6 +96,10 @@ struct DecodeAttnArgs {
   float* part = nullptr;  // scratch [B][Nh][2 * splits][rv + 2]
   int* counters = nullptr;  // scratch [B][Nkv] zero-initialised; the last CTA per (b, g) merges
   int prefetch_before_wait = 1;  // stage cached rows before the PDL dependency wait
+  // weights of the next kernels (a5 of this layer, a1 of the next) pulled into L2 while this
+  // latency-bound kernel leaves HBM bandwidth idle; split evenly over the CTAs
+  const void* pf_ptr[2] = {nullptr, nullptr};
+  int64_t pf_bytes[2] = {0, 0};
   int B = 0, Nh = 0, Nkv = 0;
   float scale = 0.f;
   int splits = 1;
@@ -105,6 +109,38 @@ cudaError_t launch_decode2_partial(const DecodeAttnArgs& a, int width, const uin
                                    int pool, int slot0, int nslots, cudaStream_t s);
 int decode2_splits(int B, int Nkv, int len, int width, int G);
 int decode_splits(int B, int Nkv, int len);
+
+// ---- the fused decode layer-step (decode_fused.cu): a1 + a2 + a3 + a5 in one persistent
+// kernel for B <= 8 on uniform-rank layers (width RK = r_k = r_v padded)
+struct DecFusedArgs {
+  const uint16_t* wqkv = nullptr;  // [n_qkv][d]
+  const uint16_t* wo = nullptr;    // [d][ko_p]
+  const uint16_t* x = nullptr;     // [B][ldx]
+  int64_t ldx = 0;
+  uint16_t* y = nullptr;           // [B][ldy]
+  int64_t ldy = 0;
+  uint16_t* q = nullptr;           // Q' staging [B][ldq]
+  int64_t ldq = 0;
+  uint16_t* kc = nullptr;          // K'/V' cache: row (b, g, p) at ((b*Nkv+g)*S_cap + p)*RK
+  uint16_t* vc = nullptr;
+  int* len_ptr = nullptr;          // cached rows before this step; advanced by the kernel
+  float* part = nullptr;           // [B][Nh][splits][RK+2]
+  float* lse = nullptr;            // [B][Nh]
+  uint16_t* o = nullptr;           // O' [B][ko_p] (bf16), written by the last CTA of each (b, g)
+  int* counters = nullptr;         // [B][Nkv] arrival counters, zero between launches
+  unsigned long long* gbar = nullptr;  // grid barrier arrival counter (monotonic), zero-initialised
+  unsigned long long* trace = nullptr;  // optional [ncta][16] globaltimer stamps (ZDC_FUSED_TRACE)
+  int B = 0, d = 0, n_qkv = 0, nq = 0, nk = 0, Nh = 0, Nkv = 0, S_cap = 0, splits = 1, ko_p = 0;
+  float scale = 0.f;
+  // ring geometry (set by the launcher)
+  int slot_bytes = 0, spw = 0, xw = 0;
+  int stage_part = 0, pst_floats = 0, wts_floats = 0;
+  int64_t pst_bytes = 0;
+};
+bool decode_fused_supported(int B, int RK, int G);
+int decode_fused_splits(int B, int Nkv);
+cudaError_t launch_decode_fused(const DecFusedArgs& a, int RK, cudaStream_t s);
+unsigned long long* fused_trace_buffer();  // null unless ZDC_FUSED_TRACE is set
 
 // ---- weight packing (load time): f32/bf16 full-rank folded -> truncated, padded, bf16
 cudaError_t launch_pack_weights_bf16(const uint16_t* wq, const uint16_t* wk, const uint16_t* wv,
@@ -156,7 +192,7 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 
 // ---- per-kernel-class timing (zdc_profile): CUDA events bracket each launch on its stream
 enum ProfClass { kProfGemmQkv = 0, kProfAttnPrefill, kProfGemmO, kProfGemvQkv, kProfAttnDecode, kProfAttnCombine,
-                 kProfGemvO, kProfOther, kProfClasses };
+                 kProfGemvO, kProfOther, kProfDecodeLayer, kProfClasses };
 extern int g_prof_class;  // class the next launches belong to (set by the orchestration)
 void prof_mark(cudaStream_t s, bool begin, int cls);
 bool prof_enabled();
