@@ -510,6 +510,17 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
       f.o = reinterpret_cast<uint16_t*>(c->scratch + c->s_o);
       f.counters = reinterpret_cast<int*>(c->scratch + c->s_cnt);
       f.trace = fused_trace_buffer();
+      {
+        // the layer expected next (l + 1, wrapping to 0 for the next step) when it takes this
+        // path too; opt-in with ZDC_FUSED_L2PF=1 (measured slower in round 1: the prefetch traffic
+        // delays the grid-barrier polls on the critical path)
+        static const bool pf = getenv("ZDC_FUSED_L2PF") && atoi(getenv("ZDC_FUSED_L2PF")) != 0;
+        const LayerInfo& N = c->layers[(l + 1) % c->dims.n_layers];
+        if (pf && !N.split) {
+          f.next_wqkv = reinterpret_cast<const uint16_t*>(c->w + N.w_qkv);
+          f.next_n_qkv = N.n_qkv;
+        }
+      }
       f.B = B;
       f.d = d;
       f.n_qkv = L.n_qkv;

@@ -20,7 +20,7 @@
 // phase boundaries; only the consumers wait.
 //
 // Consumers: warps 0..kNW-1; ring slot sequence number k is consumed by warp k % kNW, which owns
-// the sub-ring slots [w*spw, (w+1)*spw) (every mbarrier wait is for the phase right after the last one
+// its own sub-ring of slots (ProducerCursor / ConsumerCursor) (every mbarrier wait is for the phase right after the last one
 // the waiter observed; see profiles/r01/NOTES.md on parity aliasing).
 //
 // Rounding points (DESIGN.md §4 faithful mode): Q'/K'/V' to bf16 in phase 1; P = exp(s - m)
@@ -76,9 +76,35 @@ static constexpr int kNC = kNW * 32;  // consumer threads
 
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kNC) : "memory"); }
 
-// ring slot of sequence number k (8 consumer warps, spw slots each)
-__device__ __forceinline__ int ring_slot(int k, int spw) { return (k % kNW) * spw + (k / kNW) % spw; }
-__device__ __forceinline__ uint32_t ring_parity(int k, int spw) { return ((k / kNW) / spw) & 1; }
+// Ring geometry: sequence number k is consumed by warp w = k % kNW, which owns a sub-ring of
+// spw slots, plus one more when w < ex (so the ring can use every slot the shared memory holds).
+// Both sides walk the sequence incrementally (no integer division on the issue path: the single
+// producer thread issues every slot of the CTA, so its per-slot cost is on the critical path).
+struct ProducerCursor {
+  int w = 0, u = 0;        // k = u * kNW + w
+  int pa = 0, fa = 0;      // position / phase in the sub-rings of spw + 1 slots
+  int pb = 0, fb = 0;      // ... of spw slots
+  __device__ __forceinline__ int slot(int spw, int ex) const { return w * spw + min(w, ex) + (w < ex ? pa : pb); }
+  __device__ __forceinline__ uint32_t phase(int ex) const { return w < ex ? fa : fb; }
+  __device__ __forceinline__ bool reuse(int spw, int ex) const { return u >= spw + (w < ex ? 1 : 0); }
+  __device__ __forceinline__ void next(int spw) {
+    if (++w == kNW) {
+      w = 0;
+      ++u;
+      if (++pa == spw + 1) { pa = 0; fa ^= 1; }
+      if (++pb == spw) { pb = 0; fb ^= 1; }
+    }
+  }
+};
+struct ConsumerCursor {  // warp w's slots, visited in sequence order
+  int base, n, pos = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ ConsumerCursor(int w, int spw, int ex) : base(w * spw + min(w, ex)), n(spw + (w < ex ? 1 : 0)) {}
+  __device__ __forceinline__ int slot() const { return base + pos; }
+  __device__ __forceinline__ void next() {
+    if (++pos == n) { pos = 0; ph ^= 1; }
+  }
+};
 
 template <int RK>
 struct Dims2 {
@@ -186,32 +212,55 @@ __device__ __forceinline__ void attn_rows(const uint16_t* Ks, const uint16_t* Vs
   for (int j = 0; j < np; ++j) pv_row<RK, G>(Vs, j, lane, pb, o);
 }
 
-// GEMV rows of one ring slot: out[b][row] = W[row] . xs[b] for NB input rows (B valid).
-template <int NB>
-__device__ __forceinline__ void gemv_rows(const uint8_t* slot, int nrows, int K, const uint4* xs4, int xw8,
-                                          int lane, float (&acc)[NB], int r) {
-  const uint4* w = reinterpret_cast<const uint4*>(slot) + static_cast<size_t>(r) * (K >> 3);
-#pragma unroll
-  for (int b = 0; b < NB; ++b) acc[b] = 0.f;
+// GEMV of R consecutive rows of one ring slot against NB input rows (x converted once per
+// chunk and shared by the R rows): acc[r][b] = W[r0 + r] . xs[b]
+template <int NB, int R>
+__device__ __forceinline__ void gemv_rows(const uint8_t* slot, int K, const uint4* xs4, int xw8, int lane,
+                                          float (&acc)[R][NB], int r0) {
   const int kc = K >> 3;
-#pragma unroll 4
+  const uint4* w = reinterpret_cast<const uint4*>(slot) + static_cast<size_t>(r0) * kc;
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc[r][b] = 0.f;
+#pragma unroll 2
   for (int c = lane; c < kc; c += 32) {
-    const uint4 wv = w[c];
+    uint4 wv[R];
 #pragma unroll
-    for (int b = 0; b < NB; ++b) acc[b] += dot8(wv, xs4[b * xw8 + c]);
+    for (int r = 0; r < R; ++r) wv[r] = w[r * kc + c];
+    float xf[NB][8];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) bf16x8_to_f32(xs4[b * xw8 + c], xf[b]);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      float wf[8];
+      bf16x8_to_f32(wv[r], wf);
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        float x0 = 0.f, x1 = 0.f;  // two short chains per chunk
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+          x0 = fmaf(wf[e], xf[b][e], x0);
+          x1 = fmaf(wf[e + 1], xf[b][e + 1], x1);
+        }
+        acc[r][b] += x0 + x1;
+      }
+    }
   }
 #pragma unroll
-  for (int b = 0; b < NB; ++b) {
+  for (int r = 0; r < R; ++r)
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], off);
-  }
+    for (int b = 0; b < NB; ++b) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc[r][b] += __shfl_xor_sync(0xffffffffu, acc[r][b], off);
+    }
 }
 
 template <int NB, int RK, int G>
 __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFusedArgs a) {
   constexpr int DPL = Dims2<RK>::DPL;
   extern __shared__ __align__(128) uint8_t smem[];
-  const int SB = a.slot_bytes, spw = a.spw, nslot = kNW * spw;
+  const int SB = a.slot_bytes, spw = a.spw, ex = a.ring_extra, nslot = kNW * spw + ex;
   const int xw = a.xw, xw8 = xw >> 3;
   uint8_t* ring = smem;
   uint16_t* xs = reinterpret_cast<uint16_t*>(smem + static_cast<size_t>(nslot) * SB);  // [NB][xw]
@@ -219,8 +268,7 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
   float* wst = qf + G * RK;                                                            // [kNW][G][RK+2]
   uint16_t* nrow = reinterpret_cast<uint16_t*>(wst + kNW * G * (RK + 2));             // [2][RK]
   float* pst = reinterpret_cast<float*>(nrow + 2 * RK);  // staged partials [B*Nh][splits][RK+2] (stage_part)
-  float* wts = pst + a.pst_floats;                       // merge weights [B*Nh][splits] (stage_part)
-  uint64_t* full = reinterpret_cast<uint64_t*>(wts + a.wts_floats);
+  uint64_t* full = reinterpret_cast<uint64_t*>(pst + a.pst_floats);
   uint64_t* empty = full + nslot;
   uint64_t* lenbar = empty + nslot;
   uint64_t* pbar = lenbar + 1;
@@ -259,11 +307,13 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
     // ================= producer (one thread): every HBM byte of this CTA, in consumption order
     if (lane == 0) {
       int k = 0;
+      ProducerCursor pc;
       // phase 1 weights: static, issued before the dependency wait
       for (int r = r1a; r < r1b; r += rps1, ++k) {
         const int nr = min(rps1, r1b - r);
-        const int s = ring_slot(k, spw);
-        if ((k / kNW) >= spw) mbar_wait(&empty[s], ring_parity(k, spw) ^ 1);
+        const int s = pc.slot(spw, ex);
+        if (pc.reuse(spw, ex)) mbar_wait(&empty[s], pc.phase(ex) ^ 1);
+        pc.next(spw);
         const uint32_t bytes = static_cast<uint32_t>(nr) * d * 2u;
         mbar_arrive_expect_tx(&full[s], bytes);
         bulk_g2s(ring + static_cast<size_t>(s) * SB, a.wqkv + static_cast<int64_t>(r) * d, bytes, &full[s]);
@@ -280,8 +330,9 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
         const int64_t row0 = (static_cast<int64_t>(b) * a.Nkv + g) * a.S_cap;
         for (int p = s0; p < e0; p += RPS, ++k) {
           const int np = min(RPS, e0 - p);
-          const int s = ring_slot(k, spw);
-          if ((k / kNW) >= spw) mbar_wait(&empty[s], ring_parity(k, spw) ^ 1);
+          const int s = pc.slot(spw, ex);
+          if (pc.reuse(spw, ex)) mbar_wait(&empty[s], pc.phase(ex) ^ 1);
+          pc.next(spw);
           const uint32_t bytes = static_cast<uint32_t>(np) * RK * 2u;
           mbar_arrive_expect_tx(&full[s], 2 * bytes);
           uint8_t* dst = ring + static_cast<size_t>(s) * SB;
@@ -293,13 +344,24 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
       // phase 3 weights
       for (int r = r3a; r < r3b; r += rps3, ++k) {
         const int nr = min(rps3, r3b - r);
-        const int s = ring_slot(k, spw);
-        if ((k / kNW) >= spw) mbar_wait(&empty[s], ring_parity(k, spw) ^ 1);
+        const int s = pc.slot(spw, ex);
+        if (pc.reuse(spw, ex)) mbar_wait(&empty[s], pc.phase(ex) ^ 1);
+        pc.next(spw);
         const uint32_t bytes = static_cast<uint32_t>(nr) * ko * 2u;
         mbar_arrive_expect_tx(&full[s], bytes);
         bulk_g2s(ring + static_cast<size_t>(s) * SB, a.wo + static_cast<int64_t>(r) * ko, bytes, &full[s]);
       }
       ZDC_STAMP(10);
+      // every byte of this layer is requested: pull this CTA's share of the NEXT layer's W_QKV^R
+      // rows into L2, so its phase 1 streams from L2 while this layer's critical path finishes
+      if (a.next_wqkv != nullptr) {
+        const int pn = (a.next_n_qkv + ncta - 1) / ncta;
+        const int na = min(a.next_n_qkv, cta * pn), nb = min(a.next_n_qkv, na + pn);
+        const uint8_t* base = reinterpret_cast<const uint8_t*>(a.next_wqkv + static_cast<int64_t>(na) * d);
+        const int64_t bytes = static_cast<int64_t>(nb - na) * d * 2;
+        for (int64_t o = 0; o < bytes; o += 65536)
+          l2_prefetch(base + o, static_cast<uint32_t>(min(static_cast<int64_t>(65536), bytes - o)));
+      }
     }
     return;
   }
@@ -323,21 +385,23 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
   consumer_sync();
   if (tid == 0) ZDC_STAMP(1);
   const int L = *s_len, L1 = L + 1;
+  ConsumerCursor cc(warp, spw, ex);
   const uint4* xs4 = reinterpret_cast<const uint4*>(xs);
 
   // ---- phase 1: a1 + a2
   for (int k = warp; k < n1; k += kNW) {
-    const int s = ring_slot(k, spw);
-    mbar_wait(&full[s], ring_parity(k, spw));
+    const int s = cc.slot();
+    mbar_wait(&full[s], cc.ph);
+    cc.next();
     const int rb = r1a + k * rps1, nr = min(rps1, r1b - rb);
     for (int r = 0; r < nr; ++r) {
-      float acc[NB];
-      gemv_rows<NB>(ring + static_cast<size_t>(s) * SB, nr, d, xs4, xw8, lane, acc, r);
+      float acc[1][NB];
+      gemv_rows<NB, 1>(ring + static_cast<size_t>(s) * SB, d, xs4, xw8, lane, acc, r);
       const int n = rb + r;
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
         if (lane == b && b < a.B) {
-          const uint16_t v = f32_to_bf16_bits(acc[b]);
+          const uint16_t v = f32_to_bf16_bits(acc[0][b]);
           if (n < a.nq) {
             a.q[b * a.ldq + n] = v;
           } else if (n < a.nq + a.nk) {
@@ -393,8 +457,9 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
     }
     for (int t = (warp - kb % kNW + kNW) % kNW; t < ns; t += kNW) {
       const int k = kb + t;
-      const int s = ring_slot(k, spw);
-      mbar_wait(&full[s], ring_parity(k, spw));
+      const int s = cc.slot();
+      mbar_wait(&full[s], cc.ph);
+      cc.next();
       const uint16_t* Ks = reinterpret_cast<const uint16_t*>(ring + static_cast<size_t>(s) * SB);
       attn_rows<RK, G>(Ks, Ks + RPS * RK, min(RPS, e0 - (s0 + t * RPS)), qf, scl, m, l, o, lane);
       __syncwarp();
@@ -489,25 +554,9 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
     mbar_wait(pbar, 0);
     if (tid == 0) ZDC_STAMP(12);
     const int S2 = a.splits;
-    for (int i = tid; i < a.B * a.Nh * S2; i += kNC) {
-      // merge weight of split s2 of head (b, h): 2^(m_s - M) / L, thread per (bh, s2)
-      const int bh = i / S2;
-      const float* hp = pst + bh * S2 * (RK + 2);
-      float M = -INFINITY;
-      for (int s2 = 0; s2 < S2; ++s2) M = fmaxf(M, hp[s2 * (RK + 2) + RK]);
-      float Ls = 0.f;
-      for (int s2 = 0; s2 < S2; ++s2) {
-        const float ms = hp[s2 * (RK + 2) + RK];
-        Ls += ms == -INFINITY ? 0.f : exp2f(ms - M) * hp[s2 * (RK + 2) + RK + 1];
-      }
-      const float ms = hp[(i - bh * S2) * (RK + 2) + RK];
-      wts[i] = ms == -INFINITY ? 0.f : exp2f(ms - M) / Ls;
-      if (i == bh * S2 && cta == 0 && a.lse) a.lse[bh] = (M + log2f(Ls)) / kLog2eF;
-    }
-    consumer_sync();
-    if (tid == 0) ZDC_STAMP(13);
     {
-      // O' chunks of 8 columns (one head never straddles a chunk: RK % 16 == 0)
+      // O' chunks of 8 columns (one head never straddles a chunk: RK % 16 == 0); each thread
+      // merges its head's splits in one pass: M = max m_s, L = sum 2^(m_s-M) l_s, O' = sum 2^(m_s-M) o_s / L
       const int ko8 = ko >> 3, hk8 = (a.Nh * RK) >> 3;
       uint4* xo = reinterpret_cast<uint4*>(xs);
       for (int i = tid; i < NB * ko8; i += kNC) {
@@ -518,16 +567,26 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
         if (b < a.B && c8 < hk8) {
           const int h = (c8 * 8) / RK, cc = c8 * 8 - h * RK;
           const int bh = b * a.Nh + h;
+          const float* hp = pst + bh * S2 * (RK + 2);
+          float M = -INFINITY;
+          for (int s2 = 0; s2 < S2; ++s2) M = fmaxf(M, hp[s2 * (RK + 2) + RK]);
+          float Ls = 0.f;
           for (int s2 = 0; s2 < S2; ++s2) {
-            const float w = wts[bh * S2 + s2];
-            const float* hp = pst + (bh * S2 + s2) * (RK + 2) + cc;  // 8-byte aligned ((RK+2) even)
+            const float* e2 = hp + s2 * (RK + 2);
+            const float ms = e2[RK];
+            const float f = ms == -INFINITY ? 0.f : exp2f(ms - M);
+            Ls = fmaf(f, e2[RK + 1], Ls);
 #pragma unroll
             for (int e = 0; e < 8; e += 2) {
-              const float2 f = *reinterpret_cast<const float2*>(hp + e);
-              v[e] = fmaf(w, f.x, v[e]);
-              v[e + 1] = fmaf(w, f.y, v[e + 1]);
+              const float2 o2 = *reinterpret_cast<const float2*>(e2 + cc + e);  // 8-byte aligned
+              v[e] = fmaf(f, o2.x, v[e]);
+              v[e + 1] = fmaf(f, o2.y, v[e + 1]);
             }
           }
+          const float inv = 1.f / Ls;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] *= inv;
+          if (cc == 0 && cta == 0 && a.lse) a.lse[bh] = (M + log2f(Ls)) / kLog2eF;
         }
         xo[b * xw8 + c8] = make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
                                       pack_bf16x2(v[6], v[7]));
@@ -549,15 +608,27 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
   // ---- phase 3: a5
   for (int t = (warp - kb % kNW + kNW) % kNW; t < n3; t += kNW) {
     const int k = kb + t;
-    const int s = ring_slot(k, spw);
-    mbar_wait(&full[s], ring_parity(k, spw));
+    const int s = cc.slot();
+    mbar_wait(&full[s], cc.ph);
+    cc.next();
     const int rb = r3a + t * rps3, nr = min(rps3, r3b - rb);
-    for (int r = 0; r < nr; ++r) {
-      float acc[NB];
-      gemv_rows<NB>(ring + static_cast<size_t>(s) * SB, nr, ko, xs4, xw8, lane, acc, r);
+    int r = 0;
+    for (; r + 2 <= nr; r += 2) {  // row pairs: two independent dot products per lane
+      float acc[2][NB];
+      gemv_rows<NB, 2>(ring + static_cast<size_t>(s) * SB, ko, xs4, xw8, lane, acc, r);
 #pragma unroll
       for (int b = 0; b < NB; ++b)
-        if (lane == b && b < a.B) a.y[b * a.ldy + rb + r] = f32_to_bf16_bits(acc[b]);
+        if (lane == b && b < a.B) {
+          a.y[b * a.ldy + rb + r] = f32_to_bf16_bits(acc[0][b]);
+          a.y[b * a.ldy + rb + r + 1] = f32_to_bf16_bits(acc[1][b]);
+        }
+    }
+    if (r < nr) {
+      float acc[1][NB];
+      gemv_rows<NB, 1>(ring + static_cast<size_t>(s) * SB, ko, xs4, xw8, lane, acc, r);
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+        if (lane == b && b < a.B) a.y[b * a.ldy + rb + r] = f32_to_bf16_bits(acc[0][b]);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -570,7 +641,7 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
 
 // ------------------------------------------------------------------ host
 // ring cap (ZDC_FUSED_RING_KB); the launcher fits as many slots as the 227 KB of shared memory allow
-static const int kFusedRingBytes = getenv("ZDC_FUSED_RING_KB") ? atoi(getenv("ZDC_FUSED_RING_KB")) * 1024 : 192 * 1024;
+static const int kFusedRingBytes = getenv("ZDC_FUSED_RING_KB") ? atoi(getenv("ZDC_FUSED_RING_KB")) * 1024 : 224 * 1024;
 
 template <int NB, int RK, int G>
 inline cudaError_t launch_fused_t(DecFusedArgs a, cudaStream_t stream) {
@@ -581,17 +652,16 @@ inline cudaError_t launch_fused_t(DecFusedArgs a, cudaStream_t stream) {
   const size_t fixed = static_cast<size_t>(NB) * a.xw * 2 + G * RK * 4 + kNW * G * (RK + 2) * 4 + 2 * RK * 2 + 48;
   // the partials of every head staged by one bulk copy after barrier 2 when they fit (<= 48 KB)
   const int64_t pbytes = (static_cast<int64_t>(a.B) * a.Nh * a.splits * (RK + 2) * 4 + 15) / 16 * 16;
-  const int64_t wfl = (static_cast<int64_t>(a.B) * a.Nh * a.splits + 3) / 4 * 4;
   const size_t per_slot = static_cast<size_t>(slot) + 16;  // slot + its two mbarriers
-  a.stage_part = pbytes <= 48 * 1024 && fixed + pbytes + wfl * 4 + kNW * per_slot <= kSmemMax ? 1 : 0;
+  a.stage_part = pbytes <= 48 * 1024 && fixed + pbytes + kNW * per_slot <= kSmemMax ? 1 : 0;
   a.pst_floats = a.stage_part ? pbytes / 4 : 0;
   a.pst_bytes = a.stage_part ? pbytes : 0;
-  a.wts_floats = a.stage_part ? wfl : 0;
-  const size_t base = fixed + static_cast<size_t>(a.pst_floats + a.wts_floats) * 4;
-  int spw = static_cast<int>(std::min<size_t>(kFusedRingBytes / (kNW * slot), (kSmemMax - std::min(base, kSmemMax)) / (kNW * per_slot)));
-  if (spw < 1) return cudaErrorNotSupported;
-  a.spw = spw;
-  const size_t smem = base + static_cast<size_t>(kNW * spw) * per_slot;
+  const size_t base = fixed + static_cast<size_t>(a.pst_floats) * 4;
+  const int nslot = static_cast<int>(std::min<size_t>(kFusedRingBytes / slot, (kSmemMax - std::min(base, kSmemMax)) / per_slot));
+  if (nslot < kNW) return cudaErrorNotSupported;
+  a.spw = nslot / kNW;
+  a.ring_extra = nslot % kNW;
+  const size_t smem = base + static_cast<size_t>(nslot) * per_slot;
   if (smem > kSmemMax) return cudaErrorNotSupported;
   static bool attr = false;
   if (!attr) {

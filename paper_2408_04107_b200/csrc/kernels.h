@@ -129,12 +129,14 @@ struct DecFusedArgs {
   uint16_t* o = nullptr;           // O' [B][ko_p] (bf16), written by the last CTA of each (b, g)
   int* counters = nullptr;         // [B][Nkv] arrival counters, zero between launches
   unsigned long long* gbar = nullptr;  // grid barrier arrival counter (monotonic), zero-initialised
+  const uint16_t* next_wqkv = nullptr;  // optional: W_QKV^R of the layer expected next (L2 prefetch)
+  int next_n_qkv = 0;
   unsigned long long* trace = nullptr;  // optional [ncta][16] globaltimer stamps (ZDC_FUSED_TRACE)
   int B = 0, d = 0, n_qkv = 0, nq = 0, nk = 0, Nh = 0, Nkv = 0, S_cap = 0, splits = 1, ko_p = 0;
   float scale = 0.f;
   // ring geometry (set by the launcher)
-  int slot_bytes = 0, spw = 0, xw = 0;
-  int stage_part = 0, pst_floats = 0, wts_floats = 0;
+  int slot_bytes = 0, spw = 0, ring_extra = 0, xw = 0;
+  int stage_part = 0, pst_floats = 0;
   int64_t pst_bytes = 0;
 };
 bool decode_fused_supported(int B, int RK, int G);

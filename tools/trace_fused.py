@@ -17,7 +17,7 @@ import zdc_synth as Z  # noqa: E402
 
 NAMES = {0: "start", 1: "x staged", 2: "phase1 done", 3: "barrier1 out", 4: "phase2 done", 5: "barrier2 out",
          6: "merge done", 7: "end", 8: "prod: ph1 issued", 9: "prod: ph2 issued", 10: "prod: all issued",
-         11: "ph2 rows done", 14: "len updated", 12: "partials staged", 13: "merge weights"}
+         11: "ph2 rows done", 14: "len updated", 12: "partials staged"}
 
 
 def main():
