@@ -510,6 +510,10 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
       f.o = reinterpret_cast<uint16_t*>(c->scratch + c->s_o);
       f.counters = reinterpret_cast<int*>(c->scratch + c->s_cnt);
       f.trace = fused_trace_buffer();
+      // opt-in (ZDC_FUSED_SELF_PF=1): measured slower in round 1, the prefetch traffic delays the
+      // latency-critical input load of the consumers
+      static const int self_pf = getenv("ZDC_FUSED_SELF_PF") ? atoi(getenv("ZDC_FUSED_SELF_PF")) : 0;
+      f.self_prefetch = self_pf;
       {
         // the layer expected next (l + 1, wrapping to 0 for the next step) when it takes this
         // path too; opt-in with ZDC_FUSED_L2PF=1 (measured slower in round 1: the prefetch traffic

@@ -308,6 +308,17 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
     if (lane == 0) {
       int k = 0;
       ProducerCursor pc;
+      if (a.self_prefetch) {
+        // the ring holds the first nslot rows; the rest of this CTA's phase-1 rows go to L2 now,
+        // while HBM is otherwise idle (the consumers are still waiting for the predecessor)
+        const int r_pf = r1a + nslot * rps1;
+        if (r_pf < r1b) {
+          const uint8_t* base = reinterpret_cast<const uint8_t*>(a.wqkv + static_cast<int64_t>(r_pf) * d);
+          const int64_t bytes = static_cast<int64_t>(r1b - r_pf) * d * 2;
+          for (int64_t o = 0; o < bytes; o += 32768)
+            l2_prefetch(base + o, static_cast<uint32_t>(min(static_cast<int64_t>(32768), bytes - o)));
+        }
+      }
       // phase 1 weights: static, issued before the dependency wait
       for (int r = r1a; r < r1b; r += rps1, ++k) {
         const int nr = min(rps1, r1b - r);

@@ -131,6 +131,7 @@ struct DecFusedArgs {
   unsigned long long* gbar = nullptr;  // grid barrier arrival counter (monotonic), zero-initialised
   const uint16_t* next_wqkv = nullptr;  // optional: W_QKV^R of the layer expected next (L2 prefetch)
   int next_n_qkv = 0;
+  int self_prefetch = 0;                 // L2-prefetch this CTA's phase-1 rows beyond the ring at start
   unsigned long long* trace = nullptr;  // optional [ncta][16] globaltimer stamps (ZDC_FUSED_TRACE)
   int B = 0, d = 0, n_qkv = 0, nq = 0, nk = 0, Nh = 0, Nkv = 0, S_cap = 0, splits = 1, ko_p = 0;
   float scale = 0.f;
