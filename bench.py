@@ -52,6 +52,8 @@ def parse():
     p.add_argument("--prompt", type=int, default=2048)
     p.add_argument("--rank", type=int, default=64)
     p.add_argument("--layers", type=int, default=32)
+    p.add_argument("--decode-calls", default="layer", choices=["layer", "chain"],
+                   help="decode step as 32 per-layer zdc_decode calls (same x per layer) or one chained call")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--profile-only", action="store_true", help="one eager step (for ncu), no JSON")
@@ -345,9 +347,13 @@ def run_zdc(args):
             launches["prefill"] += zdc.last_launch_count()
     g_dec = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g_dec, stream=stream):
-        for l in range(L):
-            ctx.decode(x_buf, y_dec, l, l + 1)
+        if args.decode_calls == "chain":
+            ctx.decode(x_buf, y_dec, 0, L)  # the model's dataflow: y of layer l feeds layer l+1
             launches["decode"] += zdc.last_launch_count()
+        else:
+            for l in range(L):
+                ctx.decode(x_buf, y_dec, l, l + 1)
+                launches["decode"] += zdc.last_launch_count()
     torch.cuda.synchronize()
     log("graphs captured")
     kernels_per_step = launches["prefill"] + T * launches["decode"]
@@ -411,7 +417,7 @@ def run_zdc(args):
                                        total_ms / args.steps)
     decode_layer_bytes = sum(kernels[k]["work_per_launch"] for k in
                              ("a1_decode_gemv", "a3_decode_attention", "a5_decode_gemv"))
-    fused = launches["decode"] == L  # one fused layer-step kernel per layer (decode_fused.cuh)
+    fused = launches["decode"] in (1, L)  # fused layer-step kernel(s) (decode_fused.cuh)
     if fused:
         # the decode step is L back-to-back launches of the fused layer kernel (a1+a2+a3+a5): its
         # average launch duration is measured LIVE, over the decode region of the timed step
@@ -421,18 +427,22 @@ def run_zdc(args):
         for k in unf:
             shares.pop(k)
             unf[k]["est_share_of_step"] = 0.0
-        avg_s = dec_ms[-1] / 1e3 / (L * T)
-        ach = decode_layer_bytes / avg_s / 1e9
+        per_launch = L if launches["decode"] == 1 else 1  # layers per fused launch
+        n_launch = L * T // per_launch
+        avg_s = dec_ms[-1] / 1e3 / n_launch
+        ach = decode_layer_bytes * per_launch / avg_s / 1e9
         peaks = load_peaks()
         kernels["decode_layer_fused"] = {
             "bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm"], "unit": "GB/s",
-            "frac": round(ach / peaks["hbm"], 4), "avg_us": round(avg_s * 1e6, 2), "launches_per_step": L * T,
-            "work_per_launch": decode_layer_bytes, "traffic": None, "timing": "live (timed region)",
+            "frac": round(ach / peaks["hbm"], 4), "avg_us": round(avg_s * 1e6, 2), "launches_per_step": n_launch,
+            "layers_per_launch": per_launch, "work_per_launch": decode_layer_bytes * per_launch, "traffic": None,
+            "timing": "live (timed region)",
             "est_share_of_step": round(dec_ms[-1] / (total_ms / args.steps), 4)}
         shares["decode_layer_fused"] = dec_ms[-1] / (total_ms / args.steps)
         traffic_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(traffic_path):
-            kernels["decode_layer_fused"]["traffic"] = json.load(open(traffic_path)).get("decode_layer_fused")
+            t = json.load(open(traffic_path)).get("decode_layer_fused")  # one layer-step, ncu
+            kernels["decode_layer_fused"]["traffic"] = t * per_launch if t else None
     dom = max(kernels, key=lambda k: shares[k])
     roof = dict(kernels[dom])
     roof["kernel"] = dom

@@ -209,6 +209,8 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
   s = align_up(s + static_cast<int64_t>(max_batch) * d.n_kv_heads * 4, 256);
   c->s_gbar = s;  // fused decode grid barrier, kept self-resetting between launches
   s = align_up(s + 64, 256);
+  c->s_ltab = s;  // fused decode layer table (DecLayer per layer), written at bind
+  s = align_up(s + static_cast<int64_t>(d.n_layers) * static_cast<int64_t>(sizeof(DecLayer)), 256);
   if (any_split) {  // staged K'/V' of a split layer before packing, compaction indices, new-row staging
     const int64_t kv_rows = static_cast<int64_t>(max_batch) * d.n_kv_heads * max_seq;
     c->s_ks = s;
@@ -248,6 +250,18 @@ zdc_status zdc_ctx_bind(zdc_ctx* c, void* w, void* cache, void* scratch) {
   ZDC_CUDA_TRY(cudaMemset(c->scratch, 0, c->scratch_bytes));
   ZDC_CUDA_TRY(cudaMemset(c->w, 0, c->weight_bytes));
   fused_trace_buffer();  // allocated here (if ZDC_FUSED_TRACE is set), never inside a graph capture
+  {
+    std::vector<DecLayer> tab(c->dims.n_layers);
+    for (int l = 0; l < c->dims.n_layers; ++l) {
+      const LayerInfo& L = c->layers[l];
+      tab[l].wqkv = reinterpret_cast<const uint16_t*>(c->w + L.w_qkv);
+      tab[l].wo = reinterpret_cast<const uint16_t*>(c->w + L.w_o);
+      tab[l].kc = reinterpret_cast<uint16_t*>(c->cache + L.k_off);
+      tab[l].vc = reinterpret_cast<uint16_t*>(c->cache + L.v_off);
+      tab[l].len_ptr = c->len_dev() + l;
+    }
+    ZDC_CUDA_TRY(cudaMemcpy(c->scratch + c->s_ltab, tab.data(), tab.size() * sizeof(DecLayer), cudaMemcpyHostToDevice));
+  }
   c->len.assign(c->dims.n_layers, 0);
   c->sp_layer.assign(c->dims.n_layers, 0);
   c->batch = 0;
@@ -490,41 +504,29 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
     const uint16_t* wqkv = reinterpret_cast<const uint16_t*>(c->w + L.w_qkv);
     const uint16_t* wo = reinterpret_cast<const uint16_t*>(c->w + L.w_o);
     static const bool fused_on = !(getenv("ZDC_DEC_FUSED") && atoi(getenv("ZDC_DEC_FUSED")) == 0);
-    if (fused_on && !L.split && decode_fused_supported(B, L.rk_p, c->G)) {
-      // the whole layer-step in one persistent kernel (decode_fused.cu)
+    auto fusable = [&](const LayerInfo& X) {
+      return fused_on && !X.split && decode_fused_supported(B, X.rk_p, c->G) && X.rk_p == L.rk_p &&
+             X.n_qkv == L.n_qkv && X.ko_p == L.ko_p;
+    };
+    if (fusable(L)) {
+      // the run of consecutive fusable layers [l, le): ONE persistent kernel (decode_fused.cuh)
+      int le = l + 1;
+      while (le < l1 && fusable(c->layers[le])) ++le;
       DecFusedArgs f;
-      f.wqkv = wqkv;
-      f.wo = wo;
+      f.layers = reinterpret_cast<const DecLayer*>(c->scratch + c->s_ltab) + l;
+      f.nl = le - l;
       f.x = xin;
       f.ldx = d;
       f.y = y;
       f.ldy = d;
       f.q = reinterpret_cast<uint16_t*>(c->scratch + c->s_q);
       f.ldq = L.nq;
-      f.kc = reinterpret_cast<uint16_t*>(c->cache + L.k_off);
-      f.vc = reinterpret_cast<uint16_t*>(c->cache + L.v_off);
-      f.len_ptr = len_dev;
       f.part = reinterpret_cast<float*>(c->scratch + c->s_part);
       f.lse = reinterpret_cast<float*>(c->scratch + c->s_lse);
       f.gbar = reinterpret_cast<unsigned long long*>(c->scratch + c->s_gbar);
       f.o = reinterpret_cast<uint16_t*>(c->scratch + c->s_o);
       f.counters = reinterpret_cast<int*>(c->scratch + c->s_cnt);
       f.trace = fused_trace_buffer();
-      // opt-in (ZDC_FUSED_SELF_PF=1): measured slower in round 1, the prefetch traffic delays the
-      // latency-critical input load of the consumers
-      static const int self_pf = getenv("ZDC_FUSED_SELF_PF") ? atoi(getenv("ZDC_FUSED_SELF_PF")) : 0;
-      f.self_prefetch = self_pf;
-      {
-        // the layer expected next (l + 1, wrapping to 0 for the next step) when it takes this
-        // path too; opt-in with ZDC_FUSED_L2PF=1 (measured slower in round 1: the prefetch traffic
-        // delays the grid-barrier polls on the critical path)
-        static const bool pf = getenv("ZDC_FUSED_L2PF") && atoi(getenv("ZDC_FUSED_L2PF")) != 0;
-        const LayerInfo& N = c->layers[(l + 1) % c->dims.n_layers];
-        if (pf && !N.split) {
-          f.next_wqkv = reinterpret_cast<const uint16_t*>(c->w + N.w_qkv);
-          f.next_n_qkv = N.n_qkv;
-        }
-      }
       f.B = B;
       f.d = d;
       f.n_qkv = L.n_qkv;
@@ -539,8 +541,11 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
       g_prof_class = kProfDecodeLayer;
       cudaError_t e = launch_decode_fused(f, L.rk_p, s);
       g_prof_class = kProfOther;
-      if (e == cudaSuccess) continue;
-      if (e != cudaErrorNotSupported) return fail(ZDC_ERR_CUDA, "fused decode layer %d: %s", l, cudaGetErrorString(e));
+      if (e == cudaSuccess) {
+        l = le - 1;
+        continue;
+      }
+      if (e != cudaErrorNotSupported) return fail(ZDC_ERR_CUDA, "fused decode layers [%d, %d): %s", l, le, cudaGetErrorString(e));
       cudaGetLastError();
     }
     g_prof_class = kProfGemvQkv;

@@ -41,7 +41,8 @@ struct zdc_ctx {
   int64_t s_q = 0, s_o = 0, s_lse = 0, s_part = 0;  // scratch offsets
   int64_t s_ks = 0, s_vs = 0, s_didx = 0, s_new = 0;  // token-split staging
   int64_t s_cnt = 0;                                  // decode merge counters
-  int64_t s_gbar = 0;                                 // fused decode grid barrier {count, generation}
+  int64_t s_gbar = 0;                                 // fused decode grid barrier (monotonic counter)
+  int64_t s_ltab = 0;                                 // fused decode layer table
   int ldq = 0, ldo = 0;
   uint8_t* w = nullptr;
   uint8_t* cache = nullptr;

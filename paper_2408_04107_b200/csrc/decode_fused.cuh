@@ -273,8 +273,8 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
   uint64_t* lenbar = empty + nslot;
   uint64_t* pbar = lenbar + 1;
   unsigned long long* s_base = reinterpret_cast<unsigned long long*>(pbar + 1);
-  int* s_len = reinterpret_cast<int*>(s_base + 1);
-  int* s_flag = s_len + 1;
+  int* s_flag = reinterpret_cast<int*>(s_base + 1);
+  int* s_lens = s_flag + 1;  // [nl] cache lengths at entry
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int cta = blockIdx.x, ncta = gridDim.x;
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
   __syncthreads();
   if (tid == 0) ZDC_STAMP(0);
 
-  // ---- static work split (identical in producer and consumers)
+  // ---- static work split, identical for every layer of the run (and in producer and consumers)
   const int d = a.d, ko = a.ko_p;
   const int per1 = (a.n_qkv + ncta - 1) / ncta;
   const int r1a = min(a.n_qkv, cta * per1), r1b = min(a.n_qkv, r1a + per1);
@@ -302,76 +302,59 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
   const int n3 = (r3b - r3a + rps3 - 1) / rps3;
   const int nitems = a.B * a.Nkv * a.splits;
   const int RPS = 32;  // K'/V' rows per slot: [32][RK] K' then [32][RK] V'
+  const int tl = a.nl > 1 ? 1 : 0;  // layer whose timeline the trace records
 
   if (warp == kNW) {
-    // ================= producer (one thread): every HBM byte of this CTA, in consumption order
+    // ================= producer (one thread): every HBM byte of this CTA, in consumption order,
+    // layer after layer: while the consumers finish layer l, the ring fills with layer l+1's W_QKV
     if (lane == 0) {
-      int k = 0;
       ProducerCursor pc;
-      if (a.self_prefetch) {
-        // the ring holds the first nslot rows; the rest of this CTA's phase-1 rows go to L2 now,
-        // while HBM is otherwise idle (the consumers are still waiting for the predecessor)
-        const int r_pf = r1a + nslot * rps1;
-        if (r_pf < r1b) {
-          const uint8_t* base = reinterpret_cast<const uint8_t*>(a.wqkv + static_cast<int64_t>(r_pf) * d);
-          const int64_t bytes = static_cast<int64_t>(r1b - r_pf) * d * 2;
-          for (int64_t o = 0; o < bytes; o += 32768)
-            l2_prefetch(base + o, static_cast<uint32_t>(min(static_cast<int64_t>(32768), bytes - o)));
-        }
-      }
-      // phase 1 weights: static, issued before the dependency wait
-      for (int r = r1a; r < r1b; r += rps1, ++k) {
-        const int nr = min(rps1, r1b - r);
-        const int s = pc.slot(spw, ex);
-        if (pc.reuse(spw, ex)) mbar_wait(&empty[s], pc.phase(ex) ^ 1);
-        pc.next(spw);
-        const uint32_t bytes = static_cast<uint32_t>(nr) * d * 2u;
-        mbar_arrive_expect_tx(&full[s], bytes);
-        bulk_g2s(ring + static_cast<size_t>(s) * SB, a.wqkv + static_cast<int64_t>(r) * d, bytes, &full[s]);
-      }
-      ZDC_STAMP(8);
-      // the cache length is read by a consumer after the PDL wait (the previous step of this
-      // layer may be the predecessor kernel)
-      mbar_wait(lenbar, 0);
-      const int L = *s_len, L1 = L + 1;
-      const int chunk = (L1 + a.splits - 1) / a.splits;
-      for (int it = cta; it < nitems; it += ncta) {
-        const int sp = it % a.splits, g = (it / a.splits) % a.Nkv, b = it / (a.splits * a.Nkv);
-        const int s0 = sp * chunk, e0 = min(min(L1, s0 + chunk), L);  // cached rows only
-        const int64_t row0 = (static_cast<int64_t>(b) * a.Nkv + g) * a.S_cap;
-        for (int p = s0; p < e0; p += RPS, ++k) {
-          const int np = min(RPS, e0 - p);
+      bool have_lens = false;
+      for (int li = 0; li < a.nl; ++li) {
+        const DecLayer Ly = a.layers[li];
+        for (int r = r1a; r < r1b; r += rps1) {  // phase 1 weights (static: no dependency wait)
+          const int nr = min(rps1, r1b - r);
           const int s = pc.slot(spw, ex);
           if (pc.reuse(spw, ex)) mbar_wait(&empty[s], pc.phase(ex) ^ 1);
           pc.next(spw);
-          const uint32_t bytes = static_cast<uint32_t>(np) * RK * 2u;
-          mbar_arrive_expect_tx(&full[s], 2 * bytes);
-          uint8_t* dst = ring + static_cast<size_t>(s) * SB;
-          bulk_g2s(dst, a.kc + (row0 + p) * RK, bytes, &full[s]);
-          bulk_g2s(dst + RPS * RK * 2, a.vc + (row0 + p) * RK, bytes, &full[s]);
+          const uint32_t bytes = static_cast<uint32_t>(nr) * d * 2u;
+          mbar_arrive_expect_tx(&full[s], bytes);
+          bulk_g2s(ring + static_cast<size_t>(s) * SB, Ly.wqkv + static_cast<int64_t>(r) * d, bytes, &full[s]);
         }
-      }
-      ZDC_STAMP(9);
-      // phase 3 weights
-      for (int r = r3a; r < r3b; r += rps3, ++k) {
-        const int nr = min(rps3, r3b - r);
-        const int s = pc.slot(spw, ex);
-        if (pc.reuse(spw, ex)) mbar_wait(&empty[s], pc.phase(ex) ^ 1);
-        pc.next(spw);
-        const uint32_t bytes = static_cast<uint32_t>(nr) * ko * 2u;
-        mbar_arrive_expect_tx(&full[s], bytes);
-        bulk_g2s(ring + static_cast<size_t>(s) * SB, a.wo + static_cast<int64_t>(r) * ko, bytes, &full[s]);
-      }
-      ZDC_STAMP(10);
-      // every byte of this layer is requested: pull this CTA's share of the NEXT layer's W_QKV^R
-      // rows into L2, so its phase 1 streams from L2 while this layer's critical path finishes
-      if (a.next_wqkv != nullptr) {
-        const int pn = (a.next_n_qkv + ncta - 1) / ncta;
-        const int na = min(a.next_n_qkv, cta * pn), nb = min(a.next_n_qkv, na + pn);
-        const uint8_t* base = reinterpret_cast<const uint8_t*>(a.next_wqkv + static_cast<int64_t>(na) * d);
-        const int64_t bytes = static_cast<int64_t>(nb - na) * d * 2;
-        for (int64_t o = 0; o < bytes; o += 65536)
-          l2_prefetch(base + o, static_cast<uint32_t>(min(static_cast<int64_t>(65536), bytes - o)));
+        if (li == tl) ZDC_STAMP(8);
+        if (!have_lens) {  // lengths are read by a consumer after the PDL wait
+          mbar_wait(lenbar, 0);
+          have_lens = true;
+        }
+        const int L = s_lens[li], L1 = L + 1;
+        const int chunk = (L1 + a.splits - 1) / a.splits;
+        for (int it = cta; it < nitems; it += ncta) {
+          const int sp = it % a.splits, g = (it / a.splits) % a.Nkv, b = it / (a.splits * a.Nkv);
+          const int s0 = sp * chunk, e0 = min(min(L1, s0 + chunk), L);  // cached rows only
+          const int64_t row0 = (static_cast<int64_t>(b) * a.Nkv + g) * a.S_cap;
+          for (int p = s0; p < e0; p += RPS) {
+            const int np = min(RPS, e0 - p);
+            const int s = pc.slot(spw, ex);
+            if (pc.reuse(spw, ex)) mbar_wait(&empty[s], pc.phase(ex) ^ 1);
+            pc.next(spw);
+            const uint32_t bytes = static_cast<uint32_t>(np) * RK * 2u;
+            mbar_arrive_expect_tx(&full[s], 2 * bytes);
+            uint8_t* dst = ring + static_cast<size_t>(s) * SB;
+            bulk_g2s(dst, Ly.kc + (row0 + p) * RK, bytes, &full[s]);
+            bulk_g2s(dst + RPS * RK * 2, Ly.vc + (row0 + p) * RK, bytes, &full[s]);
+          }
+        }
+        if (li == tl) ZDC_STAMP(9);
+        for (int r = r3a; r < r3b; r += rps3) {  // phase 3 weights
+          const int nr = min(rps3, r3b - r);
+          const int s = pc.slot(spw, ex);
+          if (pc.reuse(spw, ex)) mbar_wait(&empty[s], pc.phase(ex) ^ 1);
+          pc.next(spw);
+          const uint32_t bytes = static_cast<uint32_t>(nr) * ko * 2u;
+          mbar_arrive_expect_tx(&full[s], bytes);
+          bulk_g2s(ring + static_cast<size_t>(s) * SB, Ly.wo + static_cast<int64_t>(r) * ko, bytes, &full[s]);
+        }
+        if (li == tl) ZDC_STAMP(10);
       }
     }
     return;
@@ -381,191 +364,199 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
   pdl_wait();
   pdl_trigger();
   if (tid == 0) {
-    *s_len = *a.len_ptr;
+    for (int li = 0; li < a.nl; ++li) s_lens[li] = *a.layers[li].len_ptr;
     *s_base = ld_acquire_u64(a.gbar) / ncta * ncta;
     mbar_arrive(lenbar);
   }
-  {
-    const int kcx = d >> 3;
-    uint4* xs4 = reinterpret_cast<uint4*>(xs);
-    for (int i = tid; i < NB * kcx; i += kNC) {
-      const int b = i / kcx, c = i - b * kcx;
-      xs4[b * xw8 + c] = b < a.B ? *reinterpret_cast<const uint4*>(a.x + b * a.ldx + c * 8) : make_uint4(0, 0, 0, 0);
-    }
-  }
-  consumer_sync();
-  if (tid == 0) ZDC_STAMP(1);
-  const int L = *s_len, L1 = L + 1;
   ConsumerCursor cc(warp, spw, ex);
   const uint4* xs4 = reinterpret_cast<const uint4*>(xs);
-
-  // ---- phase 1: a1 + a2
-  for (int k = warp; k < n1; k += kNW) {
-    const int s = cc.slot();
-    mbar_wait(&full[s], cc.ph);
-    cc.next();
-    const int rb = r1a + k * rps1, nr = min(rps1, r1b - rb);
-    for (int r = 0; r < nr; ++r) {
-      float acc[1][NB];
-      gemv_rows<NB, 1>(ring + static_cast<size_t>(s) * SB, d, xs4, xw8, lane, acc, r);
-      const int n = rb + r;
-#pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        if (lane == b && b < a.B) {
-          const uint16_t v = f32_to_bf16_bits(acc[0][b]);
-          if (n < a.nq) {
-            a.q[b * a.ldq + n] = v;
-          } else if (n < a.nq + a.nk) {
-            const int nn = n - a.nq, g = nn / RK, c = nn - g * RK;
-            a.kc[((static_cast<int64_t>(b) * a.Nkv + g) * a.S_cap + L) * RK + c] = v;
-          } else {
-            const int nn = n - a.nq - a.nk, g = nn / RK, c = nn - g * RK;
-            a.vc[((static_cast<int64_t>(b) * a.Nkv + g) * a.S_cap + L) * RK + c] = v;
-          }
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
-  consumer_sync();
-  if (tid == 0) {
-    ZDC_STAMP(2);
-    grid_barrier(a.gbar, *s_base + ncta);
-    ZDC_STAMP(3);
-  }
-  consumer_sync();
-
-  // ---- phase 2: a3 partials
   const float scl = a.scale * kLog2eF;
-  const int chunk = (L1 + a.splits - 1) / a.splits;
-  int kb = n1;
-  for (int it = cta; it < nitems; it += ncta) {
-    const int sp = it % a.splits, g = (it / a.splits) % a.Nkv, b = it / (a.splits * a.Nkv);
-    const int s0 = sp * chunk, s1 = min(L1, s0 + chunk), e0 = min(s1, L);
-    const int ns = e0 > s0 ? (e0 - s0 + RPS - 1) / RPS : 0;
-    const bool has_new = s0 <= L && L < s1;
-    for (int i = tid; i < G * RK; i += kNC) {
-      const int gi = i / RK, c = i - gi * RK;
-      const uint16_t u = __ldcg(reinterpret_cast<const unsigned short*>(a.q) + b * a.ldq + (g * G + gi) * RK + c);
-      qf[i] = __uint_as_float(static_cast<uint32_t>(u) << 16);
-    }
-    if (has_new && warp == 0) {
-      const int64_t row = ((static_cast<int64_t>(b) * a.Nkv + g) * a.S_cap + L) * RK;
-      for (int c = lane; c < RK; c += 32) {
-        nrow[c] = __ldcg(reinterpret_cast<const unsigned short*>(a.kc) + row + c);
-        nrow[RK + c] = __ldcg(reinterpret_cast<const unsigned short*>(a.vc) + row + c);
+  unsigned long long nbar = 0;  // grid barriers passed in this launch
+  int kb = 0;                   // ring sequence number of the current phase's first slot
+
+  for (int li = 0; li < a.nl; ++li) {
+    const DecLayer Ly = a.layers[li];
+    if (tid == 0 && li == tl) ZDC_STAMP(13);
+    // ---- stage this layer's input: x for the first layer, the previous layer's y after
+    {
+      const uint16_t* xin = li == 0 ? a.x : a.y;
+      const int64_t ld = li == 0 ? a.ldx : a.ldy;
+      const int kcx = d >> 3;
+      uint4* xw4 = reinterpret_cast<uint4*>(xs);
+      for (int i = tid; i < NB * kcx; i += kNC) {
+        const int b = i / kcx, c = i - b * kcx;
+        xw4[b * xw8 + c] = b < a.B ? __ldcg(reinterpret_cast<const uint4*>(xin + b * ld) + c) : make_uint4(0, 0, 0, 0);
       }
     }
     consumer_sync();
-    float m[G], l[G], o[G][DPL];
-#pragma unroll
-    for (int gi = 0; gi < G; ++gi) {
-      m[gi] = -INFINITY;
-      l[gi] = 0.f;
-#pragma unroll
-      for (int i = 0; i < DPL; ++i) o[gi][i] = 0.f;
-    }
-    for (int t = (warp - kb % kNW + kNW) % kNW; t < ns; t += kNW) {
-      const int k = kb + t;
+    if (tid == 0 && li == tl) ZDC_STAMP(1);
+    const int L = s_lens[li], L1 = L + 1;
+
+    // ---- phase 1: a1 + a2
+    for (int t = (warp - kb % kNW + kNW) % kNW; t < n1; t += kNW) {
       const int s = cc.slot();
       mbar_wait(&full[s], cc.ph);
       cc.next();
-      const uint16_t* Ks = reinterpret_cast<const uint16_t*>(ring + static_cast<size_t>(s) * SB);
-      attn_rows<RK, G>(Ks, Ks + RPS * RK, min(RPS, e0 - (s0 + t * RPS)), qf, scl, m, l, o, lane);
+      const int rb = r1a + t * rps1, nr = min(rps1, r1b - rb);
+      for (int r = 0; r < nr; ++r) {
+        float acc[1][NB];
+        gemv_rows<NB, 1>(ring + static_cast<size_t>(s) * SB, d, xs4, xw8, lane, acc, r);
+        const int n = rb + r;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          if (lane == b && b < a.B) {
+            const uint16_t v = f32_to_bf16_bits(acc[0][b]);
+            if (n < a.nq) {
+              a.q[b * a.ldq + n] = v;
+            } else if (n < a.nq + a.nk) {
+              const int nn = n - a.nq, g = nn / RK, c = nn - g * RK;
+              Ly.kc[((static_cast<int64_t>(b) * a.Nkv + g) * a.S_cap + L) * RK + c] = v;
+            } else {
+              const int nn = n - a.nq - a.nk, g = nn / RK, c = nn - g * RK;
+              Ly.vc[((static_cast<int64_t>(b) * a.Nkv + g) * a.S_cap + L) * RK + c] = v;
+            }
+          }
+        }
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    if (has_new && warp == 0) attn_rows<RK, G>(nrow, nrow + RK, 1, qf, scl, m, l, o, lane);
-    // warp states -> shared memory, then the CTA merges them into this item's partial
-    float* ws = wst + warp * G * (RK + 2);
-#pragma unroll
-    for (int gi = 0; gi < G; ++gi) {
-#pragma unroll
-      for (int i = 0; i < DPL; ++i) {
-        const int c = RK >= 32 ? lane * DPL + i : lane;
-        if (c < RK) ws[gi * (RK + 2) + c] = o[gi][i];
-      }
-      if (lane == 0) {
-        ws[gi * (RK + 2) + RK] = m[gi];
-        ws[gi * (RK + 2) + RK + 1] = l[gi];
-      }
-    }
+    kb += n1;
     consumer_sync();
-    if (tid == 0) ZDC_STAMP(11);
-    for (int i = tid; i < G * RK; i += kNC) {
-      const int gi = i / RK, c = i - gi * RK;
-      float M = -INFINITY;
-#pragma unroll
-      for (int w = 0; w < kNW; ++w) M = fmaxf(M, wst[(w * G + gi) * (RK + 2) + RK]);
-      float O = 0.f, Ls = 0.f;
-      if (M != -INFINITY) {
-#pragma unroll
-        for (int w = 0; w < kNW; ++w) {
-          const float* e = wst + (w * G + gi) * (RK + 2);
-          const float f = exp2f(e[RK] - M);  // 0 for warps without rows (m = -inf)
-          O = fmaf(e[c], f, O);
-          Ls = fmaf(e[RK + 1], f, Ls);
-        }
-      }
-      float* dst = a.part + ((static_cast<int64_t>(b) * a.Nh + g * G + gi) * a.splits + sp) * (RK + 2);
-      dst[c] = O;
-      if (c == 0) {
-        dst[RK] = M;
-        dst[RK + 1] = Ls;
-      }
+    if (tid == 0) {
+      if (li == tl) ZDC_STAMP(2);
+      grid_barrier(a.gbar, *s_base + (++nbar) * ncta);
+      if (li == tl) ZDC_STAMP(3);
     }
-    // without staging (large partial sets) the last CTA to finish a chunk of (b, g) merges them:
-    // O' = sum_s o_s 2^(m_s - M) / sum_s l_s 2^(m_s - M), LSE = (M + log2 L) ln 2
+    if (tid != 0) ++nbar;
     consumer_sync();
-    if (!a.stage_part && tid == 0) {
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      *s_flag = atomic_add_acq_rel(a.counters + b * a.Nkv + g, 1) == a.splits - 1;
-    }
-    consumer_sync();
-    if (!a.stage_part && *s_flag) {
+
+    // ---- phase 2: a3 partials
+    const int chunk = (L1 + a.splits - 1) / a.splits;
+    for (int it = cta; it < nitems; it += ncta) {
+      const int sp = it % a.splits, g = (it / a.splits) % a.Nkv, b = it / (a.splits * a.Nkv);
+      const int s0 = sp * chunk, s1 = min(L1, s0 + chunk), e0 = min(s1, L);
+      const int ns = e0 > s0 ? (e0 - s0 + RPS - 1) / RPS : 0;
+      const bool has_new = s0 <= L && L < s1;
       for (int i = tid; i < G * RK; i += kNC) {
         const int gi = i / RK, c = i - gi * RK;
-        const float* hp = a.part + (static_cast<int64_t>(b) * a.Nh + g * G + gi) * a.splits * (RK + 2);
-        float M = -INFINITY;
-        for (int s2 = 0; s2 < a.splits; ++s2) M = fmaxf(M, __ldcg(hp + s2 * (RK + 2) + RK));
-        float O = 0.f, Ls = 0.f;
-        for (int s2 = 0; s2 < a.splits; ++s2) {
-          const float ms = __ldcg(hp + s2 * (RK + 2) + RK);
-          const float f = ms == -INFINITY ? 0.f : exp2f(ms - M);
-          O = fmaf(f, __ldcg(hp + s2 * (RK + 2) + c), O);
-          Ls = fmaf(f, __ldcg(hp + s2 * (RK + 2) + RK + 1), Ls);
-        }
-        a.o[b * ko + (g * G + gi) * RK + c] = f32_to_bf16_bits(O / Ls);
-        if (c == 0 && a.lse) a.lse[b * a.Nh + g * G + gi] = (M + log2f(Ls)) / kLog2eF;
+        const uint16_t u = __ldcg(reinterpret_cast<const unsigned short*>(a.q) + b * a.ldq + (g * G + gi) * RK + c);
+        qf[i] = __uint_as_float(static_cast<uint32_t>(u) << 16);
       }
-      if (tid == 0) a.counters[b * a.Nkv + g] = 0;
+      if (has_new && warp == 0) {
+        const int64_t row = ((static_cast<int64_t>(b) * a.Nkv + g) * a.S_cap + L) * RK;
+        for (int c = lane; c < RK; c += 32) {
+          nrow[c] = __ldcg(reinterpret_cast<const unsigned short*>(Ly.kc) + row + c);
+          nrow[RK + c] = __ldcg(reinterpret_cast<const unsigned short*>(Ly.vc) + row + c);
+        }
+      }
+      consumer_sync();
+      float m[G], l[G], o[G][DPL];
+#pragma unroll
+      for (int gi = 0; gi < G; ++gi) {
+        m[gi] = -INFINITY;
+        l[gi] = 0.f;
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) o[gi][i] = 0.f;
+      }
+      for (int t = (warp - kb % kNW + kNW) % kNW; t < ns; t += kNW) {
+        const int s = cc.slot();
+        mbar_wait(&full[s], cc.ph);
+        cc.next();
+        const uint16_t* Ks = reinterpret_cast<const uint16_t*>(ring + static_cast<size_t>(s) * SB);
+        attn_rows<RK, G>(Ks, Ks + RPS * RK, min(RPS, e0 - (s0 + t * RPS)), qf, scl, m, l, o, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+      if (has_new && warp == 0) attn_rows<RK, G>(nrow, nrow + RK, 1, qf, scl, m, l, o, lane);
+      // warp states -> shared memory, then the CTA merges them into this item's partial
+      float* ws = wst + warp * G * (RK + 2);
+#pragma unroll
+      for (int gi = 0; gi < G; ++gi) {
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) {
+          const int c = RK >= 32 ? lane * DPL + i : lane;
+          if (c < RK) ws[gi * (RK + 2) + c] = o[gi][i];
+        }
+        if (lane == 0) {
+          ws[gi * (RK + 2) + RK] = m[gi];
+          ws[gi * (RK + 2) + RK + 1] = l[gi];
+        }
+      }
+      consumer_sync();
+      if (tid == 0 && li == tl) ZDC_STAMP(11);
+      for (int i = tid; i < G * RK; i += kNC) {
+        const int gi = i / RK, c = i - gi * RK;
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kNW; ++w) M = fmaxf(M, wst[(w * G + gi) * (RK + 2) + RK]);
+        float O = 0.f, Ls = 0.f;
+        if (M != -INFINITY) {
+#pragma unroll
+          for (int w = 0; w < kNW; ++w) {
+            const float* e = wst + (w * G + gi) * (RK + 2);
+            const float f = exp2f(e[RK] - M);  // 0 for warps without rows (m = -inf)
+            O = fmaf(e[c], f, O);
+            Ls = fmaf(e[RK + 1], f, Ls);
+          }
+        }
+        float* dst = a.part + ((static_cast<int64_t>(b) * a.Nh + g * G + gi) * a.splits + sp) * (RK + 2);
+        dst[c] = O;
+        if (c == 0) {
+          dst[RK] = M;
+          dst[RK + 1] = Ls;
+        }
+      }
+      // without staging (large partial sets) the last CTA to finish a chunk of (b, g) merges them:
+      // O' = sum_s o_s 2^(m_s - M) / sum_s l_s 2^(m_s - M), LSE = (M + log2 L) ln 2
+      consumer_sync();
+      if (!a.stage_part && tid == 0) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        *s_flag = atomic_add_acq_rel(a.counters + b * a.Nkv + g, 1) == a.splits - 1;
+      }
+      consumer_sync();
+      if (!a.stage_part && *s_flag) {
+        for (int i = tid; i < G * RK; i += kNC) {
+          const int gi = i / RK, c = i - gi * RK;
+          const float* hp = a.part + (static_cast<int64_t>(b) * a.Nh + g * G + gi) * a.splits * (RK + 2);
+          float M = -INFINITY;
+          for (int s2 = 0; s2 < a.splits; ++s2) M = fmaxf(M, __ldcg(hp + s2 * (RK + 2) + RK));
+          float O = 0.f, Ls = 0.f;
+          for (int s2 = 0; s2 < a.splits; ++s2) {
+            const float ms = __ldcg(hp + s2 * (RK + 2) + RK);
+            const float f = ms == -INFINITY ? 0.f : exp2f(ms - M);
+            O = fmaf(f, __ldcg(hp + s2 * (RK + 2) + c), O);
+            Ls = fmaf(f, __ldcg(hp + s2 * (RK + 2) + RK + 1), Ls);
+          }
+          a.o[b * ko + (g * G + gi) * RK + c] = f32_to_bf16_bits(O / Ls);
+          if (c == 0 && a.lse) a.lse[b * a.Nh + g * G + gi] = (M + log2f(Ls)) / kLog2eF;
+        }
+        if (tid == 0) a.counters[b * a.Nkv + g] = 0;
+      }
+      consumer_sync();
+      kb += ns;
     }
     consumer_sync();
-    kb += ns;
-  }
-  consumer_sync();
-  if (tid == 0) {
-    ZDC_STAMP(4);
-    grid_barrier(a.gbar, *s_base + 2 * static_cast<unsigned long long>(ncta));
-    ZDC_STAMP(5);
-  }
-  consumer_sync();
-  if (cta == 0 && tid == 0) *a.len_ptr = L1;  // every reader of the length has passed barrier 1
-
-  if (tid == 0) ZDC_STAMP(14);
-  if (a.stage_part) {
-    // ---- every CTA merges all heads from ONE bulk copy of the partials (one round trip
-    // instead of the atomic + merge + reload chain): the same LSE merge as above
     if (tid == 0) {
-      asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> async-proxy reads
-      mbar_arrive_expect_tx(pbar, static_cast<uint32_t>(a.pst_bytes));
-      bulk_g2s(pst, a.part, static_cast<uint32_t>(a.pst_bytes), pbar);
+      if (li == tl) ZDC_STAMP(4);
+      grid_barrier(a.gbar, *s_base + (++nbar) * ncta);
+      if (li == tl) ZDC_STAMP(5);
     }
-    mbar_wait(pbar, 0);
-    if (tid == 0) ZDC_STAMP(12);
-    const int S2 = a.splits;
-    {
+    if (tid != 0) ++nbar;
+    consumer_sync();
+    if (cta == 0 && tid == 0) *Ly.len_ptr = L1;  // every reader of this length has passed barrier 1
+
+    if (a.stage_part) {
+      // ---- every CTA merges all heads from ONE bulk copy of the partials (one round trip
+      // instead of the atomic + merge + reload chain): the same LSE merge as above
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> async-proxy reads
+        mbar_arrive_expect_tx(pbar, static_cast<uint32_t>(a.pst_bytes));
+        bulk_g2s(pst, a.part, static_cast<uint32_t>(a.pst_bytes), pbar);
+      }
+      mbar_wait(pbar, static_cast<uint32_t>(li & 1));
+      if (tid == 0 && li == tl) ZDC_STAMP(12);
+      const int S2 = a.splits;
       // O' chunks of 8 columns (one head never straddles a chunk: RK % 16 == 0); each thread
       // merges its head's splits in one pass: M = max m_s, L = sum 2^(m_s-M) l_s, O' = sum 2^(m_s-M) o_s / L
       const int ko8 = ko >> 3, hk8 = (a.Nh * RK) >> 3;
@@ -576,7 +567,7 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
 #pragma unroll
         for (int e = 0; e < 8; ++e) v[e] = 0.f;
         if (b < a.B && c8 < hk8) {
-          const int h = (c8 * 8) / RK, cc = c8 * 8 - h * RK;
+          const int h = (c8 * 8) / RK, cc8 = c8 * 8 - h * RK;
           const int bh = b * a.Nh + h;
           const float* hp = pst + bh * S2 * (RK + 2);
           float M = -INFINITY;
@@ -589,7 +580,7 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
             Ls = fmaf(f, e2[RK + 1], Ls);
 #pragma unroll
             for (int e = 0; e < 8; e += 2) {
-              const float2 o2 = *reinterpret_cast<const float2*>(e2 + cc + e);  // 8-byte aligned
+              const float2 o2 = *reinterpret_cast<const float2*>(e2 + cc8 + e);  // 8-byte aligned
               v[e] = fmaf(f, o2.x, v[e]);
               v[e + 1] = fmaf(f, o2.y, v[e + 1]);
             }
@@ -597,52 +588,59 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
           const float inv = 1.f / Ls;
 #pragma unroll
           for (int e = 0; e < 8; ++e) v[e] *= inv;
-          if (cc == 0 && cta == 0 && a.lse) a.lse[bh] = (M + log2f(Ls)) / kLog2eF;
+          if (cc8 == 0 && cta == 0 && a.lse) a.lse[bh] = (M + log2f(Ls)) / kLog2eF;
         }
         xo[b * xw8 + c8] = make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
                                       pack_bf16x2(v[6], v[7]));
       }
+    } else {
+      // ---- O' (merged by the last CTA of each (b, g), published by barrier 2) -> shared memory
+      const int ko8 = ko >> 3, hk8 = (a.Nh * RK) >> 3;
+      uint4* xo = reinterpret_cast<uint4*>(xs);
+      for (int i = tid; i < NB * ko8; i += kNC) {
+        const int b = i / ko8, c = i - b * ko8;
+        xo[b * xw8 + c] = b < a.B && c < hk8 ? __ldcg(reinterpret_cast<const uint4*>(a.o + b * ko) + c)
+                                             : make_uint4(0, 0, 0, 0);
+      }
     }
-  } else {
-    // ---- O' (merged by the last CTA of each (b, g), published by barrier 2) -> shared memory
-    const int ko8 = ko >> 3, hk8 = (a.Nh * RK) >> 3;
-    uint4* xo = reinterpret_cast<uint4*>(xs);
-    for (int i = tid; i < NB * ko8; i += kNC) {
-      const int b = i / ko8, c = i - b * ko8;
-      xo[b * xw8 + c] = b < a.B && c < hk8 ? __ldcg(reinterpret_cast<const uint4*>(a.o + b * ko) + c)
-                                           : make_uint4(0, 0, 0, 0);
-    }
-  }
-  consumer_sync();
-  if (tid == 0) ZDC_STAMP(6);
+    consumer_sync();
+    if (tid == 0 && li == tl) ZDC_STAMP(6);
 
-  // ---- phase 3: a5
-  for (int t = (warp - kb % kNW + kNW) % kNW; t < n3; t += kNW) {
-    const int k = kb + t;
-    const int s = cc.slot();
-    mbar_wait(&full[s], cc.ph);
-    cc.next();
-    const int rb = r3a + t * rps3, nr = min(rps3, r3b - rb);
-    int r = 0;
-    for (; r + 2 <= nr; r += 2) {  // row pairs: two independent dot products per lane
-      float acc[2][NB];
-      gemv_rows<NB, 2>(ring + static_cast<size_t>(s) * SB, ko, xs4, xw8, lane, acc, r);
+    // ---- phase 3: a5
+    for (int t = (warp - kb % kNW + kNW) % kNW; t < n3; t += kNW) {
+      const int s = cc.slot();
+      mbar_wait(&full[s], cc.ph);
+      cc.next();
+      const int rb = r3a + t * rps3, nr = min(rps3, r3b - rb);
+      int r = 0;
+      for (; r + 2 <= nr; r += 2) {  // row pairs: two independent dot products per lane
+        float acc[2][NB];
+        gemv_rows<NB, 2>(ring + static_cast<size_t>(s) * SB, ko, xs4, xw8, lane, acc, r);
 #pragma unroll
-      for (int b = 0; b < NB; ++b)
-        if (lane == b && b < a.B) {
-          a.y[b * a.ldy + rb + r] = f32_to_bf16_bits(acc[0][b]);
-          a.y[b * a.ldy + rb + r + 1] = f32_to_bf16_bits(acc[1][b]);
-        }
-    }
-    if (r < nr) {
-      float acc[1][NB];
-      gemv_rows<NB, 1>(ring + static_cast<size_t>(s) * SB, ko, xs4, xw8, lane, acc, r);
+        for (int b = 0; b < NB; ++b)
+          if (lane == b && b < a.B) {
+            a.y[b * a.ldy + rb + r] = f32_to_bf16_bits(acc[0][b]);
+            a.y[b * a.ldy + rb + r + 1] = f32_to_bf16_bits(acc[1][b]);
+          }
+      }
+      if (r < nr) {
+        float acc[1][NB];
+        gemv_rows<NB, 1>(ring + static_cast<size_t>(s) * SB, ko, xs4, xw8, lane, acc, r);
 #pragma unroll
-      for (int b = 0; b < NB; ++b)
-        if (lane == b && b < a.B) a.y[b * a.ldy + rb + r] = f32_to_bf16_bits(acc[0][b]);
+        for (int b = 0; b < NB; ++b)
+          if (lane == b && b < a.B) a.y[b * a.ldy + rb + r] = f32_to_bf16_bits(acc[0][b]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    kb += n3;
+    if (li + 1 < a.nl) {
+      // y of this layer is the next layer's input
+      consumer_sync();
+      if (tid == 0) grid_barrier(a.gbar, *s_base + (++nbar) * ncta);
+      if (tid != 0) ++nbar;
+      consumer_sync();
+    }
   }
   if (a.trace) {
     consumer_sync();
@@ -660,7 +658,8 @@ inline cudaError_t launch_fused_t(DecFusedArgs a, cudaStream_t stream) {
   a.slot_bytes = slot;
   a.xw = std::max(a.d, a.ko_p);
   constexpr size_t kSmemMax = 227 * 1024;
-  const size_t fixed = static_cast<size_t>(NB) * a.xw * 2 + G * RK * 4 + kNW * G * (RK + 2) * 4 + 2 * RK * 2 + 48;
+  const size_t fixed = static_cast<size_t>(NB) * a.xw * 2 + G * RK * 4 + kNW * G * (RK + 2) * 4 + 2 * RK * 2 + 48 +
+                       static_cast<size_t>(a.nl) * 4;
   // the partials of every head staged by one bulk copy after barrier 2 when they fit (<= 48 KB)
   const int64_t pbytes = (static_cast<int64_t>(a.B) * a.Nh * a.splits * (RK + 2) * 4 + 15) / 16 * 16;
   const size_t per_slot = static_cast<size_t>(slot) + 16;  // slot + its two mbarriers

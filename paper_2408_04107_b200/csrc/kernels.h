@@ -110,28 +110,29 @@ cudaError_t launch_decode2_partial(const DecodeAttnArgs& a, int width, const uin
 int decode2_splits(int B, int Nkv, int len, int width, int G);
 int decode_splits(int B, int Nkv, int len);
 
-// ---- the fused decode layer-step (decode_fused.cu): a1 + a2 + a3 + a5 in one persistent
-// kernel for B <= 8 on uniform-rank layers (width RK = r_k = r_v padded)
+// ---- the fused decode layer-step (decode_fused.cuh): a1 + a2 + a3 + a5 of a run of consecutive
+// layers in one persistent kernel, for B <= 8 on uniform-rank layers (width RK = r_k = r_v padded)
+struct DecLayer {                  // per-layer pointers (device-resident table, written at bind)
+  const uint16_t* wqkv;            // [n_qkv][d]
+  const uint16_t* wo;              // [d][ko_p]
+  uint16_t* kc;                    // K'/V' cache: row (b, g, p) at ((b*Nkv+g)*S_cap + p)*RK
+  uint16_t* vc;
+  int* len_ptr;                    // cached rows before this step; advanced by the kernel
+};
 struct DecFusedArgs {
-  const uint16_t* wqkv = nullptr;  // [n_qkv][d]
-  const uint16_t* wo = nullptr;    // [d][ko_p]
-  const uint16_t* x = nullptr;     // [B][ldx]
+  const DecLayer* layers = nullptr;  // [nl] layers of the run, chained: y of layer i feeds layer i+1
+  int nl = 1;
+  const uint16_t* x = nullptr;     // [B][ldx] input of the first layer
   int64_t ldx = 0;
-  uint16_t* y = nullptr;           // [B][ldy]
+  uint16_t* y = nullptr;           // [B][ldy] output of every layer (the last one is the result)
   int64_t ldy = 0;
   uint16_t* q = nullptr;           // Q' staging [B][ldq]
   int64_t ldq = 0;
-  uint16_t* kc = nullptr;          // K'/V' cache: row (b, g, p) at ((b*Nkv+g)*S_cap + p)*RK
-  uint16_t* vc = nullptr;
-  int* len_ptr = nullptr;          // cached rows before this step; advanced by the kernel
   float* part = nullptr;           // [B][Nh][splits][RK+2]
   float* lse = nullptr;            // [B][Nh]
   uint16_t* o = nullptr;           // O' [B][ko_p] (bf16), written by the last CTA of each (b, g)
   int* counters = nullptr;         // [B][Nkv] arrival counters, zero between launches
   unsigned long long* gbar = nullptr;  // grid barrier arrival counter (monotonic), zero-initialised
-  const uint16_t* next_wqkv = nullptr;  // optional: W_QKV^R of the layer expected next (L2 prefetch)
-  int next_n_qkv = 0;
-  int self_prefetch = 0;                 // L2-prefetch this CTA's phase-1 rows beyond the ring at start
   unsigned long long* trace = nullptr;  // optional [ncta][16] globaltimer stamps (ZDC_FUSED_TRACE)
   int B = 0, d = 0, n_qkv = 0, nq = 0, nk = 0, Nh = 0, Nkv = 0, S_cap = 0, splits = 1, ko_p = 0;
   float scale = 0.f;

@@ -15,9 +15,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2408_04107_b200 as zdc  # noqa: E402
 import zdc_synth as Z  # noqa: E402
 
-NAMES = {0: "start", 1: "x staged", 2: "phase1 done", 3: "barrier1 out", 4: "phase2 done", 5: "barrier2 out",
+NAMES = {0: "kernel start", 13: "layer start", 1: "x staged", 2: "phase1 done", 3: "barrier1 out", 4: "phase2 done", 5: "barrier2 out",
          6: "merge done", 7: "end", 8: "prod: ph1 issued", 9: "prod: ph2 issued", 10: "prod: all issued",
-         11: "ph2 rows done", 14: "len updated", 12: "partials staged"}
+         11: "ph2 rows done", 12: "partials staged", 13: "layer start"}
 
 
 def main():
@@ -26,6 +26,7 @@ def main():
     p.add_argument("--ctx", type=int, default=2048)
     p.add_argument("--batch", type=int, default=1)
     p.add_argument("--steps", type=int, default=8)
+    p.add_argument("--chain", action="store_true", help="one chained zdc_decode call per step")
     args = p.parse_args()
     dev = torch.device("cuda", 0)
     base = Z.dims_of(2)
@@ -48,6 +49,9 @@ def main():
         xb = torch.randn(B, d, device=dev, generator=g).to(torch.bfloat16)
         yb = torch.empty_like(xb)
         for _ in range(args.steps):
+            if args.chain:
+                ctx.decode(xb, yb, 0, L)
+                continue
             for l in range(L):
                 ctx.decode(xb, yb, l, l + 1)
     s.synchronize()
