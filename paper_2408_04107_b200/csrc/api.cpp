@@ -549,7 +549,7 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
       cudaGetLastError();
     }
     g_prof_class = kProfGemvQkv;
-    if (B <= 8)
+    if (gemv_supported(B, d))
       ZDC_CUDA_TRY(launch_gemv(wqkv, xin, d, B, L.n_qkv, d, e1, s));
     else
       ZDC_CUDA_TRY(launch_gemm(xin, d, wqkv, d, B, L.n_qkv, d, e1, s));
@@ -638,7 +638,7 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
     e5.ldd = d;
     e5.len_inc = len_dev;
     g_prof_class = kProfGemvO;
-    if (B <= 8)
+    if (gemv_supported(B, L.ko_p))
       ZDC_CUDA_TRY(launch_gemv(wo, a.o, L.ko_p, B, d, L.ko_p, e5, s));
     else
       ZDC_CUDA_TRY(launch_gemm(a.o, L.ko_p, wo, L.ko_p, B, d, L.ko_p, e5, s));

@@ -228,6 +228,12 @@ static cudaError_t launch_gemv_nb(const uint16_t* W, const uint16_t* x, int64_t 
   return e;
 }
 
+bool gemv_supported(int B, int K) {
+  // at least one K-row slot per consumer warp plus the B input rows must fit in shared memory
+  return B >= 1 && B <= 8 && K % 8 == 0 &&
+         static_cast<size_t>(8) * K * 2 + static_cast<size_t>(B) * K * 2 + 16 * 8 + 16 <= 227 * 1024;
+}
+
 cudaError_t launch_gemv(const uint16_t* W, const uint16_t* x, int64_t ldx, int B, int N, int K, const Epilogue& epi,
                         cudaStream_t stream) {
   if (K % 8 != 0) return cudaErrorInvalidValue;

@@ -44,6 +44,7 @@ cudaError_t launch_gemm(const uint16_t* A, int64_t lda, const uint16_t* B, int64
                         const Epilogue& epi, cudaStream_t stream);
 
 // ---- decode: skinny projection (B <= 8 rows), weights streamed once from HBM
+bool gemv_supported(int B, int K);  // else the tcgen05 GEMM takes the projection
 cudaError_t launch_gemv(const uint16_t* W, const uint16_t* x, int64_t ldx, int B, int N, int K,
                         const Epilogue& epi, cudaStream_t stream);
 
