@@ -54,6 +54,10 @@ def parse():
     p.add_argument("--layers", type=int, default=32)
     p.add_argument("--decode-calls", default="layer", choices=["layer", "chain"],
                    help="decode step as 32 per-layer zdc_decode calls (same x per layer) or one chained call")
+    p.add_argument("--sp-seq", type=int, default=32768, help="SP prefill prompt length (c5), run when N > 1")
+    p.add_argument("--sp-layers", type=int, default=32)
+    p.add_argument("--sp", action="store_true", help="also run the SP prefill at N = 1 (P = 1, no exchange)")
+    p.add_argument("--no-sp", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--profile-only", action="store_true", help="one eager step (for ncu), no JSON")
@@ -269,6 +273,74 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+# ------------------------------------------------------------------------------------ SP (a6)
+def sp_bench(args, zdc, torch, dist, rank, world, dev, stream):
+    """Sequence-parallel prefill (configs[4], c5): the c2 layer stack over a S_total-token prompt
+    sharded zigzag over the `world` ranks, compressed K'/V' all-gathered in place per layer with
+    NCCL (zdc_sp_prefill).  Reports the SP prefill tok/s (S_total / max-over-ranks time), and the
+    exchange GB/s per GPU = bytes received per layer / time of the all-gather alone (CUDA events
+    around the NCCL call on the launch stream, nothing concurrent: NCCL's bus bandwidth)."""
+    import zdc_synth as Z
+    S_tot, Lsp, r = args.sp_seq, args.sp_layers, args.rank
+    base = Z.dims_of(5)
+    dims = Z.Dims(Lsp, base.d_model, base.n_heads, base.n_kv_heads, base.d_head)
+    d, nh, nkv, dh = dims.d_model, dims.n_heads, dims.n_kv_heads, dims.d_head
+    ctx = zdc.Context(dims, Z.plan_uniform(Lsp, r), 1, S_tot)
+    g = torch.Generator(device=dev).manual_seed(4321)
+    sc = 1.0 / math.sqrt(d)
+    for l in range(Lsp):
+        w = [torch.randn(d, nh * dh, device=dev, generator=g) * sc, torch.randn(d, nkv * dh, device=dev, generator=g) * sc,
+             torch.randn(d, nkv * dh, device=dev, generator=g) * sc, torch.randn(nh * dh, d, device=dev, generator=g) * sc]
+        ctx.load_folded_device(l, *[t.to(torch.bfloat16).contiguous() for t in w])
+        del w
+    uid = [zdc.comm_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(uid, src=0)
+    ctx.comm_init(uid[0], rank, world)
+    n_local = S_tot // world
+    x = torch.randn(1, n_local, d, device=dev, generator=g).to(torch.bfloat16)
+    y = torch.empty_like(x)
+    for _ in range(2):  # warm-up (NCCL connection set-up, kernel attributes)
+        ctx.reset()
+        ctx.sp_prefill(x, y, S_tot, layout=1, stream=stream)
+    torch.cuda.synchronize()
+    reps = max(1, args.steps)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    ms = 0.0
+    for _ in range(reps):
+        ctx.reset()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        ctx.sp_prefill(x, y, S_tot, layout=1, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms += e0.elapsed_time(e1)
+    ms /= reps
+    ctx.reset()
+    st = ctx.sp_prefill(x, y, S_tot, layout=1, stats=True, stream=stream)
+    torch.cuda.synchronize()
+    tt = torch.tensor([ms, st["exchange_ms"], -st["exchange_ms"]], device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms, ex_max, ex_min = float(tt[0]), float(tt[1]), -float(tt[2])
+    per_layer_recv = st["bytes_recv"] / Lsp
+    ctx.close()
+    out = {"workload": "c5_sp_llama2_7b", "S_total": S_tot, "layers": Lsp, "P": world, "layout": "zigzag",
+           "rank": r, "ms": ms, "sp_prefill_tok_s": S_tot / (ms / 1e3),
+           "bytes_recv_per_gpu_per_layer": per_layer_recv,
+           "bytes_recv_uncompressed_per_gpu_per_layer": st["bytes_recv_uncompressed"] / Lsp,
+           "compression": (st["bytes_recv"] / st["bytes_recv_uncompressed"]) if st["bytes_recv_uncompressed"] else None,
+           "exchange_ms_per_layer_max": ex_max / Lsp, "exchange_fraction_of_prefill": ex_max / st["total_ms"]
+           if st["total_ms"] else None}
+    if world > 1 and ex_max > 0:
+        out["exchange_GBps_per_gpu"] = st["bytes_recv"] / (ex_max / 1e3) / 1e9  # slowest rank
+        out["exchange_GBps_per_gpu_best"] = st["bytes_recv"] / (ex_min / 1e3) / 1e9
+        out["exchange_frac_of_nvlink_900"] = out["exchange_GBps_per_gpu"] / 900.0
+    return out
+
+
 # ------------------------------------------------------------------------------------ zdc arm
 def run_zdc(args):
     import torch
@@ -476,6 +548,17 @@ def run_zdc(args):
                "h2d_bytes_per_step": (B * S * d + T * B * d) * bpe,
                "d2h_bytes_per_step": (B * S * d + T * B * d) * bpe}
 
+    # ---- SP prefill with the compressed K'/V' all-gather (a6): N > 1 (or --sp at N = 1)
+    sp = None
+    if (world > 1 or args.sp) and not args.no_sp:
+        log("SP prefill (c5) over %d rank(s)" % world)
+        try:
+            sp = sp_bench(args, zdc, torch, dist, rank, world, dev, stream)
+        except Exception as e:  # reported, never hides the main line
+            sp = {"error": "%s: %s" % (type(e).__name__, e)}
+    elif world == 1:
+        sp = {"note": "the K'/V' exchange needs N > 1: bench.py --gpus N under torchrun (or --sp for P = 1)"}
+
     # ---- CPU baseline (oracle as it stands), rank 0 at N=1 only
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -508,7 +591,7 @@ def run_zdc(args):
                 "note": "whole decode layer-step inside the graph-replayed step: algorithmic bytes (packed "
                         "weights + K'/V' at the average context + x/y) / measured time per layer-step"},
             "clocks": clocks, "gpu_launches": kernels_per_step * args.steps,
-            "e2e": e2e, "cpu_baseline": cpu,
+            "e2e": e2e, "cpu_baseline": cpu, "sp": sp,
         }
         print(json.dumps(out), flush=True)
     ctx.close()

@@ -107,3 +107,32 @@ def test_sp_prefill_equals_single_gpu_rows(world, layout):
         # r / d_head = 32 / 64 of the uncompressed K/V bytes
         assert stats["bytes_recv_uncompressed"] == 2 * O.sp_bytes_received(world, B, S, 2, 64, 64)
     assert sorted(covered) == list(range(S))
+
+
+def test_sp_prefill_nccl_world1():
+    """The NCCL transport itself (libnccl resolved at runtime, ncclCommInitRank from a unique id):
+    with one rank the communicator is real but the exchange is empty, and zdc_sp_prefill must
+    equal zdc_prefill bit for bit; the stats report zero exchanged bytes."""
+    import paper_2408_04107_b200 as zdc
+    import zdc_synth as Z
+    from zdc_testlib import fold_stack, from_dev, to_dev_bf16
+    dims = Z.Dims(2, 256, 4, 2, 64)
+    plan = Z.plan_uniform(2, 32)
+    _, folded = fold_stack(dims, 1, n_calib=256)
+    S = 256
+    x = to_dev_bf16(Z.prompt(dims, 1, 1, S, seed=43))
+    outs = []
+    for sp in (False, True):
+        ctx = zdc.Context(dims, plan, 1, S)
+        for l, f in enumerate(folded):
+            ctx.load_folded(l, f["wq_f"], f["wk_f"], f["wv_f"], f["wo_f"])
+        y = torch.empty_like(x)
+        if sp:
+            ctx.comm_init(zdc.comm_unique_id(), 0, 1)
+            st = ctx.sp_prefill(x, y, S, layout=1, stats=True)
+            assert st["bytes_recv"] == 0 and st["bytes_recv_uncompressed"] == 0
+        else:
+            ctx.prefill(x, y)
+        torch.cuda.synchronize()
+        outs.append(from_dev(y))
+    assert np.array_equal(outs[0], outs[1])
