@@ -681,9 +681,12 @@ static cudaError_t launch_attn_t(const PrefillAttnArgs& a, cudaStream_t stream) 
 
 // v3 (attn_prefill3.cu) is the default; ZDC_ATTN_V1=1 / ZDC_ATTN_V2=1 select the older kernels
 static const bool g_attn_v3 = getenv("ZDC_ATTN_V1") == nullptr && getenv("ZDC_ATTN_V2") == nullptr;
+// v4 (attn_prefill4.cu, two query tiles per CTA, r <= 96) is the default; ZDC_ATTN_V3 selects v3
+static const bool g_attn_v4 = g_attn_v3 && getenv("ZDC_ATTN_V3") == nullptr;
 
 cudaError_t launch_prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream) {
   if (a.rk != a.rv) return cudaErrorInvalidValue;
+  if (g_attn_v4 && prefill_attention_v4_supported(a.rk)) return launch_prefill_attention_v4(a, stream);
   if (g_attn_v3) return launch_prefill_attention_v3(a, stream);
   switch (a.rk) {
     case 16: return launch_attn_t<16>(a, stream);

@@ -72,6 +72,8 @@ struct PrefillAttnArgs {
 };
 cudaError_t launch_prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream);
 cudaError_t launch_prefill_attention_v3(const PrefillAttnArgs& a, cudaStream_t stream);
+cudaError_t launch_prefill_attention_v4(const PrefillAttnArgs& a, cudaStream_t stream);
+bool prefill_attention_v4_supported(int rk);
 
 // ---- a3 decode attention: split-K over the context (one or two pools) + LSE-merge combine
 struct DecodeAttnArgs {
