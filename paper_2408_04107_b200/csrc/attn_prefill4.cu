@@ -1,8 +1,10 @@
 // attn_prefill4.cu — a3 prefill attention, v4 (default for head dims r <= 96): the math and
 // rounding points of v1/v3 (Eqs. 2-3, scale 1/sqrt(d_h), LSE out), re-pipelined so the
 // tensor core and the exp units stay busy at the same time:
-//   * each CTA owns TWO consecutive 128-row query tiles of one head ("a" and "b") and streams the
-//     K'/V' tiles once for both (tile a needs a prefix of tile b's causal key range);
+//   * a work item is TWO consecutive 128-row query tiles of one head ("a" and "b"); their K'/V'
+//     tiles stream once for both (tile a needs a prefix of tile b's causal key range);
+//   * persistent CTAs (one per SM) take the items longest-first in a snake order, so the
+//     triangular causal work is balanced over the SMs instead of leaving a ragged last wave;
 //   * S_a, S_b, O_a, O_b live in TMEM; the MMA warp interleaves S_a(j+1), PV_a(j), S_b(j+1),
 //     PV_b(j), so while one softmax group computes exponentials the tensor core works for the other;
 //   * a softmax thread owns a whole query row (128 scores of a key tile in registers): no
@@ -15,6 +17,7 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace zdc {
@@ -60,7 +63,8 @@ __global__ void __launch_bounds__(352, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bar + 0;
-  uint64_t* k_full = bar + 1;        // [ST]
+  uint64_t* q_empty = bar + 1;
+  uint64_t* k_full = bar + 2;        // [ST]
   uint64_t* k_empty = k_full + ST;   // [ST]
   uint64_t* v_full = k_empty + ST;   // [ST]
   uint64_t* v_empty = v_full + ST;   // [ST]
@@ -70,28 +74,43 @@ __global__ void __launch_bounds__(352, 1)
   uint64_t* pv_done = p_full + 2;    // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
 
-  // this CTA's query tiles: pair index reversed so the longest causal rows start first
+  // Persistent: work items = (query-tile pair, sequence, head), ordered by causal cost (longest
+  // pairs first) and dealt to the CTAs in a snake order (pass r: CTA c takes item r*ncta + c for
+  // even r, r*ncta + ncta-1-c for odd r), which balances the triangular work across the SMs.
   const int n_qt = (a.n_q + C::BM - 1) / C::BM;
   const int n_pairs = (n_qt + 1) / 2;
-  const int pair = n_pairs - 1 - static_cast<int>(blockIdx.x);
-  const int h = blockIdx.y, b = blockIdx.z;
-  const int G = a.Nh / a.Nkv, g = h / G;
-  int nkv[2], q0[2];
+  const int n_bh = a.B * a.Nh;
+  const int n_items = n_pairs * n_bh;
+  const int ncta = gridDim.x, cta = blockIdx.x;
+  const int G = a.Nh / a.Nkv;
+  auto item_of = [&](int r) -> int { return r * ncta + ((r & 1) ? ncta - 1 - cta : cta); };
+  struct Item {
+    int b, h, g, q0[2], nkv[2], nmax;
+  };
+  auto decode_item = [&](int k) -> Item {
+    Item it;
+    const int pd = k / n_bh, bh = k - pd * n_bh;
+    const int pair = n_pairs - 1 - pd;
+    it.b = bh / a.Nh;
+    it.h = bh - it.b * a.Nh;
+    it.g = it.h / G;
 #pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    const int qt = 2 * pair + t;
-    q0[t] = qt * C::BM;
-    if (qt < n_qt) {
-      const int last_q = min(q0[t] + C::BM, a.n_q) - 1;
-      nkv[t] = (a.q_pos0 + last_q + 1 + C::BN - 1) / C::BN;
-    } else {
-      nkv[t] = 0;  // an odd tile count leaves the last pair with one tile
+    for (int t = 0; t < 2; ++t) {
+      const int qt = 2 * pair + t;
+      it.q0[t] = qt * C::BM;
+      if (qt < n_qt) {
+        const int last_q = min(it.q0[t] + C::BM, a.n_q) - 1;
+        it.nkv[t] = (a.q_pos0 + last_q + 1 + C::BN - 1) / C::BN;
+      } else {
+        it.nkv[t] = 0;  // an odd tile count leaves the last pair with one tile
+      }
     }
-  }
-  const int nmax = max(nkv[0], nkv[1]);
-  auto kv_tile_row = [&](int j) -> int {
+    it.nmax = max(it.nkv[0], it.nkv[1]);
+    return it;
+  };
+  auto kv_tile_row = [&](const Item& it, int j) -> int {
     const int pos = j * C::BN;
-    if (a.kv_mode == 0) return (b * a.Nkv + g) * a.S_cap + pos;
+    if (a.kv_mode == 0) return (it.b * a.Nkv + it.g) * a.S_cap + pos;
     const int qq = pos / a.sp_chunk, rr = pos - qq * a.sp_chunk;  // SP gather buffer
     int owner, local;
     if (!a.sp_zigzag) {
@@ -101,7 +120,7 @@ __global__ void __launch_bounds__(352, 1)
       owner = qq < a.sp_P ? qq : 2 * a.sp_P - 1 - qq;
       local = (qq < a.sp_P ? 0 : a.sp_chunk) + rr;
     }
-    return ((owner * 2 * a.B + b) * a.Nkv + g) * a.sp_n_local + local;
+    return ((owner * 2 * a.B + it.b) * a.Nkv + it.g) * a.sp_n_local + local;
   };
   const uint32_t warp = warp_id(), lane = lane_id();
 
@@ -111,6 +130,7 @@ __global__ void __launch_bounds__(352, 1)
       tma_prefetch_desc(&tk);
       tma_prefetch_desc(&tv);
       mbar_init(q_full, 1);
+      mbar_init(q_empty, 1);
       for (int i = 0; i < ST; ++i) {
         mbar_init(&k_full[i], 1);
         mbar_init(&k_empty[i], 1);
@@ -137,35 +157,44 @@ __global__ void __launch_bounds__(352, 1)
     // ------------------------------------------------ Q' (both tiles) and K' producer
     if (elect_one()) {
       const uint64_t keep = policy_evict_last();
-      const int n_tiles = nkv[1] > 0 ? 2 : 1;
-      mbar_arrive_expect_tx(q_full, C::TILE * n_tiles);
-      for (int t = 0; t < n_tiles; ++t)
+      int gk = 0;  // K'/V' tiles streamed by this CTA so far
+      for (int r = 0, k = item_of(0); k < n_items; k = item_of(++r)) {
+        const Item it = decode_item(k);
+        const int n_tiles = it.nkv[1] > 0 ? 2 : 1;
+        if (r > 0) mbar_wait(q_empty, (r - 1) & 1);  // every S MMA of the previous item is done
+        mbar_arrive_expect_tx(q_full, C::TILE * n_tiles);
+        for (int t = 0; t < n_tiles; ++t)
 #pragma unroll
-        for (int c = 0; c < C::NCH; ++c)
-          tma_load_2d(smem + C::OFF_Q + t * C::TILE + c * C::CHUNK, &tq, q_full, h * HD + c * C::CW,
-                      b * a.S + a.q_row0 + q0[t]);
-      for (int j = 0; j < nmax; ++j) {
-        const int s = j % ST;
-        mbar_wait(&k_empty[s], ((j / ST) & 1) ^ 1);
-        mbar_arrive_expect_tx(&k_full[s], C::TILE);
+          for (int c = 0; c < C::NCH; ++c)
+            tma_load_2d(smem + C::OFF_Q + t * C::TILE + c * C::CHUNK, &tq, q_full, it.h * HD + c * C::CW,
+                        it.b * a.S + a.q_row0 + it.q0[t]);
+        for (int j = 0; j < it.nmax; ++j, ++gk) {
+          const int s = gk % ST;
+          mbar_wait(&k_empty[s], ((gk / ST) & 1) ^ 1);
+          mbar_arrive_expect_tx(&k_full[s], C::TILE);
 #pragma unroll
-        for (int c = 0; c < C::NCH; ++c)
-          tma_load_2d_hint(smem + C::OFF_K + s * C::TILE + c * C::CHUNK, &tk, &k_full[s], c * C::CW,
-                           kv_tile_row(j), keep);
+          for (int c = 0; c < C::NCH; ++c)
+            tma_load_2d_hint(smem + C::OFF_K + s * C::TILE + c * C::CHUNK, &tk, &k_full[s], c * C::CW,
+                             kv_tile_row(it, j), keep);
+        }
       }
     }
   } else if (warp == 9) {
     // ------------------------------------------------ V' producer
     if (elect_one()) {
       const uint64_t keep = policy_evict_last();
-      for (int j = 0; j < nmax; ++j) {
-        const int s = j % ST;
-        mbar_wait(&v_empty[s], ((j / ST) & 1) ^ 1);
-        mbar_arrive_expect_tx(&v_full[s], C::TILE);
+      int gk = 0;
+      for (int r = 0, k = item_of(0); k < n_items; k = item_of(++r)) {
+        const Item it = decode_item(k);
+        for (int j = 0; j < it.nmax; ++j, ++gk) {
+          const int s = gk % ST;
+          mbar_wait(&v_empty[s], ((gk / ST) & 1) ^ 1);
+          mbar_arrive_expect_tx(&v_full[s], C::TILE);
 #pragma unroll
-        for (int c = 0; c < C::NCH; ++c)
-          tma_load_2d_hint(smem + C::OFF_V + s * C::TILE + c * C::CHUNK, &tv, &v_full[s], c * C::CW,
-                           static_cast<int>(kv_tile_row(j) + a.v_row_off), keep);
+          for (int c = 0; c < C::NCH; ++c)
+            tma_load_2d_hint(smem + C::OFF_V + s * C::TILE + c * C::CHUNK, &tv, &v_full[s], c * C::CW,
+                             static_cast<int>(kv_tile_row(it, j) + a.v_row_off), keep);
+        }
       }
     }
   } else if (warp == 10) {
@@ -173,10 +202,11 @@ __global__ void __launch_bounds__(352, 1)
     if (elect_one()) {
       constexpr uint32_t idesc_s = make_idesc_bf16(C::BM, C::BN, 0, 0);
       constexpr uint32_t idesc_o = make_idesc_bf16(C::BM, HD, 0, 1);
-      auto issue_s = [&](int t, int j) {
-        const int s = j % ST;
-        mbar_wait(&k_full[s], (j / ST) & 1);
-        if (j > 0) mbar_wait(&s_free[t], (j - 1) & 1);  // the softmax warps have read S_t(j-1)
+      int cs[2] = {0, 0}, cp[2] = {0, 0};  // S / PV tiles issued per query tile (all items)
+      auto issue_s = [&](int t, int gk) {
+        const int s = gk % ST;
+        mbar_wait(&k_full[s], (gk / ST) & 1);
+        if (cs[t] > 0) mbar_wait(&s_free[t], (cs[t] - 1) & 1);  // the softmax warps have read S_t
         tc_fence_after();
         const uint32_t q_addr = smem_u32(smem + C::OFF_Q + t * C::TILE);
         const uint32_t k_addr = smem_u32(smem + C::OFF_K + s * C::TILE);
@@ -189,11 +219,12 @@ __global__ void __launch_bounds__(352, 1)
             umma_bf16_ss(tmem + t * 128, ad, bd, idesc_s, (c | kk) != 0 ? 1u : 0u);
           }
         umma_commit(&s_full[t]);
+        ++cs[t];
       };
-      auto issue_pv = [&](int t, int j) {
-        const int s = j % ST;
-        mbar_wait(&p_full[t], j & 1);
-        mbar_wait(&v_full[s], (j / ST) & 1);
+      auto issue_pv = [&](int t, int gk, bool first) {
+        const int s = gk % ST;
+        mbar_wait(&p_full[t], cp[t] & 1);
+        mbar_wait(&v_full[s], (gk / ST) & 1);
         tc_fence_after();
         const uint32_t p_addr = smem_u32(smem + C::OFF_P + t * C::P_BYTES);
         const uint32_t v_addr = smem_u32(smem + C::OFF_V + s * C::TILE);
@@ -201,137 +232,153 @@ __global__ void __launch_bounds__(352, 1)
         for (int kk = 0; kk < C::BN / 16; ++kk) {
           const uint64_t ad = make_sdesc(p_addr + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, kSw128);
           const uint64_t bd = make_sdesc(v_addr + kk * 16 * C::SWB, C::CHUNK, 8 * C::SWB, C::LAYOUT);
-          umma_bf16_ss(tmem + C::O_COL + t * HD, ad, bd, idesc_o, (j | kk) != 0 ? 1u : 0u);
+          umma_bf16_ss(tmem + C::O_COL + t * HD, ad, bd, idesc_o, (!first || kk != 0) ? 1u : 0u);
         }
         umma_commit(&pv_done[t]);
+        ++cp[t];
       };
-      mbar_wait(q_full, 0);
-      for (int t = 0; t < 2; ++t)
-        if (nkv[t] > 0) issue_s(t, 0);
-      if (nmax > 0) umma_commit(&k_empty[0]);
-      for (int j = 0; j < nmax; ++j) {
-        for (int t = 0; t < 2; ++t) {
-          if (j + 1 < nkv[t]) issue_s(t, j + 1);
-          if (j < nkv[t]) issue_pv(t, j);
+      int gk0 = 0;
+      for (int r = 0, k = item_of(0); k < n_items; k = item_of(++r)) {
+        const Item it = decode_item(k);
+        mbar_wait(q_full, r & 1);
+        for (int t = 0; t < 2; ++t)
+          if (it.nkv[t] > 0) issue_s(t, gk0);
+        if (it.nmax > 0) umma_commit(&k_empty[gk0 % ST]);
+        for (int j = 0; j < it.nmax; ++j) {
+          for (int t = 0; t < 2; ++t) {
+            if (j + 1 < it.nkv[t]) issue_s(t, gk0 + j + 1);
+            if (j < it.nkv[t]) issue_pv(t, gk0 + j, j == 0);
+          }
+          if (j + 1 < it.nmax) umma_commit(&k_empty[(gk0 + j + 1) % ST]);  // K'(j+1) read by both S
+          umma_commit(&v_empty[(gk0 + j) % ST]);                           // V'(j) read by both PV
         }
-        if (j + 1 < nmax) umma_commit(&k_empty[(j + 1) % ST]);  // K'(j+1) read by both S MMAs
-        umma_commit(&v_empty[j % ST]);                          // V'(j) read by both PV MMAs
+        umma_commit(q_empty);  // Q' of this item no longer read once these MMAs complete
+        gk0 += it.nmax;
       }
     }
   } else {
     // ------------------------------------------------ softmax: warps 0-3 tile a, 4-7 tile b
     const int t = warp >> 2, qq = warp & 3;
     const int r = qq * 32 + lane;  // query row of the tile = TMEM lane
-    const int n = nkv[t];
-    const int qpos = a.q_pos0 + q0[t] + r;
-    const int qbase = a.q_pos0 + q0[t] + qq * 32;  // first row of this warp
     const uint32_t lane_base = (qq * 32) << 16;
     const uint32_t s_col = tmem + lane_base + t * 128;
     const uint32_t o_col = tmem + lane_base + C::O_COL + t * HD;
     const float sl = a.scale * kLog2e4;
     const uint32_t p_base = smem_u32(smem + C::OFF_P + t * C::P_BYTES);
-    float m_ref = -INFINITY, l_run = 0.f;
-    for (int j = 0; j < n; ++j) {
-      mbar_wait(&s_full[t], j & 1);
-      tc_fence_after();
-      uint32_t sv[4][32];
+    int base = 0;  // S / P / PV tiles of this query tile consumed so far (all items)
+    for (int ri = 0, k = item_of(0); k < n_items; k = item_of(++ri)) {
+      const Item it = decode_item(k);
+      const int n = it.nkv[t];
+      const int q0 = it.q0[t];
+      const int qpos = a.q_pos0 + q0 + r;
+      const int qbase = a.q_pos0 + q0 + qq * 32;  // first row of this warp
+      float m_ref = -INFINITY, l_run = 0.f;
+      for (int j = 0; j < n; ++j) {
+        const int gi = base + j;
+        mbar_wait(&s_full[t], gi & 1);
+        tc_fence_after();
+        uint32_t sv[4][32];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(s_col + c * 32, sv[c]);
-      tc_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[t]);
-      const int key0 = j * C::BN;
-      if (key0 + C::BN - 1 > qbase) {  // tile crosses this warp's diagonal
+        for (int c = 0; c < 4; ++c) tmem_ld32(s_col + c * 32, sv[c]);
+        tc_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_free[t]);
+        const int key0 = j * C::BN;
+        if (key0 + C::BN - 1 > qbase) {  // tile crosses this warp's diagonal
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (key0 + c * 32 + e > qpos) sv[c][e] = __float_as_uint(-INFINITY);
+        }
+        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
         for (int c = 0; c < 4; ++c)
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (key0 + c * 32 + e > qpos) sv[c][e] = __float_as_uint(-INFINITY);
-      }
-      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+          for (int e = 0; e < 32; ++e) mx4[e & 3] = fmaxf(mx4[e & 3], __uint_as_float(sv[c][e]));
+        const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sl;  // scale > 0
+        // lazy rescale: raise the reference only when this tile exceeds it by > 2^kLazyRescale
+        const bool raise = mx > m_ref + kLazyRescale;
+        const float m_new = raise ? mx : m_ref;
+        const float alpha = raise ? exp2f(m_ref - m_new) : 1.f;  // 0 on the first tile
+        const float mref = m_new == -INFINITY ? 0.f : m_new;
+        float ps4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < 4; ++c)
 #pragma unroll
-        for (int e = 0; e < 32; ++e) mx4[e & 3] = fmaxf(mx4[e & 3], __uint_as_float(sv[c][e]));
-      const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sl;  // scale > 0
-      // lazy rescale: raise the reference only when this tile exceeds it by > 2^kLazyRescale
-      const bool raise = mx > m_ref + kLazyRescale;
-      const float m_new = raise ? mx : m_ref;
-      const float alpha = raise ? exp2f(m_ref - m_new) : 1.f;  // 0 on the first tile
-      const float mref = m_new == -INFINITY ? 0.f : m_new;
-      float ps4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          // 2^(s * scale*log2e - m): one FFMA + MUFU.EX2 per score (masked scores are -inf -> 0)
-          const float p0 = fast_exp2(fmaf(__uint_as_float(sv[c][2 * e]), sl, -mref));
-          const float p1 = fast_exp2(fmaf(__uint_as_float(sv[c][2 * e + 1]), sl, -mref));
-          ps4[e & 3] += p0 + p1;
-          sv[c][e] = pack_bf16x2(p0, p1);  // packed in place (e <= 2e)
-        }
-      l_run = l_run * alpha + ((ps4[0] + ps4[1]) + (ps4[2] + ps4[3]));
-      m_ref = m_new;
-      // O_t and the P_t buffer are free once PV_t(j-1) has completed
-      if (j > 0) {
-        mbar_wait(&pv_done[t], (j - 1) & 1);
-        tc_fence_after();
-        if (__any_sync(0xffffffffu, raise)) {
-#pragma unroll
-          for (int c0 = 0; c0 < HD; c0 += 16) {
-            uint32_t ov[16];
-            tmem_ld16(o_col + c0, ov);
-            tc_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 16; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-            tmem_st16(o_col + c0, ov);
+          for (int e = 0; e < 16; ++e) {
+            // 2^(s * scale*log2e - m): one FFMA + MUFU.EX2 per score (masked scores are -inf -> 0)
+            const float p0 = fast_exp2(fmaf(__uint_as_float(sv[c][2 * e]), sl, -mref));
+            const float p1 = fast_exp2(fmaf(__uint_as_float(sv[c][2 * e + 1]), sl, -mref));
+            ps4[e & 3] += p0 + p1;
+            sv[c][e] = pack_bf16x2(p0, p1);  // packed in place (e <= 2e)
           }
-          tc_wait_st();
-        }
-      }
-      // P row -> shared memory, K-major 128B swizzle: keys [0,64) in chunk 0, [64,128) in chunk 1
+        l_run = l_run * alpha + ((ps4[0] + ps4[1]) + (ps4[2] + ps4[3]));
+        m_ref = m_new;
+        // O_t and the P_t buffer are free once PV_t(j-1) has completed
+        if (j > 0) {
+          mbar_wait(&pv_done[t], (gi - 1) & 1);
+          tc_fence_after();
+          if (__any_sync(0xffffffffu, raise)) {
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const int c = u >> 2, e = (u & 3) * 4;  // 8 keys per 16-byte unit: sv[c][e..e+3]
-        sts128_4(p_base + (u >> 3) * 16384 + sw128_off(r, u & 7), sv[c][e], sv[c][e + 1], sv[c][e + 2],
-                 sv[c][e + 3]);
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[t]);
-    }
-    // ---- epilogue: O / l -> bf16, LSE = m + log2 l (natural log out)
-    if (n > 0) {
-      mbar_wait(&pv_done[t], (n - 1) & 1);
-      tc_fence_after();
-      const float inv_l = 1.f / l_run;
-      const bool valid = q0[t] + r < a.n_q;
-      uint16_t* orow = a.o + static_cast<int64_t>(b * a.S + a.q_row0 + q0[t] + r) * a.ldo + h * HD;
+            for (int c0 = 0; c0 < HD; c0 += 16) {
+              uint32_t ov[16];
+              tmem_ld16(o_col + c0, ov);
+              tc_wait_ld();
 #pragma unroll
-      for (int c0 = 0; c0 < HD; c0 += 16) {
-        uint32_t ov[16];
-        tmem_ld16(o_col + c0, ov);
-        tc_wait_ld();
-        if (valid) {
-          uint4 w0, w1;
-          w0.x = pack_bf16x2(__uint_as_float(ov[0]) * inv_l, __uint_as_float(ov[1]) * inv_l);
-          w0.y = pack_bf16x2(__uint_as_float(ov[2]) * inv_l, __uint_as_float(ov[3]) * inv_l);
-          w0.z = pack_bf16x2(__uint_as_float(ov[4]) * inv_l, __uint_as_float(ov[5]) * inv_l);
-          w0.w = pack_bf16x2(__uint_as_float(ov[6]) * inv_l, __uint_as_float(ov[7]) * inv_l);
-          w1.x = pack_bf16x2(__uint_as_float(ov[8]) * inv_l, __uint_as_float(ov[9]) * inv_l);
-          w1.y = pack_bf16x2(__uint_as_float(ov[10]) * inv_l, __uint_as_float(ov[11]) * inv_l);
-          w1.z = pack_bf16x2(__uint_as_float(ov[12]) * inv_l, __uint_as_float(ov[13]) * inv_l);
-          w1.w = pack_bf16x2(__uint_as_float(ov[14]) * inv_l, __uint_as_float(ov[15]) * inv_l);
-          *reinterpret_cast<uint4*>(orow + c0) = w0;
-          *reinterpret_cast<uint4*>(orow + c0 + 8) = w1;
+              for (int e = 0; e < 16; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+              tmem_st16(o_col + c0, ov);
+            }
+            tc_wait_st();
+          }
         }
+        // P row -> shared memory, K-major 128B swizzle: keys [0,64) in chunk 0, [64,128) in chunk 1
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int c = u >> 2, e = (u & 3) * 4;  // 8 keys per 16-byte unit: sv[c][e..e+3]
+          sts128_4(p_base + (u >> 3) * 16384 + sw128_off(r, u & 7), sv[c][e], sv[c][e + 1], sv[c][e + 2],
+                   sv[c][e + 3]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t]);
       }
-      if (valid && a.lse)
-        a.lse[(static_cast<int64_t>(b) * a.Nh + h) * a.S + a.q_row0 + q0[t] + r] = (m_ref + log2f(l_run)) * kLn2_4;
+      // ---- epilogue: O / l -> bf16, LSE = m + log2 l (natural log out).  The next item's first
+      // PV (which overwrites O_t) waits for this tile's next P, written after these reads.
+      if (n > 0) {
+        mbar_wait(&pv_done[t], (base + n - 1) & 1);
+        tc_fence_after();
+        const float inv_l = 1.f / l_run;
+        const bool valid = q0 + r < a.n_q;
+        uint16_t* orow = a.o + static_cast<int64_t>(it.b * a.S + a.q_row0 + q0 + r) * a.ldo + it.h * HD;
+#pragma unroll
+        for (int c0 = 0; c0 < HD; c0 += 16) {
+          uint32_t ov[16];
+          tmem_ld16(o_col + c0, ov);
+          tc_wait_ld();
+          if (valid) {
+            uint4 w0, w1;
+            w0.x = pack_bf16x2(__uint_as_float(ov[0]) * inv_l, __uint_as_float(ov[1]) * inv_l);
+            w0.y = pack_bf16x2(__uint_as_float(ov[2]) * inv_l, __uint_as_float(ov[3]) * inv_l);
+            w0.z = pack_bf16x2(__uint_as_float(ov[4]) * inv_l, __uint_as_float(ov[5]) * inv_l);
+            w0.w = pack_bf16x2(__uint_as_float(ov[6]) * inv_l, __uint_as_float(ov[7]) * inv_l);
+            w1.x = pack_bf16x2(__uint_as_float(ov[8]) * inv_l, __uint_as_float(ov[9]) * inv_l);
+            w1.y = pack_bf16x2(__uint_as_float(ov[10]) * inv_l, __uint_as_float(ov[11]) * inv_l);
+            w1.z = pack_bf16x2(__uint_as_float(ov[12]) * inv_l, __uint_as_float(ov[13]) * inv_l);
+            w1.w = pack_bf16x2(__uint_as_float(ov[14]) * inv_l, __uint_as_float(ov[15]) * inv_l);
+            *reinterpret_cast<uint4*>(orow + c0) = w0;
+            *reinterpret_cast<uint4*>(orow + c0 + 8) = w1;
+          }
+        }
+        if (valid && a.lse)
+          a.lse[(static_cast<int64_t>(it.b) * a.Nh + it.h) * a.S + a.q_row0 + q0 + r] =
+              (m_ref + log2f(l_run)) * kLn2_4;
+        tc_fence_before();
+      }
+      base += n;
     }
-    tc_fence_before();
   }
   __syncthreads();
   if (warp == 8) {
@@ -359,7 +406,8 @@ static cudaError_t launch_attn4_t(const PrefillAttnArgs& a, cudaStream_t stream)
   if (!make_tmap_2d(&tk, a.k, HD, kv_rows, HD * 2, C::CW, C::BN, C::SWB)) return cudaErrorInvalidValue;
   if (!make_tmap_2d(&tv, a.v, HD, kv_rows, HD * 2, C::CW, C::BN, C::SWB)) return cudaErrorInvalidValue;
   const int n_qt = (a.n_q + C::BM - 1) / C::BM;
-  dim3 grid((n_qt + 1) / 2, a.Nh, a.B);
+  const int n_items = (n_qt + 1) / 2 * a.Nh * a.B;
+  dim3 grid(std::min(n_items, num_sms()));  // persistent: the kernel deals the items to the CTAs
   prof_mark(stream, true, kProfAttnPrefill);
   prefill_attn4_kernel<HD><<<grid, 352, C::SMEM, stream>>>(tq, tk, tv, a);
   prof_mark(stream, false, kProfAttnPrefill);
