@@ -1,2 +1,3 @@
-timeout 600 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_prefill.py tests/test_gpu_sp.py -x -q 2>&1 | tail -2
-timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --sp 2>/dev/null | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); k=d['kernels']['a3_prefill_attention']; print('ATTN v4e', round(d['value']), round(d['prefill_tok_s']), d['prefill_ms'], k['avg_us'], k['achieved'], k['frac'], d['sp']['sp_prefill_tok_s'])"
+timeout 900 python -m pytest tests -m gpu -x -q -k "decode or configs" 2>&1 | tail -2
+timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-sp 2>/dev/null | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('FLAT', round(d['value']), d['ms_per_step'], round(d['decode_tok_s']), d['roofline']['frac'])"
+ZDC_FUSED_TRACE=1 timeout 300 python tools/trace_fused.py --layers 4 --ctx 2176
