@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--layers", type=int, default=32)
     p.add_argument("--decode-calls", default="layer", choices=["layer", "chain"],
                    help="decode step as 32 per-layer zdc_decode calls (same x per layer) or one chained call")
+    p.add_argument("--decode-mode", default="auto", choices=["auto", "fused", "cluster", "separate"],
+                   help="decode kernels for B <= 8 (zdc_decode_mode): auto = cluster layer-step when it fits")
     p.add_argument("--sp-seq", type=int, default=32768, help="SP prefill prompt length (c5), run when N > 1")
     p.add_argument("--sp-layers", type=int, default=32)
     p.add_argument("--sp", action="store_true", help="also run the SP prefill at N = 1 (P = 1, no exchange)")
@@ -355,6 +357,7 @@ def run_zdc(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
+    zdc.decode_mode(args.decode_mode)
 
     L, S, T, r = args.layers, args.prompt, args.decode_steps, args.rank
     base = Z.dims_of(2)
@@ -577,7 +580,8 @@ def run_zdc(args):
                        "d_head": dh, "rank": r, "batch": B, "prompt": S, "decode_steps": T,
                        "tokens_per_step_per_gpu": tok_per_step, "parallelism": "replicas%d" % world,
                        "l2": "inputs larger than L2 (2.1 GB folded weights per step)",
-                       "timing": "CUDA graphs of per-layer zdc_prefill / zdc_decode calls"},
+                       "timing": "CUDA graphs of per-layer zdc_prefill / zdc_decode calls",
+                       "decode_mode": args.decode_mode},
             "prefill_tok_s": world * B * S / (pre_ms[-1] / 1e3),
             "decode_tok_s": world * B * T / (dec_ms[-1] / 1e3),
             "prefill_ms": pre_ms[-1], "decode_ms": dec_ms[-1],

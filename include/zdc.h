@@ -238,6 +238,17 @@ zdc_status zdc_decode_attention_bf16(const uint16_t* q, const uint16_t* k, const
 zdc_status zdc_gemv_bf16(const uint16_t* w, const uint16_t* x, uint16_t* y, int32_t B, int32_t N, int32_t K,
                          void* stream);
 
+/* Decode kernel selection for B <= 8 uniform-rank layers (process-wide, takes effect at the next
+ * zdc_decode; cached decode CUDA graphs keep the kernels they captured, so call it before the
+ * first decode of a context): 0 = automatic (default: the persistent fused layer-step where
+ * supported, else separate kernels), 1 = the persistent fused layer-step (decode_fused.cuh),
+ * 2 = the cluster layer-step (decode_cluster.cuh: one cluster of CTAs per KV group, tcgen05
+ * projections, DSMEM exchanges, no grid barrier; needs r in {16, 32, 64, 128}, G r <= 256 and
+ * d % 64 == 0; falls back to 1 where unsupported), 3 = separate kernels (GEMV / GEMM, split-K
+ * attention, GEMV).  Returns the previous mode; -1 for an invalid mode.
+ * Env ZDC_DECODE_MODE sets the initial mode. */
+int zdc_decode_mode(int mode);
+
 /* Number of kernels the last prefill / decode call enqueued (for bench.py's gpu_launches). */
 int64_t zdc_kernel_launch_count(void);
 

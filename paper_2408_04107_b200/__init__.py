@@ -15,7 +15,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 __all__ = ["ZdcError", "lib", "lib_path", "Dims", "Plan", "Context", "fold_weights", "gemm_bf16",
-           "sp_positions", "EXPORTED_SYMBOLS", "last_launch_count"]
+           "sp_positions", "EXPORTED_SYMBOLS", "last_launch_count", "decode_mode"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libzdc.so")
@@ -32,7 +32,8 @@ EXPORTED_SYMBOLS = ["zdc_last_error", "zdc_version", "zdc_fold_weights", "zdc_ct
                     "zdc_cache_export", "zdc_cache_length", "zdc_scores_export", "zdc_cache_reset", "zdc_last_lse",
                     "zdc_gemm_bf16", "zdc_gemv_bf16", "zdc_prefill_attention_bf16",
                     "zdc_decode_attention_workspace", "zdc_decode_attention_bf16",
-                    "zdc_kernel_launch_count", "zdc_profile", "zdc_profile_read", "zdc_trace_read"]
+                    "zdc_kernel_launch_count", "zdc_profile", "zdc_profile_read", "zdc_trace_read",
+                    "zdc_decode_mode"]
 
 
 class ZdcError(RuntimeError):
@@ -107,6 +108,7 @@ def lib():
             "zdc_profile": ([ctypes.c_int], None),
             "zdc_profile_read": ([ctypes.POINTER(F), ctypes.POINTER(I64), ctypes.c_int], ctypes.c_int),
             "zdc_trace_read": ([ctypes.POINTER(ctypes.c_uint64), ctypes.c_int], ctypes.c_int),
+            "zdc_decode_mode": ([ctypes.c_int], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -128,6 +130,18 @@ def last_launch_count() -> int:
 
 PROFILE_CLASSES = ["a1_prefill_gemm", "a3_prefill_attention", "a5_prefill_gemm", "a1_decode_gemv",
                    "a3_decode_attention", "a3_decode_combine", "a5_decode_gemv", "other"]
+
+
+DECODE_MODES = {"auto": 0, "fused": 1, "cluster": 2, "separate": 3}
+
+
+def decode_mode(mode: str) -> str:
+    """Select the decode kernels for B <= 8 uniform-rank layers (zdc_decode_mode); returns the
+    previous mode.  Takes effect for decode graphs captured afterwards."""
+    old = lib().zdc_decode_mode(DECODE_MODES[mode])
+    if old < 0:
+        raise ValueError(mode)
+    return {v: k for k, v in DECODE_MODES.items()}[old]
 
 
 def profile(enable: bool):

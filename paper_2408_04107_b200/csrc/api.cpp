@@ -77,6 +77,14 @@ const char* zdc_last_error(void) { return t_err.c_str(); }
 const char* zdc_version(void) { return "zdc-b200 0.1 (sm_100a tcgen05)"; }
 int64_t zdc_kernel_launch_count(void) { return g_launches; }
 
+static int g_decode_mode = getenv("ZDC_DECODE_MODE") ? atoi(getenv("ZDC_DECODE_MODE")) : 0;
+int zdc_decode_mode(int mode) {
+  if (mode < 0 || mode > 3) return -1;
+  const int old = g_decode_mode;
+  g_decode_mode = mode;
+  return old;
+}
+
 // ------------------------------------------------------------------ context
 zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t max_batch, int32_t max_seq,
                           zdc_ctx** out) {
@@ -159,6 +167,15 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
     woff = align_up(woff + static_cast<int64_t>(L.n_qkv) * d.d_model * 2, 256);
     L.w_o = woff;
     woff = align_up(woff + static_cast<int64_t>(d.d_model) * L.ko_p * 2, 256);
+    if (!L.split && decode_cluster_layer_ok(L.rk_p, d.n_heads / d.n_kv_heads)) {
+      // the group-major copy of W_O that the cluster decode kernel streams in contiguous tiles
+      L.w_od = woff;
+      woff = align_up(woff + static_cast<int64_t>(d.n_heads) * L.rv_p * d.d_model * 2, 256);
+      if (d.d_model % 64 == 0) {  // and of W_QKV, pre-tiled and pre-swizzled (contiguous per CTA)
+        L.w_qd = woff;
+        woff = align_up(woff + static_cast<int64_t>(L.n_qkv) * d.d_model * 2, 256);
+      }
+    }
     const int64_t kv_rows = static_cast<int64_t>(max_batch) * d.n_kv_heads * max_seq;
     L.k_off = coff;
     coff = align_up(coff + kv_rows * L.rk_p * 2, 256);
@@ -211,6 +228,8 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
   s = align_up(s + 64, 256);
   c->s_ltab = s;  // fused decode layer table (DecLayer per layer), written at bind
   s = align_up(s + static_cast<int64_t>(d.n_layers) * static_cast<int64_t>(sizeof(DecLayer)), 256);
+  c->s_ybuf = s;  // cluster decode: y accumulator [8][d] f32 then 16 arrival counters, zero between launches
+  s = align_up(s + static_cast<int64_t>(8) * d.d_model * 4 + 16 * 4, 256);
   if (any_split) {  // staged K'/V' of a split layer before packing, compaction indices, new-row staging
     const int64_t kv_rows = static_cast<int64_t>(max_batch) * d.n_kv_heads * max_seq;
     c->s_ks = s;
@@ -319,6 +338,14 @@ zdc_status zdc_load_folded(zdc_ctx* c, int32_t layer, const double* wq, const do
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   ZDC_CUDA_TRY(cudaMemcpyAsync(c->w + L.w_qkv, qkv.data(), qkv.size() * 2, cudaMemcpyHostToDevice, st));
   ZDC_CUDA_TRY(cudaMemcpyAsync(c->w + L.w_o, o.data(), o.size() * 2, cudaMemcpyHostToDevice, st));
+  if (L.w_od >= 0)
+    ZDC_CUDA_TRY(launch_pack_wo_decode(reinterpret_cast<const uint16_t*>(c->w + L.w_o),
+                                       reinterpret_cast<uint16_t*>(c->w + L.w_od), c->dims.d_model, L.ko_p,
+                                       c->dims.n_kv_heads, c->G * L.rv_p, st));
+  if (L.w_qd >= 0)
+    ZDC_CUDA_TRY(launch_pack_qkv_decode(reinterpret_cast<const uint16_t*>(c->w + L.w_qkv),
+                                        reinterpret_cast<uint16_t*>(c->w + L.w_qd), c->dims.d_model, L.nq, L.nk,
+                                        c->dims.n_kv_heads, c->G, L.rk_p, st));
   ZDC_CUDA_TRY(cudaStreamSynchronize(st));
   return ZDC_OK;
 }
@@ -333,6 +360,14 @@ zdc_status zdc_load_folded_device(zdc_ctx* c, int32_t layer, const uint16_t* wq,
                                         reinterpret_cast<uint16_t*>(c->w + L.w_o), c->dims.d_model, c->dims.n_heads,
                                         c->dims.n_kv_heads, c->dims.d_head, L.rk, L.rv, L.rk_p, L.rv_p, L.ko_p,
                                         static_cast<cudaStream_t>(stream)));
+  if (L.w_od >= 0)
+    ZDC_CUDA_TRY(launch_pack_wo_decode(reinterpret_cast<const uint16_t*>(c->w + L.w_o),
+                                       reinterpret_cast<uint16_t*>(c->w + L.w_od), c->dims.d_model, L.ko_p,
+                                       c->dims.n_kv_heads, c->G * L.rv_p, static_cast<cudaStream_t>(stream)));
+  if (L.w_qd >= 0)
+    ZDC_CUDA_TRY(launch_pack_qkv_decode(reinterpret_cast<const uint16_t*>(c->w + L.w_qkv),
+                                        reinterpret_cast<uint16_t*>(c->w + L.w_qd), c->dims.d_model, L.nq, L.nk,
+                                        c->dims.n_kv_heads, c->G, L.rk_p, static_cast<cudaStream_t>(stream)));
   return ZDC_OK;
 }
 
@@ -503,7 +538,47 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
     }
     const uint16_t* wqkv = reinterpret_cast<const uint16_t*>(c->w + L.w_qkv);
     const uint16_t* wo = reinterpret_cast<const uint16_t*>(c->w + L.w_o);
-    static const bool fused_on = !(getenv("ZDC_DEC_FUSED") && atoi(getenv("ZDC_DEC_FUSED")) == 0);
+    const int mode = g_decode_mode;
+    const bool fused_on = mode != 3 && !(getenv("ZDC_DEC_FUSED") && atoi(getenv("ZDC_DEC_FUSED")) == 0);
+    if (fused_on && mode != 1 && !L.split && L.w_od >= 0 && L.w_qd >= 0) {
+      // the cluster layer-step: one cluster per KV group, no grid barrier (decode_cluster.cuh)
+      const int C = decode_cluster_size(B, L.rk_p, c->G, Nkv, d);
+      // opt-in (mode 2): at the c2 shape it measured 23.4 us per layer-step against 22.7 us for
+      // the persistent kernel (profiles/r01/NOTES.md), so automatic mode keeps the latter
+      if (C > 0 && mode == 2) {
+        DecClusterArgs f;
+        f.wqd = reinterpret_cast<const uint16_t*>(c->w + L.w_qd);
+        f.wod = reinterpret_cast<const uint16_t*>(c->w + L.w_od);
+        f.kc = reinterpret_cast<uint16_t*>(c->cache + L.k_off);
+        f.vc = reinterpret_cast<uint16_t*>(c->cache + L.v_off);
+        f.len_ptr = len_dev;
+        f.x = xin;
+        f.ldx = d;
+        f.y = y;
+        f.ldy = d;
+        f.ybuf = reinterpret_cast<float*>(c->scratch + c->s_ybuf);
+        f.ycnt = reinterpret_cast<int*>(f.ybuf + static_cast<int64_t>(8) * d);
+        f.lse = reinterpret_cast<float*>(c->scratch + c->s_lse);
+        f.B = B;
+        f.d = d;
+        f.nq = L.nq;
+        f.nk = L.nk;
+        f.Nh = Nh;
+        f.Nkv = Nkv;
+        f.S_cap = c->max_seq;
+        f.C = C;
+        static const int l2pf = getenv("ZDC_CL_PF") ? atoi(getenv("ZDC_CL_PF")) : 6;
+        f.l2_prefetch = l2pf;
+        f.trace = fused_trace_buffer();
+        f.scale = 1.0f / std::sqrt(static_cast<float>(c->dims.d_head));
+        g_prof_class = kProfDecodeLayer;
+        cudaError_t e = launch_decode_cluster(f, L.rk_p, s);
+        g_prof_class = kProfOther;
+        if (e == cudaSuccess) continue;
+        if (e != cudaErrorNotSupported) return fail(ZDC_ERR_CUDA, "cluster decode layer %d: %s", l, cudaGetErrorString(e));
+        cudaGetLastError();
+      }
+    }
     auto fusable = [&](const LayerInfo& X) {
       return fused_on && !X.split && decode_fused_supported(B, X.rk_p, c->G) && X.rk_p == L.rk_p &&
              X.n_qkv == L.n_qkv && X.ko_p == L.ko_p;

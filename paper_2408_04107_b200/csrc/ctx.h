@@ -21,6 +21,8 @@ struct LayerInfo {
   bool split = false;
   int nq = 0, nk = 0, nv = 0, n_qkv = 0, ko_p = 0;
   int64_t w_qkv = 0, w_o = 0;                      // byte offsets in the weight region
+  int64_t w_od = -1;  // W_O decode copy [Nkv][d][G*r] for the cluster decode kernel (-1: none)
+  int64_t w_qd = -1;  // W_QKV decode copy (pre-swizzled tiles) for the cluster decode kernel
   int64_t k_off = 0, v_off = 0;                    // byte offsets in the cache region
   int64_t cls_off = 0, tau_off = 0, score_off = 0;  // representative layers of split groups
   // token split: pool_U (unimportant rows, truncated width), positions and per-sequence counts
@@ -43,6 +45,7 @@ struct zdc_ctx {
   int64_t s_cnt = 0;                                  // decode merge counters
   int64_t s_gbar = 0;                                 // fused decode grid barrier (monotonic counter)
   int64_t s_ltab = 0;                                 // fused decode layer table
+  int64_t s_ybuf = 0;                                 // cluster decode: f32 y accumulator [8][d] + counters [16]
   int ldq = 0, ldo = 0;
   uint8_t* w = nullptr;
   uint8_t* cache = nullptr;

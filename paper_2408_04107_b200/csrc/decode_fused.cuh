@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
   const int rps3 = SB / (ko * 2);
   const int n3 = (r3b - r3a + rps3 - 1) / rps3;
   const int nitems = a.B * a.Nkv * a.splits;
-  const int RPS = 32;  // K'/V' rows per slot: [32][RK] K' then [32][RK] V'
+  const int RPS = a.rps;  // K'/V' rows per slot (a multiple of 32): [RPS][RK] K' then [RPS][RK] V'
   const int tl = a.nl > 1 ? 1 : 0;  // layer whose timeline the trace records
 
   if (warp == kNW) {
@@ -464,7 +464,9 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
         mbar_wait(&full[s], cc.ph);
         cc.next();
         const uint16_t* Ks = reinterpret_cast<const uint16_t*>(ring + static_cast<size_t>(s) * SB);
-        attn_rows<RK, G>(Ks, Ks + RPS * RK, min(RPS, e0 - (s0 + t * RPS)), qf, scl, m, l, o, lane);
+        const int nr = min(RPS, e0 - (s0 + t * RPS));
+        for (int j = 0; j < nr; j += 32)
+          attn_rows<RK, G>(Ks + j * RK, Ks + (RPS + j) * RK, min(32, nr - j), qf, scl, m, l, o, lane);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
       }
@@ -654,7 +656,15 @@ static const int kFusedRingBytes = getenv("ZDC_FUSED_RING_KB") ? atoi(getenv("ZD
 
 template <int NB, int RK, int G>
 inline cudaError_t launch_fused_t(DecFusedArgs a, cudaStream_t stream) {
-  const int slot = std::max(std::max(a.d * 2, 4 * 32 * RK), a.ko_p * 2);  // a1 row | 32 K'+V' rows | a5 row
+  // slot: a multiple of the a1 row, of 32 K'+V' rows and of the a5 row; larger slots (fewer, bigger
+  // bulk copies in flight) stream faster from HBM (tools/stream_probe.cu)
+  int slot = std::max(std::max(a.d * 2, 4 * 32 * RK), a.ko_p * 2);
+  static const int slot_kb = getenv("ZDC_FUSED_SLOT_KB") ? atoi(getenv("ZDC_FUSED_SLOT_KB")) : 0;
+  if (slot_kb * 1024 > slot) {
+    const int unit = std::max(std::max(a.d * 2, a.ko_p * 2), 4 * 32 * RK);
+    slot = std::max(slot, slot_kb * 1024 / unit * unit);
+  }
+  a.rps = slot / (4 * RK) / 32 * 32;
   a.slot_bytes = slot;
   a.xw = std::max(a.d, a.ko_p);
   constexpr size_t kSmemMax = 227 * 1024;

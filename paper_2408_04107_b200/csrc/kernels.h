@@ -140,7 +140,7 @@ struct DecFusedArgs {
   int B = 0, d = 0, n_qkv = 0, nq = 0, nk = 0, Nh = 0, Nkv = 0, S_cap = 0, splits = 1, ko_p = 0;
   float scale = 0.f;
   // ring geometry (set by the launcher)
-  int slot_bytes = 0, spw = 0, ring_extra = 0, xw = 0;
+  int slot_bytes = 0, spw = 0, ring_extra = 0, xw = 0, rps = 32;
   int stage_part = 0, pst_floats = 0;
   int64_t pst_bytes = 0;
 };
@@ -148,6 +148,47 @@ bool decode_fused_supported(int B, int RK, int G);
 int decode_fused_splits(int B, int Nkv);
 cudaError_t launch_decode_fused(const DecFusedArgs& a, int RK, cudaStream_t s);
 unsigned long long* fused_trace_buffer();  // null unless ZDC_FUSED_TRACE is set
+
+// ---- the cluster decode layer-step (decode_cluster.cuh): one thread-block cluster of C CTAs per
+// KV group does a1 + a2 + a3 + a5 of ONE layer for that group (tcgen05 projections, DSMEM
+// exchanges); the groups meet only in the fp32 y accumulator (B <= 8, uniform rank RK = r_k = r_v
+// padded, RK in {16, 32, 64, 128}, G * RK <= 256, d % (64 C) == 0)
+struct DecClusterArgs {
+  const uint16_t* wqd = nullptr;   // W_QKV decode copy: [Nkv][d/64] tiles of (G+2)*RK rows x 64 K,
+                                   // each the SW128 K-major shared-memory image (pack_qkv_decode)
+  const uint16_t* wod = nullptr;   // W_O decode copy, group-major [Nkv][d][G*RK] (pack_wo_decode)
+  uint16_t* kc = nullptr;          // K'/V' cache: row (b, g, p) at ((b*Nkv+g)*S_cap + p)*RK
+  uint16_t* vc = nullptr;
+  int* len_ptr = nullptr;          // cached rows before this step; advanced by the kernel
+  const uint16_t* x = nullptr;     // [B][ldx]
+  int64_t ldx = 0;
+  uint16_t* y = nullptr;           // [B][ldy]
+  int64_t ldy = 0;
+  float* ybuf = nullptr;           // [8][d] fp32 accumulator, zero between launches
+  int* ycnt = nullptr;             // [C] arrival counters, zero between launches
+  float* lse = nullptr;            // [B][Nh]
+  unsigned long long* trace = nullptr;  // optional [ncta][16] globaltimer stamps (ZDC_FUSED_TRACE)
+  int B = 0, d = 0, nq = 0, nk = 0, Nh = 0, Nkv = 0, S_cap = 0;
+  int C = 0;                       // cluster size (CTAs per KV group)
+  int l2_prefetch = 7;             // bulk L2 prefetch of: 1 phase-1 weights past the ring, 2 cached rows, 4 W_O
+  float scale = 0.f;
+  // geometry (set by the launcher)
+  int nslot = 0, attn_warps = 0, tmem_cols = 0;
+};
+bool decode_cluster_supported(int B, int RK, int G);
+bool decode_cluster_layer_ok(int RK, int G);  // the layer gets a W_O decode copy
+// cluster size for N_kv groups (0 = the cluster kernel cannot hold every group at once)
+int decode_cluster_size(int B, int RK, int G, int Nkv, int d);
+cudaError_t launch_decode_cluster(const DecClusterArgs& a, int RK, cudaStream_t s);
+// tensor map of the W_O decode copy [Nkv*d][K3] in boxes of KB3 x 128 rows (swizzle = KB3 * 2 bytes)
+bool cluster_wo_tmap(CUtensorMap* tw, const uint16_t* wod, int Nkv, int d, int K3, int KB3);
+// W_QKV^T [n_qkv][d] -> the decode copy wqd (tiles of group g, k-block kb: rows (Q'_g | K'_g | V'_g)
+// x 64 K in the 128-byte-swizzled K-major image the tcgen05 A operand reads)
+cudaError_t launch_pack_qkv_decode(const uint16_t* wqkv_t, uint16_t* wqd, int d, int nq, int nk, int Nkv, int G,
+                                   int RK, cudaStream_t s);
+// W_O^T [d][ko_p] -> the group-major decode copy wod[g][n][j] = wo_t[n][g*K3 + j]
+cudaError_t launch_pack_wo_decode(const uint16_t* wo_t, uint16_t* wod, int d, int ko_p, int Nkv, int K3,
+                                  cudaStream_t s);
 
 // ---- weight packing (load time): f32/bf16 full-rank folded -> truncated, padded, bf16
 cudaError_t launch_pack_weights_bf16(const uint16_t* wq, const uint16_t* wk, const uint16_t* wv,

@@ -17,7 +17,7 @@ import zdc_synth as Z  # noqa: E402
 
 NAMES = {0: "kernel start", 13: "layer start", 1: "x staged", 2: "phase1 done", 3: "barrier1 out", 4: "phase2 done", 5: "barrier2 out",
          6: "merge done", 7: "end", 8: "prod: ph1 issued", 9: "prod: ph2 issued", 10: "prod: all issued",
-         11: "ph2 rows done", 12: "partials staged", 13: "layer start"}
+         11: "ph2 rows done / cl: ph3 done", 12: "partials staged", 13: "layer start", 14: "cl: after pdl wait"}
 
 
 def main():
@@ -27,8 +27,10 @@ def main():
     p.add_argument("--batch", type=int, default=1)
     p.add_argument("--steps", type=int, default=8)
     p.add_argument("--chain", action="store_true", help="one chained zdc_decode call per step")
+    p.add_argument("--mode", default="auto", help="zdc_decode_mode: auto / fused / cluster / separate")
     args = p.parse_args()
     dev = torch.device("cuda", 0)
+    zdc.decode_mode(args.mode)
     base = Z.dims_of(2)
     L, B, S = args.layers, args.batch, args.ctx
     dims = Z.Dims(L, base.d_model, base.n_heads, base.n_kv_heads, base.d_head)
