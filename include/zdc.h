@@ -246,7 +246,9 @@ zdc_status zdc_gemv_bf16(const uint16_t* w, const uint16_t* x, uint16_t* y, int3
  * projections, DSMEM exchanges, no grid barrier; needs r in {16, 32, 64, 128}, G r <= 256 and
  * d % 64 == 0; falls back to 1 where unsupported), 3 = separate kernels (GEMV / GEMM, split-K
  * attention, GEMV).  Returns the previous mode; -1 for an invalid mode.
- * Env ZDC_DECODE_MODE sets the initial mode. */
+ * Mode 2 must be selected before zdc_ctx_create: the cluster kernel streams decode copies of the
+ * weights (pre-tiled W_QKV, group-major W_O) that zdc_ctx_sizes then counts and zdc_load_folded
+ * fills.  Env ZDC_DECODE_MODE sets the initial mode. */
 int zdc_decode_mode(int mode);
 
 /* Number of kernels the last prefill / decode call enqueued (for bench.py's gpu_launches). */

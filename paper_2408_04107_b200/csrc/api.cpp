@@ -77,6 +77,9 @@ const char* zdc_last_error(void) { return t_err.c_str(); }
 const char* zdc_version(void) { return "zdc-b200 0.1 (sm_100a tcgen05)"; }
 int64_t zdc_kernel_launch_count(void) { return g_launches; }
 
+
+
+// ------------------------------------------------------------------ context
 static int g_decode_mode = getenv("ZDC_DECODE_MODE") ? atoi(getenv("ZDC_DECODE_MODE")) : 0;
 int zdc_decode_mode(int mode) {
   if (mode < 0 || mode > 3) return -1;
@@ -85,7 +88,6 @@ int zdc_decode_mode(int mode) {
   return old;
 }
 
-// ------------------------------------------------------------------ context
 zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t max_batch, int32_t max_seq,
                           zdc_ctx** out) {
   if (!dims || !plan || !out) return fail(ZDC_ERR_INVALID_ARG, "zdc_ctx_create: null argument");
@@ -167,7 +169,7 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
     woff = align_up(woff + static_cast<int64_t>(L.n_qkv) * d.d_model * 2, 256);
     L.w_o = woff;
     woff = align_up(woff + static_cast<int64_t>(d.d_model) * L.ko_p * 2, 256);
-    if (!L.split && decode_cluster_layer_ok(L.rk_p, d.n_heads / d.n_kv_heads)) {
+    if (g_decode_mode == 2 && !L.split && decode_cluster_layer_ok(L.rk_p, d.n_heads / d.n_kv_heads)) {
       // the group-major copy of W_O that the cluster decode kernel streams in contiguous tiles
       L.w_od = woff;
       woff = align_up(woff + static_cast<int64_t>(d.n_heads) * L.rv_p * d.d_model * 2, 256);

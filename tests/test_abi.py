@@ -67,11 +67,20 @@ def test_ctx_sizes_closed_form():
     wb, cb, sb = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
     assert L.zdc_ctx_sizes(h, ctypes.byref(wb), ctypes.byref(cb), ctypes.byref(sb)) == 0
     assert cb.value == 2 * 3 * 100 * 2 * (32 + 32) * 2 + 256  # + int32 lengths, 256-B aligned
-    # weights: [N_h r + N_kv (r + r)] x d  +  d x roundup(N_h r, 64)  +  the cluster decode
-    # kernel's copies: W_O group-major (N_h r x d) and W_QKV pre-tiled ([N_h r + N_kv (r + r)] x d), bf16
+    # weights: [N_h r + N_kv (r + r)] x d  +  d x roundup(N_h r, 64), bf16
     wqkv = (4 * 32 + 2 * 64) * 256 * 2
-    assert wb.value == 2 * (wqkv + 256 * 128 * 2 + 4 * 32 * 256 * 2 + wqkv)
+    assert wb.value == 2 * (wqkv + 256 * 128 * 2)
     L.zdc_ctx_destroy(h)
+    # decode mode 2 (cluster kernel) adds its decode copies: W_O group-major (N_h r x d) and W_QKV
+    # pre-tiled ([N_h r + N_kv (r + r)] x d)
+    old = L.zdc_decode_mode(2)
+    try:
+        assert L.zdc_ctx_create(ctypes.byref(D), ctypes.byref(P), 3, 100, ctypes.byref(h)) == 0
+        assert L.zdc_ctx_sizes(h, ctypes.byref(wb), ctypes.byref(cb), ctypes.byref(sb)) == 0
+        assert wb.value == 2 * (wqkv + 256 * 128 * 2 + 4 * 32 * 256 * 2 + wqkv)
+        L.zdc_ctx_destroy(h)
+    finally:
+        L.zdc_decode_mode(old)
 
 
 def test_unbound_ctx_calls_fail():
