@@ -20,6 +20,7 @@ N > 1: independent replicas (decode is "replicas only"; the c2 prefill fits one 
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import math
 import os
@@ -28,6 +29,8 @@ import subprocess
 import sys
 import threading
 import time
+
+import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -56,6 +59,8 @@ def parse():
                    help="decode step as 32 per-layer zdc_decode calls (same x per layer) or one chained call")
     p.add_argument("--decode-mode", default="auto", choices=["auto", "fused", "cluster", "separate"],
                    help="decode kernels for B <= 8 (zdc_decode_mode): auto = cluster layer-step when it fits")
+    p.add_argument("--configs", default="c3,c4",
+                   help="per-layer prefill/decode measurements of these configs at N = 1 ('' to skip)")
     p.add_argument("--sp-seq", type=int, default=32768, help="SP prefill prompt length (c5), run when N > 1")
     p.add_argument("--sp-layers", type=int, default=32)
     p.add_argument("--sp", action="store_true", help="also run the SP prefill at N = 1 (P = 1, no exchange)")
@@ -343,6 +348,131 @@ def sp_bench(args, zdc, torch, dist, rank, world, dev, stream):
     return out
 
 
+# ------------------------------------------------------------------------------------ c3 / c4 layers
+def config_bench(args, zdc, torch, dev, stream, cid, n_layers=4, T=16):
+    """Per-layer prefill and decode of config `cid` (3: Llama-2-13B shape, batch 32, prompt 1024,
+    token split r^i = 96 / r^u = 32 at g = 0.5 over one 4-layer group; 4: Llama-2-70B shape, GQA 8 KV
+    heads, batch 64, prompt 8192, r = 64) on `n_layers` layers with timing-only weights (the ideal
+    fold of SURVEY.md §8(d)), each layer called separately with the same x (as for c2).  Prefill:
+    algorithmic FLOP / time against the bf16 peak; decode: algorithmic bytes (weights at the plan
+    ranks + K'/V' at the realised per-token widths + append + x/y) per layer-step / time against
+    the HBM peak.  The whole-model figures scale the per-layer time to the config's layer count
+    (labelled extrapolated)."""
+    import zdc_synth as Z
+    cfg = Z.CONFIGS[cid]
+    full = cfg["dims"]
+    dims = Z.Dims(n_layers, full.d_model, full.n_heads, full.n_kv_heads, full.d_head)
+    d, nh, nkv, dh = dims.d_model, dims.n_heads, dims.n_kv_heads, dims.d_head
+    B, S, r = cfg["B"], cfg["S"], cfg["r"]
+    if cid == 3:
+        ru = cfg["r_u"]
+        plan = Z.plan_split(n_layers, r, ru, [list(range(n_layers))], [5000])
+    else:
+        ru = r
+        plan = Z.plan_uniform(n_layers, r)
+    ctx = zdc.Context(dims, plan, B, S + T + 4)
+    g = torch.Generator(device=dev).manual_seed(4321 + cid)
+    sv = torch.tensor([10.0 ** (-2.0 * j / (dh - 1)) for j in range(dh)], device=dev)
+    a = (4.0 * dh / float((sv ** 4).sum())) ** 0.25
+    bta = math.sqrt(dh / float((sv ** 2).sum()))
+    gam = math.sqrt(dh / (nh * float((sv ** 2).sum())))
+    for l in range(n_layers):
+        wq = (torch.randn(d, nh, dh, device=dev, generator=g) * (a * sv / math.sqrt(d))).reshape(d, nh * dh)
+        wk = (torch.randn(d, nkv, dh, device=dev, generator=g) * (a * sv / math.sqrt(d))).reshape(d, nkv * dh)
+        wv = (torch.randn(d, nkv, dh, device=dev, generator=g) * (bta * sv / math.sqrt(d))).reshape(d, nkv * dh)
+        wo = (torch.randn(nh, dh, d, device=dev, generator=g) * (gam * sv[:, None] / math.sqrt(d))).reshape(nh * dh, d)
+        ctx.load_folded_device(l, *[t.to(torch.bfloat16).contiguous() for t in (wq, wk, wv, wo)])
+        del wq, wk, wv, wo
+    x = torch.randn(B, S, d, device=dev, generator=g).to(torch.bfloat16)
+    y = torch.empty_like(x)
+    xd = torch.randn(T + 2, B, d, device=dev, generator=g).to(torch.bfloat16)
+    xb = torch.empty(B, d, device=dev, dtype=torch.bfloat16)
+    yb = torch.empty_like(xb)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+
+    def prefill(timed):
+        ctx.reset()
+        if timed:
+            ev[0].record(stream)
+        for l in range(n_layers):
+            ctx.prefill(x, y, l, l + 1)
+        if timed:
+            ev[1].record(stream)
+
+    def decode_steps(t0, n, timed):
+        if timed:
+            ev[2].record(stream)
+        for t in range(t0, t0 + n):
+            xb.copy_(xd[t])
+            for l in range(n_layers):
+                ctx.decode(xb, yb, l, l + 1)
+        if timed:
+            ev[3].record(stream)
+
+    prefill(False)                 # warm-up (kernel attributes)
+    decode_steps(0, 2, False)      # warm-up (decode graphs)
+    torch.cuda.synchronize()
+    prefill(True)
+    decode_steps(0, 2, False)
+    decode_steps(2, T, True)
+    torch.cuda.synchronize()
+    pre_ms = ev[0].elapsed_time(ev[1]) / n_layers
+    dec_us = ev[2].elapsed_time(ev[3]) * 1e3 / (T * n_layers)
+    per_class = None
+    if os.environ.get("ZDC_BENCH_CLASS_PROFILE"):  # diagnostics: per-kernel-class time of 2 eager steps
+        zdc.profile(True)
+        zdc.profile_read()
+        decode_steps(T + 2 - 2, 2, False)  # cache has room: S + T + 4 rows
+        per_class = {k: (round(v[0] / (2 * n_layers) * 1e3, 1), v[1]) for k, v in zdc.profile_read().items() if v[1]}
+        zdc.profile(False)
+    # algorithmic work (SURVEY.md §8(d)): unpadded ranks (multiples of 16 here: padding = 0)
+    nq, nkvr = nh * r, nkv * r
+    n_qkv = nq + 2 * nkvr
+    flop = 2.0 * B * S * d * n_qkv + 4.0 * r * nh * B * S * (S + 1) / 2 + 2.0 * B * S * nq * d
+    wbytes = (n_qkv * d + d * nq) * 2
+    wI, wU = 2 * nkv * r * 2, 2 * nkv * ru * 2  # bytes per cached token per layer (K' + V')
+    if cid == 3:
+        imp = np.zeros((B, ctx.cache_length(0)), dtype=np.uint8)
+        zdc._check(zdc.lib().zdc_cache_export(ctx.h, 0, None, None, imp.ctypes.data_as(ctypes.c_void_p), None,
+                                              ctypes.c_void_p(stream.cuda_stream)), "zdc_cache_export")
+        cum = np.cumsum(imp.astype(np.int64), axis=1)  # important tokens among the first j+1
+        kv = 0.0
+        for t in range(2, T + 2):
+            n_before = S + t  # cached rows the step-t query attends to (+ its own, appended)
+            ni = cum[:, n_before - 1]
+            kv += float((ni * wI + (n_before - ni) * wU).sum())
+        kv /= T
+        frac_imp_prompt = float(imp[:, :S].mean())
+        frac_imp_decode = float(imp[:, S:S + T + 2].mean())
+    else:
+        kv = float(B * (S + 2 + (T - 1) / 2.0) * wI)
+        frac_imp_prompt = frac_imp_decode = None
+    dbytes = wbytes + kv + B * wI + 2 * B * d * 2
+    peaks = load_peaks()
+    out = {
+        "workload": cfg["name"], "layers_measured": n_layers, "layers_model": full.n_layers, "batch": B,
+        "prompt": S, "rank": r, "rank_unimportant": ru if cid == 3 else None,
+        "prefill": {"ms_per_layer": round(pre_ms, 3), "flop_per_layer": flop,
+                    "achieved_tflops": round(flop / (pre_ms / 1e3) / 1e12, 1), "peak": peaks["tf"],
+                    "frac": round(flop / (pre_ms / 1e3) / 1e12 / peaks["tf"], 4),
+                    "tok_s_model_extrapolated": round(B * S / (pre_ms / 1e3 * full.n_layers), 1)},
+        "decode": {"us_per_layer_step": round(dec_us, 2), "bytes_per_layer_step": dbytes,
+                   "weight_bytes": wbytes, "kv_bytes_avg": kv,
+                   "achieved_gbs": round(dbytes / (dec_us / 1e6) / 1e9, 1), "peak": peaks["hbm"],
+                   "frac": round(dbytes / (dec_us / 1e6) / 1e9 / peaks["hbm"], 4), "steps_timed": T,
+                   "tok_s_model_extrapolated": round(B / (dec_us / 1e6 * full.n_layers), 1)},
+    }
+    if per_class:
+        out["decode"]["per_class_us_per_layer"] = per_class
+    if cid == 3:
+        out["realised_important_fraction"] = {"prompt": round(frac_imp_prompt, 4),
+                                              "decode": round(frac_imp_decode, 4), "g_bp": 5000}
+    ctx.close()
+    del x, y, xd
+    torch.cuda.empty_cache()
+    return out
+
+
 # ------------------------------------------------------------------------------------ zdc arm
 def run_zdc(args):
     import torch
@@ -562,6 +692,17 @@ def run_zdc(args):
     elif world == 1:
         sp = {"note": "the K'/V' exchange needs N > 1: bench.py --gpus N under torchrun (or --sp for P = 1)"}
 
+    # ---- per-layer measurements of the other configs (c3 token split, c4 GQA KV-bound decode)
+    other = None
+    if world == 1 and args.configs:
+        other = {}
+        for name in [c for c in args.configs.split(",") if c]:
+            log("config %s layers" % name)
+            try:
+                other[name] = config_bench(args, zdc, torch, dev, stream, int(name.lstrip("c")))
+            except Exception as e:  # reported, never hides the main line
+                other[name] = {"error": "%s: %s" % (type(e).__name__, e)}
+
     # ---- CPU baseline (oracle as it stands), rank 0 at N=1 only
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -595,7 +736,7 @@ def run_zdc(args):
                 "note": "whole decode layer-step inside the graph-replayed step: algorithmic bytes (packed "
                         "weights + K'/V' at the average context + x/y) / measured time per layer-step"},
             "clocks": clocks, "gpu_launches": kernels_per_step * args.steps,
-            "e2e": e2e, "cpu_baseline": cpu, "sp": sp,
+            "e2e": e2e, "cpu_baseline": cpu, "sp": sp, "other_configs": other,
         }
         print(json.dumps(out), flush=True)
     ctx.close()

@@ -694,7 +694,18 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
       a.rk1 = L.rku_p;
       a.rv1 = L.rvu_p;
     }
-    ZDC_CUDA_TRY(launch_decode_attention(a, s));
+    static const bool attn_tc_on = !(getenv("ZDC_DEC_ATTN_TC") && atoi(getenv("ZDC_DEC_ATTN_TC")) == 0);
+    cudaError_t ea = cudaErrorNotSupported;
+    if (attn_tc_on && !L.split && decode_attention_tc_supported(L.rk_p, L.rv_p, c->G)) {
+      // grouped-query heads: the tensor-core kernel (decode_attn_tc.cu)
+      DecodeAttnArgs at = a;
+      at.splits = decode_tc_splits(B, Nkv, c->max_seq);
+      ea = launch_decode_attention_tc(at, s);
+      if (ea != cudaSuccess && ea != cudaErrorNotSupported)
+        return fail(ZDC_ERR_CUDA, "decode attention (tensor cores) layer %d: %s", l, cudaGetErrorString(ea));
+      if (ea == cudaErrorNotSupported) cudaGetLastError();
+    }
+    if (ea != cudaSuccess) ZDC_CUDA_TRY(launch_decode_attention(a, s));
     if (L.split && is_rep) {
       g_prof_class = kProfOther;
       ZDC_CUDA_TRY(launch_classify(a.lse, Nh, c->importance_mode, reinterpret_cast<const float*>(c->cache + L.tau_off),

@@ -108,6 +108,11 @@ struct DecodeAttnArgs {
   int splits = 1;
 };
 cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t stream);
+// tcgen05 decode attention for grouped-query layers (decode_attn_tc.cu): uniform rank r in
+// {64, 128}, G in {2, 4, 8, 16}, device-side length (len_ptr); a.splits from decode_tc_splits
+bool decode_attention_tc_supported(int rk, int rv, int G);
+int decode_tc_splits(int B, int Nkv, int len);
+cudaError_t launch_decode_attention_tc(const DecodeAttnArgs& a, cudaStream_t stream);
 cudaError_t launch_decode2_partial(const DecodeAttnArgs& a, int width, const uint16_t* kp, const uint16_t* vp,
                                    int pool, int slot0, int nslots, cudaStream_t s);
 int decode2_splits(int B, int Nkv, int len, int width, int G);
