@@ -122,7 +122,7 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
   c->len.assign(d.n_layers, 0);
   c->sp_layer.assign(d.n_layers, 0);
   int64_t woff = 0, coff = 0;
-  int max_nq = 0, max_ko = 0, max_rv = 0, max_split_w = 0;
+  int max_nq = 0, max_ko = 0, max_rv = 0, max_split_w = 0, max_nqkv = 0;
   bool any_split = false;
   for (int l = 0; l < d.n_layers; ++l) {
     LayerInfo& L = c->layers[l];
@@ -208,6 +208,7 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
     }
     if (L.nq > max_nq) max_nq = L.nq;
     if (L.ko_p > max_ko) max_ko = L.ko_p;
+    if (L.n_qkv > max_nqkv) max_nqkv = L.n_qkv;
     if (L.rv_p > max_rv) max_rv = L.rv_p;
   }
   c->len_dev_off = coff;
@@ -230,6 +231,11 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
   s = align_up(s + 64, 256);
   c->s_ltab = s;  // fused decode layer table (DecLayer per layer), written at bind
   s = align_up(s + static_cast<int64_t>(d.n_layers) * static_cast<int64_t>(sizeof(DecLayer)), 256);
+  if (max_batch > 8) {  // split-K decode GEMMs (B > 8): f32 workspace [min(B,128)][max N] + tile counters
+    c->s_gsk = s;
+    s = align_up(s + static_cast<int64_t>(std::min(max_batch, 128)) * std::max(max_nqkv, d.d_model) * 4 + 1024 * 4,
+                 256);
+  }
   c->s_ybuf = s;  // cluster decode: y accumulator [8][d] f32 then 16 arrival counters, zero between launches
   s = align_up(s + static_cast<int64_t>(8) * d.d_model * 4 + 16 * 4, 256);
   if (any_split) {  // staged K'/V' of a split layer before packing, compaction indices, new-row staging
@@ -244,6 +250,7 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
     s = align_up(s + static_cast<int64_t>(max_batch) * d.n_kv_heads * max_split_w * 2 * 2, 256);
   }
   c->ldq = max_nq;
+  c->max_nqkv = max_nqkv;
   c->ldo = max_ko;
   c->scratch_bytes = s;
   *out = c;
@@ -514,6 +521,14 @@ zdc_status zdc_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, ui
   return ZDC_OK;
 }
 
+static void set_splitk_ws(zdc_ctx* c, Epilogue& e, int M, int N) {
+  e.ws = reinterpret_cast<float*>(c->scratch + c->s_gsk);
+  e.ws_cnt = reinterpret_cast<int*>(e.ws + static_cast<int64_t>(std::min(c->max_batch, 128)) *
+                                             std::max(c->max_nqkv, c->dims.d_model));
+  (void)M;
+  (void)N;
+}
+
 static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, uint16_t* y, int B,
                                  cudaStream_t s) {
   const int d = c->dims.d_model, Nh = c->dims.n_heads, Nkv = c->dims.n_kv_heads;
@@ -629,7 +644,10 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
     if (gemv_supported(B, d))
       ZDC_CUDA_TRY(launch_gemv(wqkv, xin, d, B, L.n_qkv, d, e1, s));
     else
+    {
+      if (c->s_gsk >= 0 && B <= 128) set_splitk_ws(c, e1, B, L.n_qkv);
       ZDC_CUDA_TRY(launch_gemm(xin, d, wqkv, d, B, L.n_qkv, d, e1, s));
+    }
     const LayerInfo& R = c->layers[L.rep];
     const bool is_rep = L.rep == l;
     if (L.split) {
@@ -729,7 +747,10 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
     if (gemv_supported(B, L.ko_p))
       ZDC_CUDA_TRY(launch_gemv(wo, a.o, L.ko_p, B, d, L.ko_p, e5, s));
     else
+    {
+      if (c->s_gsk >= 0 && B <= 128) set_splitk_ws(c, e5, B, d);
       ZDC_CUDA_TRY(launch_gemm(a.o, L.ko_p, wo, L.ko_p, B, d, L.ko_p, e5, s));
+    }
     g_prof_class = kProfOther;
   }
   return ZDC_OK;

@@ -45,7 +45,9 @@ struct zdc_ctx {
   int64_t s_cnt = 0;                                  // decode merge counters
   int64_t s_gbar = 0;                                 // fused decode grid barrier (monotonic counter)
   int64_t s_ltab = 0;                                 // fused decode layer table
-  int64_t s_ybuf = 0;                                 // cluster decode: f32 y accumulator [8][d] + counters [16]
+  int64_t s_ybuf = 0;
+  int64_t s_gsk = -1;                                 // split-K decode GEMM workspace (max_batch > 8)
+  int max_nqkv = 0;                                 // cluster decode: f32 y accumulator [8][d] + counters [16]
   int ldq = 0, ldo = 0;
   uint8_t* w = nullptr;
   uint8_t* cache = nullptr;

@@ -32,7 +32,8 @@ struct DTC {
   static constexpr int NCH = HD / 64;             // 64-element (128-byte swizzle) chunks of a row
   static constexpr uint32_t CHUNK = 128 * 128;    // one 128-row chunk
   static constexpr uint32_t TILE = CHUNK * NCH;   // 128 K' or V' rows
-  static constexpr int ST = HD == 64 ? 5 : 3;     // K and V stages
+  static constexpr int ST = HD == 64 ? 2 : 3;     // K and V stages
+  static constexpr int CPS = HD == 64 ? 2 : 1;    // CTAs per SM (two independent softmax->PV chains)
   static constexpr uint32_t OFF_K = 0;
   static constexpr uint32_t OFF_V = ST * TILE;
   static constexpr uint32_t OFF_Q = OFF_V + ST * TILE;  // [NCH][16 rows x 128 B]
@@ -46,6 +47,16 @@ struct DTC {
 };
 
 __device__ __forceinline__ void softmax_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// barrier of the 4 softmax warps that also ORs a predicate over their 128 threads
+__device__ __forceinline__ bool softmax_any(bool v) {
+  uint32_t r;
+  asm volatile(
+      "{\n .reg .pred p, q;\n setp.ne.u32 p, %1, 0;\n barrier.red.or.pred q, 1, 128, p;\n selp.u32 %0, 1, 0, q;\n}\n"
+      : "=r"(r)
+      : "r"(static_cast<uint32_t>(v))
+      : "memory");
+  return r != 0;
+}
 
 struct TcItem {
   int b, g, split, s0, n_keys, n_tiles;
@@ -54,7 +65,7 @@ struct TcItem {
 }  // namespace
 
 template <int HD, int G>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(192, DTC<HD>::CPS)
     decode_attn_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                           const __grid_constant__ CUtensorMap tv, const DecodeAttnArgs a) {
   using C = DTC<HD>;
@@ -231,27 +242,41 @@ __global__ void __launch_bounds__(192, 1)
         if (lane == 0) mbar_arrive(&s_free[buf]);
         const bool valid = j * 128 + t < it.n_keys;
         float sc[G];
+        bool need = false;
 #pragma unroll
         for (int q = 0; q < G; ++q) {
           sc[q] = valid ? __uint_as_float(sv[q]) * sl : -INFINITY;
-          float mx = sc[q];
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-          if (lane == 0) red_m[((ti & 1) * 4 + warp) * 16 + q] = mx;
+          need |= sc[q] > m_ref[q] + kLazyT;
         }
-        softmax_sync();
+        // fast path: no score of the tile exceeds the reference by more than 2^8 (one barrier with
+        // an OR); otherwise the exact tile maxima decide which references rise (lazy rescaling)
         bool any_raise = false;
         float alpha[G], p[G];
 #pragma unroll
+        for (int q = 0; q < G; ++q) alpha[q] = 1.f;
+        if (softmax_any(need)) {
+#pragma unroll
+          for (int q = 0; q < G; ++q) {
+            float mx = sc[q];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+            if (lane == 0) red_m[((ti & 1) * 4 + warp) * 16 + q] = mx;
+          }
+          softmax_sync();
+#pragma unroll
+          for (int q = 0; q < G; ++q) {
+            const float* rm = red_m + (ti & 1) * 64 + q;
+            const float tmax = fmaxf(fmaxf(rm[0], rm[16]), fmaxf(rm[32], rm[48]));
+            if (tmax > m_ref[q] + kLazyT) {
+              alpha[q] = exp2f(m_ref[q] - tmax);  // 0 on the first tile
+              m_ref[q] = tmax;
+              any_raise = true;
+            }
+          }
+        }
+#pragma unroll
         for (int q = 0; q < G; ++q) {
-          const float* rm = red_m + (ti & 1) * 64 + q;
-          const float tmax = fmaxf(fmaxf(rm[0], rm[16]), fmaxf(rm[32], rm[48]));
-          const bool raise = tmax > m_ref[q] + kLazyT;
-          const float m_new = raise ? tmax : m_ref[q];
-          alpha[q] = raise ? exp2f(m_ref[q] - m_new) : 1.f;  // 0 on the first tile
-          any_raise |= raise;
-          m_ref[q] = m_new;
-          const float mr = m_new == -INFINITY ? 0.f : m_new;
+          const float mr = m_ref[q] == -INFINITY ? 0.f : m_ref[q];
           p[q] = valid ? fast_exp2(sc[q] - mr) : 0.f;
           l_part[q] = l_part[q] * alpha[q] + p[q];
         }
@@ -373,7 +398,7 @@ __global__ void __launch_bounds__(192, 1)
 // splits per (b, g): the fewest that fill the persistent CTAs' last round to >= 90 % (each split
 // keeps >= 2 key tiles at the capacity bound)
 int decode_tc_splits(int B, int Nkv, int len) {
-  const int pairs = B * Nkv, nsm = num_sms();
+  const int pairs = B * Nkv, nsm = 2 * num_sms();  // resident CTAs at r = 64 (r = 128: a bound)
   const int max_s = std::max(1, std::min(64, (len + 255) / 256));
   for (int s = 1; s <= max_s; ++s) {
     const int items = pairs * s;
@@ -404,7 +429,7 @@ static cudaError_t launch_tc_t(const DecodeAttnArgs& a, cudaStream_t stream) {
   if (!make_tmap_2d(&tv, a.v, HD, kv_rows, HD * 2, 64, 128, 128)) return cudaErrorInvalidValue;
   const int n_items = a.B * a.Nkv * a.splits;
   prof_mark(stream, true, kProfAttnDecode);
-  cudaError_t e = launch_k(decode_attn_tc_kernel<HD, G>, dim3(std::min(n_items, num_sms())), dim3(192), C::SMEM,
+  cudaError_t e = launch_k(decode_attn_tc_kernel<HD, G>, dim3(std::min(n_items, C::CPS * num_sms())), dim3(192), C::SMEM,
                            stream, g_pdl && (g_pdl_mask & 2), tq, tk, tv, a);
   prof_mark(stream, false, kProfAttnDecode);
   ++g_launches;

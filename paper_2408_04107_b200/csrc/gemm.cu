@@ -165,11 +165,16 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int m_tiles = (M + C::BM - 1) / C::BM;
   const int n_tiles = (N + BN - 1) / BN;
   const int num_tiles = m_tiles * n_tiles;
   const int k_blocks = K / C::BK;
+  // work item w: output tile w % num_tiles, k-split w / num_tiles (k-blocks [kb0, kb1))
+  const int ks = epi.k_splits;
+  const int num_work = num_tiles * ks;
+  const int kpb = (k_blocks + ks - 1) / ks;
   const uint32_t warp = warp_id(), lane = lane_id();
   if (epi.len_inc && blockIdx.x == 0 && threadIdx.x == 0) *epi.len_inc += 1;
 
@@ -197,9 +202,11 @@ __global__ void __launch_bounds__(256, 1)
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
+        const int tile = w % num_tiles, sp = w / num_tiles;
         const int mb = tile % m_tiles, nb = tile / m_tiles;
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        const int kb1 = min(k_blocks, (sp + 1) * kpb);
+        for (int kb = sp * kpb; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           tma_load_2d(sA + stage * C::A_BYTES, &tma_a, &full[stage], kb * C::BK, mb * C::BM);
@@ -219,11 +226,12 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
+        const int sp = w / num_tiles, kb0 = sp * kpb, kb1 = min(k_blocks, kb0 + kpb);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
@@ -232,7 +240,7 @@ __global__ void __launch_bounds__(256, 1)
           for (int kk = 0; kk < C::BK / 16; ++kk) {
             const uint64_t ad = make_sdesc(a_addr + kk * 32, 16, 1024, kSw128);
             const uint64_t bd = make_sdesc(b_addr + kk * 32, 16, 1024, kSw128);
-            umma_bf16_ss(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+            umma_bf16_ss(d_tmem, ad, bd, idesc, (kb != kb0 || kk != 0) ? 1u : 0u);
           }
           umma_commit(&empty[stage]);  // frees the smem slot once these MMAs have read it
           if (++stage == C::STAGES) {
@@ -250,11 +258,64 @@ __global__ void __launch_bounds__(256, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
+      const int tile = w % num_tiles;
       const int mb = tile % m_tiles, nb = tile / m_tiles;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = mb * C::BM + q * 32 + lane;
+      if (ks > 1) {
+        // split-K: this split's partial tile into the f32 workspace (vector reductions at L2)
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(tmem_base + ((q * 32) << 16) + acc * BN + c, r);
+          tc_wait_ld();
+          const int n0 = nb * BN + c;
+          if (row < M && n0 < N) {
+            float* wrow = epi.ws + static_cast<int64_t>(row) * N;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int n = n0 + u * 4;
+              if (n + 4 <= N)
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(wrow + n), "f"(__uint_as_float(r[u * 4])),
+                             "f"(__uint_as_float(r[u * 4 + 1])), "f"(__uint_as_float(r[u * 4 + 2])),
+                             "f"(__uint_as_float(r[u * 4 + 3]))
+                             : "memory");
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        __threadfence();
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        if (warp == 4 && lane == 0) *s_last = atomicAdd(epi.ws_cnt + tile, 1) == ks - 1;
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        if (*s_last) {  // the last split: summed tile -> bf16 -> the epilogue's destination; reset
+          __threadfence();
+          if (row < M) {
+            float* wrow = epi.ws + static_cast<int64_t>(row) * N;
+            for (int n = nb * BN; n < min(N, nb * BN + BN); n += 8) {
+              if (n + 8 > N) break;
+              const float4 v0 = __ldcg(reinterpret_cast<const float4*>(wrow + n));
+              const float4 v1 = __ldcg(reinterpret_cast<const float4*>(wrow + n + 4));
+              uint4 val;
+              val.x = pack_bf16x2(v0.x, v0.y);
+              val.y = pack_bf16x2(v0.z, v0.w);
+              val.z = pack_bf16x2(v1.x, v1.y);
+              val.w = pack_bf16x2(v1.z, v1.w);
+              store_unit(epi, row, n, val);
+              __stcg(reinterpret_cast<float4*>(wrow + n), make_float4(0.f, 0.f, 0.f, 0.f));
+              __stcg(reinterpret_cast<float4*>(wrow + n + 4), make_float4(0.f, 0.f, 0.f, 0.f));
+            }
+          }
+          if (warp == 4 && lane == 0) epi.ws_cnt[tile] = 0;
+        }
+        asm volatile("bar.sync 2, 128;" ::: "memory");  // s_last is rewritten by the next item
+        continue;
+      }
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
@@ -300,7 +361,7 @@ static cudaError_t launch_gemm_bn(const CUtensorMap& ta, const CUtensorMap& tb, 
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int tiles = ((M + C::BM - 1) / C::BM) * ((N + BN - 1) / BN);
+  const int tiles = ((M + C::BM - 1) / C::BM) * ((N + BN - 1) / BN) * epi.k_splits;
   const int grid = tiles < num_sms() ? tiles : num_sms();
   prof_mark(stream, true, g_prof_class);
   gemm_bf16_tc_kernel<BN><<<grid, 256, C::SMEM, stream>>>(ta, tb, M, N, K, epi);
@@ -314,11 +375,20 @@ cudaError_t launch_gemm(const uint16_t* A, int64_t lda, const uint16_t* B, int64
   if (M <= 0 || N <= 0) return cudaSuccess;
   if (K % 64 != 0) return cudaErrorInvalidValue;
   const int BN = N > 128 ? 256 : 128;
+  Epilogue ep = epi;
+  ep.k_splits = 1;
+  if (epi.ws && epi.ws_cnt && M <= 128 && N % 8 == 0) {
+    // skinny M: split K so the weight stream spreads over the SMs (>= 4 k-blocks per split)
+    const int tiles = (N + BN - 1) / BN, kbs = K / 64;
+    int sk = num_sms() / tiles;
+    if (sk > kbs / 4) sk = kbs / 4;
+    if (sk > 1) ep.k_splits = sk;
+  }
   CUtensorMap ta, tb;
   if (!make_tmap_2d(&ta, A, K, M, lda * 2, 64, 128, 128)) return cudaErrorInvalidValue;
   if (!make_tmap_2d(&tb, B, K, N, ldb * 2, 64, BN, 128)) return cudaErrorInvalidValue;
-  return BN == 256 ? launch_gemm_bn<256>(ta, tb, M, N, K, epi, stream)
-                   : launch_gemm_bn<128>(ta, tb, M, N, K, epi, stream);
+  return BN == 256 ? launch_gemm_bn<256>(ta, tb, M, N, K, ep, stream)
+                   : launch_gemm_bn<128>(ta, tb, M, N, K, ep, stream);
 }
 
 }  // namespace zdc

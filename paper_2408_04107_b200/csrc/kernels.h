@@ -31,6 +31,12 @@ struct Epilogue {
   int64_t ldd = 0;
   QkvDest qkv;
   int* len_inc = nullptr;  // if set, the kernel increments *len_inc once (decode: advances the layer length)
+  // split-K for skinny M (M <= 128, few output tiles: decode at B > 8): fp32 workspace [M][N] and
+  // per-tile arrival counters, both zero between launches; the last split of a tile applies the
+  // epilogue above to the summed tile.  k_splits is chosen by launch_gemm when ws is set.
+  float* ws = nullptr;
+  int* ws_cnt = nullptr;
+  int k_splits = 1;
 };
 
 // ---- tensor maps (driver entry point resolved at runtime; no -lcuda link)
