@@ -349,7 +349,7 @@ def sp_bench(args, zdc, torch, dist, rank, world, dev, stream):
 
 
 # ------------------------------------------------------------------------------------ c3 / c4 layers
-def config_bench(args, zdc, torch, dev, stream, cid, n_layers=4, T=16):
+def config_bench(args, zdc, torch, dev, stream, cid, n_layers=4, T=48):
     """Per-layer prefill and decode of config `cid` (3: Llama-2-13B shape, batch 32, prompt 1024,
     token split r^i = 96 / r^u = 32 at g = 0.5 over one 4-layer group; 4: Llama-2-70B shape, GQA 8 KV
     heads, batch 64, prompt 8192, r = 64) on `n_layers` layers with timing-only weights (the ideal

@@ -27,22 +27,22 @@ constexpr float kLog2eT = 1.4426950408889634f;
 constexpr float kLn2T = 0.6931471805599453f;
 constexpr float kLazyT = 8.0f;  // log2 units
 
-template <int HD>
+template <int HD, int ST_ = 3>
 struct DTC {
   static constexpr int NCH = HD / 64;             // 64-element (128-byte swizzle) chunks of a row
   static constexpr uint32_t CHUNK = 128 * 128;    // one 128-row chunk
   static constexpr uint32_t TILE = CHUNK * NCH;   // 128 K' or V' rows
-  static constexpr int ST = HD == 64 ? 2 : 3;     // K and V stages
+  static constexpr int ST = ST_;                  // K and V stages
   static constexpr int CPS = HD == 64 ? 2 : 1;    // CTAs per SM (two independent softmax->PV chains)
-  static constexpr uint32_t OFF_K = 0;
-  static constexpr uint32_t OFF_V = ST * TILE;
-  static constexpr uint32_t OFF_Q = OFF_V + ST * TILE;  // [NCH][16 rows x 128 B]
+  // V stages first: the MN-major V' read at M = 128 (HD = 64) touches [stage + CHUNK, + 2 CHUNK),
+  // which for the last V stage is K stage 0 (read, never used): no slack needed
+  static constexpr uint32_t OFF_V = 0;
+  static constexpr uint32_t OFF_K = ST * TILE;
+  static constexpr uint32_t OFF_Q = OFF_K + ST * TILE;  // [NCH][16 rows x 128 B]
   static constexpr uint32_t OFF_P = OFF_Q + NCH * 2048;  // P^T [16][128 keys]: 2 chunks of 2 KB
   static constexpr uint32_t OFF_RED = OFF_P + 4096;      // [2][4 warps][16] maxima + [4][16] sums
   static constexpr uint32_t OFF_BAR = OFF_RED + 2048;
-  // the MN-major V' read at M = 128 touches [V stage + CHUNK, + 2 CHUNK) when HD = 64
-  static constexpr uint32_t END = OFF_BAR + 512 > OFF_V + ST * TILE + CHUNK ? OFF_BAR + 512 : OFF_V + ST * TILE + CHUNK;
-  static constexpr uint32_t SMEM = END + 1024;
+  static constexpr uint32_t SMEM = OFF_BAR + 512 + 1024;
   static constexpr uint32_t TMEM_COLS = 64;  // S^T double buffer [0, 32), O^T [32, 48)
 };
 
@@ -64,11 +64,11 @@ struct TcItem {
 
 }  // namespace
 
-template <int HD, int G>
-__global__ void __launch_bounds__(192, DTC<HD>::CPS)
+template <int HD, int G, int STG>
+__global__ void __launch_bounds__(192, DTC<HD, STG>::CPS)
     decode_attn_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                           const __grid_constant__ CUtensorMap tv, const DecodeAttnArgs a) {
-  using C = DTC<HD>;
+  using C = DTC<HD, STG>;
   constexpr int ST = C::ST;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -412,12 +412,12 @@ bool decode_attention_tc_supported(int rk, int rv, int G) {
   return rk == rv && (rk == 64 || rk == 128) && (G == 2 || G == 4 || G == 8 || G == 16);
 }
 
-template <int HD, int G>
-static cudaError_t launch_tc_t(const DecodeAttnArgs& a, cudaStream_t stream) {
-  using C = DTC<HD>;
+template <int HD, int G, int STG>
+static cudaError_t launch_tc_s(const DecodeAttnArgs& a, cudaStream_t stream) {
+  using C = DTC<HD, STG>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(decode_attn_tc_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(decode_attn_tc_kernel<HD, G, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(C::SMEM));
     if (e != cudaSuccess) return e;
     attr = true;
@@ -429,12 +429,19 @@ static cudaError_t launch_tc_t(const DecodeAttnArgs& a, cudaStream_t stream) {
   if (!make_tmap_2d(&tv, a.v, HD, kv_rows, HD * 2, 64, 128, 128)) return cudaErrorInvalidValue;
   const int n_items = a.B * a.Nkv * a.splits;
   prof_mark(stream, true, kProfAttnDecode);
-  cudaError_t e = launch_k(decode_attn_tc_kernel<HD, G>, dim3(std::min(n_items, C::CPS * num_sms())), dim3(192), C::SMEM,
+  cudaError_t e = launch_k(decode_attn_tc_kernel<HD, G, STG>, dim3(std::min(n_items, C::CPS * num_sms())), dim3(192), C::SMEM,
                            stream, g_pdl && (g_pdl_mask & 2), tq, tk, tv, a);
   prof_mark(stream, false, kProfAttnDecode);
   ++g_launches;
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+// stages per CTA (two CTAs per SM at r = 64): ZDC_TC_STAGES = 2 or 3 (default 3)
+static const int g_tc_stages = getenv("ZDC_TC_STAGES") ? atoi(getenv("ZDC_TC_STAGES")) : 3;
+template <int HD, int G>
+static cudaError_t launch_tc_t(const DecodeAttnArgs& a, cudaStream_t stream) {
+  return g_tc_stages == 2 ? launch_tc_s<HD, G, 2>(a, stream) : launch_tc_s<HD, G, 3>(a, stream);
 }
 
 cudaError_t launch_decode_attention_tc(const DecodeAttnArgs& a, cudaStream_t stream) {
