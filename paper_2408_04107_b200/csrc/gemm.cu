@@ -295,20 +295,38 @@ __global__ void __launch_bounds__(256, 1)
         asm volatile("bar.sync 2, 128;" ::: "memory");
         if (*s_last) {  // the last split: summed tile -> bf16 -> the epilogue's destination; reset
           __threadfence();
-          if (row < M) {
-            float* wrow = epi.ws + static_cast<int64_t>(row) * N;
-            for (int n = nb * BN; n < min(N, nb * BN + BN); n += 8) {
-              if (n + 8 > N) break;
-              const float4 v0 = __ldcg(reinterpret_cast<const float4*>(wrow + n));
-              const float4 v1 = __ldcg(reinterpret_cast<const float4*>(wrow + n + 4));
-              uint4 val;
-              val.x = pack_bf16x2(v0.x, v0.y);
-              val.y = pack_bf16x2(v0.z, v0.w);
-              val.z = pack_bf16x2(v1.x, v1.y);
-              val.w = pack_bf16x2(v1.z, v1.w);
-              store_unit(epi, row, n, val);
-              __stcg(reinterpret_cast<float4*>(wrow + n), make_float4(0.f, 0.f, 0.f, 0.f));
-              __stcg(reinterpret_cast<float4*>(wrow + n + 4), make_float4(0.f, 0.f, 0.f, 0.f));
+          // 8-column units of the tile's valid rows, spread over the 128 epilogue threads with four
+          // independent L2 round trips in flight per thread (a row per thread serialises ~BN/8 of them)
+          const int et = (warp - 4) * 32 + lane;
+          const int r0 = mb * C::BM, rows = min(C::BM, M - r0);
+          const int c0 = nb * BN, cols = min(BN, N - c0) / 8;
+          const int units = rows * cols;
+          for (int u0 = 0; u0 < units; u0 += 4 * 128) {
+            float4 v[4][2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int u = u0 + i * 128 + et;
+              if (u < units) {
+                const float* src = epi.ws + static_cast<int64_t>(r0 + u / cols) * N + c0 + (u % cols) * 8;
+                v[i][0] = __ldcg(reinterpret_cast<const float4*>(src));
+                v[i][1] = __ldcg(reinterpret_cast<const float4*>(src + 4));
+              }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int u = u0 + i * 128 + et;
+              if (u < units) {
+                const int rr = r0 + u / cols, n = c0 + (u % cols) * 8;
+                uint4 val;
+                val.x = pack_bf16x2(v[i][0].x, v[i][0].y);
+                val.y = pack_bf16x2(v[i][0].z, v[i][0].w);
+                val.z = pack_bf16x2(v[i][1].x, v[i][1].y);
+                val.w = pack_bf16x2(v[i][1].z, v[i][1].w);
+                store_unit(epi, rr, n, val);
+                float* dst = epi.ws + static_cast<int64_t>(rr) * N + n;
+                __stcg(reinterpret_cast<float4*>(dst), make_float4(0.f, 0.f, 0.f, 0.f));
+                __stcg(reinterpret_cast<float4*>(dst + 4), make_float4(0.f, 0.f, 0.f, 0.f));
+              }
             }
           }
           if (warp == 4 && lane == 0) epi.ws_cnt[tile] = 0;
