@@ -646,6 +646,7 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
     else
     {
       if (c->s_gsk >= 0 && B <= 128) set_splitk_ws(c, e1, B, L.n_qkv);
+      e1.pdl = 1;
       ZDC_CUDA_TRY(launch_gemm(xin, d, wqkv, d, B, L.n_qkv, d, e1, s));
     }
     const LayerInfo& R = c->layers[L.rep];
@@ -749,6 +750,7 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
     else
     {
       if (c->s_gsk >= 0 && B <= 128) set_splitk_ws(c, e5, B, d);
+      e5.pdl = 1;
       ZDC_CUDA_TRY(launch_gemm(a.o, L.ko_p, wo, L.ko_p, B, d, L.ko_p, e5, s));
     }
     g_prof_class = kProfOther;

@@ -578,7 +578,10 @@ static cudaError_t launch_partial(const DecodeAttnArgs& a, int width, const uint
 
 // v2 (decode_attn2.cu) is opt-in (ZDC_DEC_ATTN_V2=1): measured 12.3 us vs 11.3 us for v1 at the
 // c2 shape in round 1 (profiles/r01/NOTES.md)
-static const bool g_dec_attn_v2 = getenv("ZDC_DEC_ATTN_V2") != nullptr;
+// v2 (decode_attn2.cu) is the default for the separate-kernel decode path (B > 8, token-split
+// layers): 8-warp pipelined CTAs, ~30 % faster than v1 at config 3 (profiles/r01/NOTES.md);
+// ZDC_DEC_ATTN_V2=0 selects v1
+static const bool g_dec_attn_v2 = !(getenv("ZDC_DEC_ATTN_V2") && atoi(getenv("ZDC_DEC_ATTN_V2")) == 0);
 static bool v2_width(int w) { return w == 32 || w == 64 || w == 96 || w == 128; }
 
 cudaError_t launch_decode_attention(const DecodeAttnArgs& a_in, cudaStream_t stream) {

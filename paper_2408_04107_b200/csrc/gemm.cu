@@ -176,7 +176,6 @@ __global__ void __launch_bounds__(256, 1)
   const int num_work = num_tiles * ks;
   const int kpb = (k_blocks + ks - 1) / ks;
   const uint32_t warp = warp_id(), lane = lane_id();
-  if (epi.len_inc && blockIdx.x == 0 && threadIdx.x == 0) *epi.len_inc += 1;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tma_a);
@@ -197,16 +196,39 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  // Launched with programmatic dependent launch (decode): everything that reads the predecessor's
+  // output waits for it; the producer first requests the weight (B) tiles of the ring's first
+  // stages, which do not depend on it (griddepcontrol.wait is a no-op without PDL).
+  if (warp != 0) pdl_wait();
+  if (epi.len_inc && blockIdx.x == 0 && threadIdx.x == 4 * 32) *epi.len_inc += 1;
   if (warp == 0) {
     // ---------------- TMA producer
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
+      int issued = 0;
+      bool waited = false;
       for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
         const int tile = w % num_tiles, sp = w / num_tiles;
         const int mb = tile % m_tiles, nb = tile / m_tiles;
         const int kb1 = min(k_blocks, (sp + 1) * kpb);
-        for (int kb = sp * kpb; kb < kb1; ++kb) {
+        if (!waited && w == static_cast<int>(blockIdx.x)) {
+          // prologue: B of the first stages, then the dependency wait, then their A
+          const int n0 = max(0, min(C::STAGES, kb1 - sp * kpb));
+          for (int i = 0; i < n0; ++i) {
+            mbar_arrive_expect_tx(&full[i], C::STAGE_BYTES);
+            tma_load_2d(sB + i * C::B_BYTES, &tma_b, &full[i], (sp * kpb + i) * C::BK, nb * BN);
+          }
+          pdl_wait();
+          pdl_trigger();
+          for (int i = 0; i < n0; ++i)
+            tma_load_2d(sA + i * C::A_BYTES, &tma_a, &full[i], (sp * kpb + i) * C::BK, mb * C::BM);
+          issued = n0;
+          waited = true;
+          stage = n0 % C::STAGES;
+          phase = n0 == C::STAGES ? 1u : 0u;
+        }
+        for (int kb = sp * kpb + issued; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           tma_load_2d(sA + stage * C::A_BYTES, &tma_a, &full[stage], kb * C::BK, mb * C::BM);
@@ -216,7 +238,9 @@ __global__ void __launch_bounds__(256, 1)
             phase ^= 1;
           }
         }
+        issued = 0;
       }
+      if (!waited) pdl_wait();
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer
@@ -382,8 +406,10 @@ static cudaError_t launch_gemm_bn(const CUtensorMap& ta, const CUtensorMap& tb, 
   const int tiles = ((M + C::BM - 1) / C::BM) * ((N + BN - 1) / BN) * epi.k_splits;
   const int grid = tiles < num_sms() ? tiles : num_sms();
   prof_mark(stream, true, g_prof_class);
-  gemm_bf16_tc_kernel<BN><<<grid, 256, C::SMEM, stream>>>(ta, tb, M, N, K, epi);
+  cudaError_t e = launch_k(gemm_bf16_tc_kernel<BN>, dim3(grid), dim3(256), C::SMEM, stream,
+                           epi.pdl && g_pdl && (g_pdl_mask & 1), ta, tb, M, N, K, epi);
   prof_mark(stream, false, g_prof_class);
+  if (e != cudaSuccess) return e;
   ++g_launches;
   return cudaGetLastError();
 }
@@ -400,7 +426,10 @@ cudaError_t launch_gemm(const uint16_t* A, int64_t lda, const uint16_t* B, int64
     const int tiles = (N + BN - 1) / BN, kbs = K / 64;
     int sk = num_sms() / tiles;
     if (sk > kbs / 4) sk = kbs / 4;
-    if (sk > 1) ep.k_splits = sk;
+    if (sk > 1) {
+      const int kpb = (kbs + sk - 1) / sk;
+      ep.k_splits = (kbs + kpb - 1) / kpb;  // every split keeps >= 1 k-block
+    }
   }
   CUtensorMap ta, tb;
   if (!make_tmap_2d(&ta, A, K, M, lda * 2, 64, 128, 128)) return cudaErrorInvalidValue;

@@ -37,6 +37,7 @@ struct Epilogue {
   float* ws = nullptr;
   int* ws_cnt = nullptr;
   int k_splits = 1;
+  int pdl = 0;  // launch with programmatic dependent launch (decode chains)
 };
 
 // ---- tensor maps (driver entry point resolved at runtime; no -lcuda link)
