@@ -18,7 +18,8 @@ __all__ = ["ZdcError", "lib", "lib_path", "Dims", "Plan", "Context", "fold_weigh
            "sp_positions", "EXPORTED_SYMBOLS", "last_launch_count", "decode_mode"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libzdc.so")
+# ZDC_LIB_PATH: an alternative in-tree build of the same library (same-box A/B of kernel variants)
+_LIB_PATH = os.environ.get("ZDC_LIB_PATH") or os.path.join(_HERE, "libzdc.so")
 _lib = None
 
 ZDC_STATUS = {0: "ZDC_OK", -1: "ZDC_ERR_INVALID_ARG", -2: "ZDC_ERR_SHAPE", -3: "ZDC_ERR_NOT_ORTHONORMAL",
