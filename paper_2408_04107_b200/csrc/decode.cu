@@ -264,7 +264,7 @@ template <int RK, int RV, int G>
 __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs a, const uint16_t* __restrict__ kp,
                                                            const uint16_t* __restrict__ vp, int pool, int slot0,
                                                            int nslots) {
-  constexpr int UK = RK / 8, UKP = pow2_at_least(UK), RPW = 32 / UKP;   // lanes per K' row (padded)
+  constexpr int UK = RK / 8;                                            // 16-byte chunks per K' row
   constexpr int UV = RV / 8, UVP = pow2_at_least(UV), RPWV = 32 / UVP;  // lanes per V' row (padded)
   __shared__ float sc[G][kMaxChunk];
   __shared__ float red[4][G][RV];

@@ -8,10 +8,11 @@
 //   S^T[128 keys][16]  = K'[128 keys][r] · Q'_g[16][r]^T         (rows G..15 of Q'_g unused)
 //   O^T[128][16]      += V'^T[r (M; rows >= r unused)][128 keys] · P^T[128 keys][16]
 // with K' read K-major and V' MN-major straight from the cache layout (TMA, 128-byte swizzle),
-// FP32 accumulators in TMEM.  Softmax: one key per thread (warps 0-3 own the 128 TMEM lanes), a
-// per-tile cross-warp max per query head, lazy rescaling (the reference max only moves when a tile
-// exceeds it by more than 2^8, reading c20), P rounded to bf16 before PV with l taken from
-// the unrounded P.  Splits of one (b, g) are LSE-merged by the last CTA to finish (no combine
+// FP32 accumulators in TMEM.  Softmax: one key per thread (warps 0-3 own the 128 TMEM lanes) with
+// lazy rescaling (the reference max only moves when a tile exceeds it by more than 2^8, DESIGN.md
+// reading c20): a tile normally costs one barrier that ORs "some score exceeds the reference"; only
+// then are the exact per-head tile maxima exchanged.  P is rounded to bf16 before PV with l taken
+// from the unrounded P.  Two CTAs per SM (r = 64) keep two softmax -> PV chains in flight.  Splits of one (b, g) are LSE-merged by the last CTA to finish (no combine
 // launch).  Persistent CTAs take items round-robin.  Warps: 0-3 softmax, 4 TMA producer, 5 MMA.
 #include "common.cuh"
 #include "kernels.h"
@@ -220,7 +221,6 @@ __global__ void __launch_bounds__(192, DTC<HD, STG>::CPS)
     const int t = static_cast<int>(warp * 32 + lane);
     const uint32_t lane_base = (warp * 32) << 16;
     const float sl = a.scale * kLog2eT;
-    const uint32_t p_base = smem_u32(smem + C::OFF_P);
     int gt = 0;
     for (int k = blockIdx.x; k < n_items; k += gridDim.x) {
       const TcItem it = item_at(k);
@@ -301,7 +301,6 @@ __global__ void __launch_bounds__(192, DTC<HD, STG>::CPS)
           const uint32_t byte = static_cast<uint32_t>(q) * 128 + static_cast<uint32_t>(t & 63) * 2;
           *reinterpret_cast<uint16_t*>(pb + (byte ^ (((byte >> 7) & 7) << 4))) = f32_to_bf16_bits(p[q]);
         }
-        (void)p_base;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
         __syncwarp();

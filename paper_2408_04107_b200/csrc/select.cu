@@ -19,7 +19,6 @@
 
 namespace zdc {
 
-static constexpr float kLog2eS = 1.4426950408889634f;
 
 // ------------------------------------------------------------------ importance
 __global__ void importance_kernel(const float* __restrict__ lse, int T, int Nh, int B, int t0, int mode,
