@@ -204,6 +204,12 @@ zdc_status zdc_sp_positions(int32_t S_total, int32_t world, int32_t rank, int32_
 zdc_status zdc_cache_export(const zdc_ctx* ctx, int32_t layer, float* k, float* v,
                             uint8_t* is_important, float* tau, void* stream);
 zdc_status zdc_cache_length(const zdc_ctx* ctx, int32_t layer, int32_t* len);
+/* The cache lengths live on the device (decode kernels advance them, so one decode graph serves
+ * every position); the host keeps a copy for argument checks and the inspection calls, advanced by
+ * each zdc_prefill / zdc_decode call.  A caller that replays zdc_decode calls inside its OWN captured
+ * CUDA graph calls zdc_cache_sync afterwards: it copies the device lengths back (synchronises
+ * `stream`).  ZDC_ERR_STATE if the ctx is not bound. */
+zdc_status zdc_cache_sync(zdc_ctx* ctx, void* stream);
 /* Importance scores (reading c9: log of sum_h sum_{k<=t} exp(s_k^h), f32 as computed on the GPU)
  * of every cached token of a representative layer of a split group: scores [B][len], host. */
 zdc_status zdc_scores_export(const zdc_ctx* ctx, int32_t layer, float* scores, void* stream);

@@ -30,7 +30,7 @@ EXPORTED_SYMBOLS = ["zdc_last_error", "zdc_version", "zdc_fold_weights", "zdc_ct
                     "zdc_ctx_bind", "zdc_ctx_destroy", "zdc_load_folded", "zdc_load_folded_device",
                     "zdc_prefill", "zdc_decode", "zdc_comm_unique_id", "zdc_comm_init",
                     "zdc_sp_set_exchange_hook", "zdc_sp_prefill", "zdc_sp_positions",
-                    "zdc_cache_export", "zdc_cache_length", "zdc_scores_export", "zdc_cache_reset", "zdc_last_lse",
+                    "zdc_cache_export", "zdc_cache_length", "zdc_cache_sync", "zdc_scores_export", "zdc_cache_reset", "zdc_last_lse",
                     "zdc_gemm_bf16", "zdc_gemv_bf16", "zdc_prefill_attention_bf16",
                     "zdc_decode_attention_workspace", "zdc_decode_attention_bf16",
                     "zdc_kernel_launch_count", "zdc_profile", "zdc_profile_read", "zdc_trace_read",
@@ -97,6 +97,7 @@ def lib():
             "zdc_sp_positions": ([I32, I32, I32, I32, ctypes.POINTER(I32)], I32),
             "zdc_cache_export": ([P, I32, P, P, P, P, P], I32),
             "zdc_cache_length": ([P, I32, ctypes.POINTER(I32)], I32),
+            "zdc_cache_sync": ([P, P], I32),
             "zdc_scores_export": ([P, I32, P, P], I32),
             "zdc_cache_reset": ([P, P], I32),
             "zdc_last_lse": ([P, I32, P, P], I32),
@@ -336,6 +337,11 @@ class Context:
         n = ctypes.c_int32()
         _check(lib().zdc_cache_length(self.h, layer, ctypes.byref(n)), "zdc_cache_length")
         return n.value
+
+    def cache_sync(self, stream=None):
+        """Refresh the host copy of the cache lengths from the device (after replaying zdc_decode
+        calls inside a caller-captured CUDA graph)."""
+        _check(lib().zdc_cache_sync(self.h, ctypes.c_void_p(_stream(stream))), "zdc_cache_sync")
 
     def cache_export(self, layer: int, B: int, stream=None):
         length = self.cache_length(layer)

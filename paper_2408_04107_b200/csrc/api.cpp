@@ -827,6 +827,17 @@ zdc_status zdc_cache_length(const zdc_ctx* c, int32_t layer, int32_t* len) {
   return ZDC_OK;
 }
 
+zdc_status zdc_cache_sync(zdc_ctx* c, void* stream) {
+  if (!c) return fail(ZDC_ERR_INVALID_ARG, "zdc_cache_sync: null ctx");
+  if (!c->cache) return fail(ZDC_ERR_STATE, "zdc_cache_sync: ctx not bound");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<int> h(c->dims.n_layers);
+  ZDC_CUDA_TRY(cudaMemcpyAsync(h.data(), c->len_dev(), h.size() * 4, cudaMemcpyDeviceToHost, s));
+  ZDC_CUDA_TRY(cudaStreamSynchronize(s));
+  for (int l = 0; l < c->dims.n_layers; ++l) c->len[l] = h[l];
+  return ZDC_OK;
+}
+
 zdc_status zdc_cache_reset(zdc_ctx* c, void* stream) {
   if (!c) return fail(ZDC_ERR_INVALID_ARG, "zdc_cache_reset: null ctx");
   if (!c->cache) return fail(ZDC_ERR_STATE, "zdc_cache_reset: ctx not bound");

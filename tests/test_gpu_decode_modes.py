@@ -123,3 +123,38 @@ def test_decode_cluster_graph_layers(mode):
     s.synchronize()
     assert normwise(np.stack([from_dev(v) for v in ys], 1), want) <= TOL
     ctx.close()
+
+
+@pytest.mark.parametrize("mode", ["auto"], indirect=True)
+def test_decode_in_caller_graph_and_cache_sync(mode):
+    """zdc_decode captured inside the CALLER's CUDA graph and replayed per step (device-side cache
+    lengths make one graph valid at every position): rows equal the oracle's, and after
+    zdc_cache_sync the host lengths agree with the device (P7)."""
+    dims = Dims(2, 256, 4, 4, 64)
+    plan = plan_uniform(2, 32)
+    _, folded = fold_stack(dims, 1, n_calib=256)
+    T = 12
+    x = Z.prompt(dims, 1, 2, T, seed=24)
+    ctx = make_context(dims, plan, folded, 2, T + 2)
+    s = torch.cuda.Stream()
+    xb = torch.empty(2, 256, device="cuda", dtype=torch.bfloat16)
+    yb = torch.empty_like(xb)
+    ys = []
+    with torch.cuda.stream(s):
+        xb.copy_(to_dev_bf16(x[:, 0]))
+        ctx.decode(xb, yb, 0, 2)  # eager first step (also warms the library)
+        ys.append(yb.clone())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            ctx.decode(xb, yb, 0, 2)
+        for t in range(1, T):
+            xb.copy_(to_dev_bf16(x[:, t]))
+            g.replay()
+            ys.append(yb.clone())
+    s.synchronize()
+    got = np.stack([from_dev(v) for v in ys], axis=1)
+    want = O.OracleModel(dims, plan, folded, faithful=True).prefill(x)
+    assert normwise(got, want) <= TOL
+    ctx.cache_sync(s)
+    assert ctx.cache_length(0) == T and ctx.cache_length(1) == T
+    ctx.close()
