@@ -87,13 +87,13 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, dev: int):
-        self.dev, self.proc, self.lines = dev, None, []
+    def __init__(self, dev: int, period_ms: int = 200):
+        self.dev, self.proc, self.lines, self.period = dev, None, [], period_ms
 
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
-                                          "-lms", "200", "-i", str(self.dev)], stdout=subprocess.PIPE,
+                                          "-lms", str(self.period), "-i", str(self.dev)], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -414,6 +414,11 @@ def config_bench(args, zdc, torch, dev, stream, cid, n_layers=4, T=48):
     torch.cuda.synchronize()
     prefill(True)
     decode_steps(0, 2, False)
+    torch.cuda.synchronize()
+    # Decode is timed in its own power regime: the max-power prefill GEMMs just before leave this
+    # power-capped box at sw_power_cap with SM clocks of ~800-950 MHz for a while, which would
+    # otherwise bleed into the decode window (profiles/r01/NOTES.md); clocks are sampled during it.
+    time.sleep(0.5)
     # one decode step (the n_layers per-layer calls) captured as one CUDA graph, as for c2; the
     # device-side cache lengths make it replayable at every position
     g_step = torch.cuda.CUDAGraph()
@@ -421,12 +426,16 @@ def config_bench(args, zdc, torch, dev, stream, cid, n_layers=4, T=48):
         for l in range(n_layers):
             ctx.decode(xb, yb, l, l + 1)
     torch.cuda.synchronize()
+    clk = ClockSampler(dev.index if dev.index is not None else 0, period_ms=20)
+    clk.start()
+    time.sleep(0.1)
     ev[2].record(stream)
     for t in range(2, T + 2):
         xb.copy_(xd[t])
         g_step.replay()
     ev[3].record(stream)
     torch.cuda.synchronize()
+    dec_clocks = clk.stop()
     ctx.cache_sync(stream)  # the replays advanced the device lengths only
     pre_ms = ev[0].elapsed_time(ev[1]) / n_layers
     dec_us = ev[2].elapsed_time(ev[3]) * 1e3 / (T * n_layers)
@@ -467,12 +476,16 @@ def config_bench(args, zdc, torch, dev, stream, cid, n_layers=4, T=48):
         "prefill": {"ms_per_layer": round(pre_ms, 3), "flop_per_layer": flop,
                     "achieved_tflops": round(flop / (pre_ms / 1e3) / 1e12, 1), "peak": peaks["tf"],
                     "frac": round(flop / (pre_ms / 1e3) / 1e12 / peaks["tf"], 4),
+                    # a long region of back-to-back GEMMs: the sustained bf16 peak is the roofline
+                    "peak_sustained": peaks["tf_sus"],
+                    "frac_sustained": round(flop / (pre_ms / 1e3) / 1e12 / peaks["tf_sus"], 4),
                     "tok_s_model_extrapolated": round(B * S / (pre_ms / 1e3 * full.n_layers), 1)},
         "decode": {"us_per_layer_step": round(dec_us, 2), "bytes_per_layer_step": dbytes,
                    "weight_bytes": wbytes, "kv_bytes_avg": kv,
                    "achieved_gbs": round(dbytes / (dec_us / 1e6) / 1e9, 1), "peak": peaks["hbm"],
                    "frac": round(dbytes / (dec_us / 1e6) / 1e9 / peaks["hbm"], 4), "steps_timed": T,
-                   "tok_s_model_extrapolated": round(B / (dec_us / 1e6 * full.n_layers), 1)},
+                   "tok_s_model_extrapolated": round(B / (dec_us / 1e6 * full.n_layers), 1),
+                   "clocks": dec_clocks, "timing": "one CUDA graph per decode step, after a 0.5 s idle gap"},
     }
     if per_class:
         out["decode"]["per_class_us_per_layer"] = per_class
