@@ -25,6 +25,22 @@ namespace zdc {
 static constexpr float kLog2e4 = 1.4426950408889634f;
 static constexpr float kLn2_4 = 0.6931471805599453f;
 static constexpr float kLazyRescale = 8.0f;  // log2 units
+// P in tensor memory (as in FlashAttention-4): the softmax stores P (bf16 pairs per 32-bit column)
+// with tcgen05.st and the PV MMA reads its A operand from TMEM, instead of a 16 KB shared-memory
+// write + proxy fence per tile.  Fits the 512 TMEM columns for r <= 64.
+#ifndef ZDC_TMEM_P
+#define ZDC_TMEM_P 1
+#endif
+
+// D[tmem] (+)= A[tmem] * B[smem] (A: M = 128 lanes x K packed two bf16 per column)
+__device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 
 template <int HD>
 struct Attn4Cfg {
@@ -47,6 +63,8 @@ struct Attn4Cfg {
   static constexpr bool OK = 2 * TILE + 2 * STAGES * TILE + 2 * P_BYTES <= budget;
   static constexpr uint32_t TMEM_COLS = 512;  // S_a [0,128) S_b [128,256) O_a [256,+HD) O_b [256+HD,+HD)
   static constexpr uint32_t O_COL = 256;
+  static constexpr bool TP = ZDC_TMEM_P && O_COL + 2 * HD + 2 * 64 <= TMEM_COLS;  // P_a, P_b: 64 columns each
+  static constexpr uint32_t P_COL = O_COL + 2 * HD;
 };
 
 __device__ __forceinline__ void sts128_4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
@@ -230,9 +248,14 @@ __global__ void __launch_bounds__(352, 1)
         const uint32_t v_addr = smem_u32(smem + C::OFF_V + s * C::TILE);
 #pragma unroll
         for (int kk = 0; kk < C::BN / 16; ++kk) {
-          const uint64_t ad = make_sdesc(p_addr + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, kSw128);
           const uint64_t bd = make_sdesc(v_addr + kk * 16 * C::SWB, C::CHUNK, 8 * C::SWB, C::LAYOUT);
-          umma_bf16_ss(tmem + C::O_COL + t * HD, ad, bd, idesc_o, (!first || kk != 0) ? 1u : 0u);
+          if constexpr (C::TP) {
+            umma_bf16_ts(tmem + C::O_COL + t * HD, tmem + C::P_COL + t * 64 + kk * 8, bd, idesc_o,
+                         (!first || kk != 0) ? 1u : 0u);
+          } else {
+            const uint64_t ad = make_sdesc(p_addr + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, kSw128);
+            umma_bf16_ss(tmem + C::O_COL + t * HD, ad, bd, idesc_o, (!first || kk != 0) ? 1u : 0u);
+          }
         }
         umma_commit(&pv_done[t]);
         ++cp[t];
@@ -333,14 +356,26 @@ __global__ void __launch_bounds__(352, 1)
             tc_wait_st();
           }
         }
-        // P row -> shared memory, K-major 128B swizzle: keys [0,64) in chunk 0, [64,128) in chunk 1
+        if constexpr (C::TP) {
+          // P row -> TMEM columns [P_COL + 64 t, +64): column j = keys 2j (low half), 2j+1
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int c = u >> 2, e = (u & 3) * 4;  // 8 keys per 16-byte unit: sv[c][e..e+3]
-          sts128_4(p_base + (u >> 3) * 16384 + sw128_off(r, u & 7), sv[c][e], sv[c][e + 1], sv[c][e + 2],
-                   sv[c][e + 3]);
+          for (int c = 0; c < 4; ++c) {
+            uint32_t pv[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) pv[e] = sv[c][e];
+            tmem_st16(tmem + lane_base + C::P_COL + t * 64 + c * 16, pv);
+          }
+          tc_wait_st();
+        } else {
+          // P row -> shared memory, K-major 128B swizzle: keys [0,64) in chunk 0, [64,128) in chunk 1
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const int c = u >> 2, e = (u & 3) * 4;  // 8 keys per 16-byte unit: sv[c][e..e+3]
+            sts128_4(p_base + (u >> 3) * 16384 + sw128_off(r, u & 7), sv[c][e], sv[c][e + 1], sv[c][e + 2],
+                     sv[c][e + 3]);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[t]);
