@@ -447,6 +447,7 @@ zdc_status zdc_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, ui
       e1.qkv.k = ks;
       e1.qkv.v = vs;
     }
+    e1.pdl = 1;  // PDL: the weight tiles of the first stages stream before the dependency wait
     g_prof_class = kProfGemmQkv;
     ZDC_CUDA_TRY(launch_gemm(xin, d, reinterpret_cast<const uint16_t*>(c->w + L.w_qkv), d, M, L.n_qkv, d, e1, s));
     const LayerInfo& R = c->layers[L.rep];
@@ -508,6 +509,7 @@ zdc_status zdc_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, ui
     e5.mode = 0;
     e5.d = y;
     e5.ldd = d;
+    e5.pdl = 1;
     g_prof_class = kProfGemmO;
     ZDC_CUDA_TRY(launch_gemm(a.o, L.ko_p, reinterpret_cast<const uint16_t*>(c->w + L.w_o), L.ko_p, M, d, L.ko_p, e5,
                              s));

@@ -170,6 +170,9 @@ __global__ void __launch_bounds__(352, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // launched with programmatic dependent launch: Q'/K'/V' come from the a1 projection before it
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 8) {
     // ------------------------------------------------ Q' (both tiles) and K' producer
@@ -444,8 +447,9 @@ static cudaError_t launch_attn4_t(const PrefillAttnArgs& a, cudaStream_t stream)
   const int n_items = (n_qt + 1) / 2 * a.Nh * a.B;
   dim3 grid(std::min(n_items, num_sms()));  // persistent: the kernel deals the items to the CTAs
   prof_mark(stream, true, kProfAttnPrefill);
-  prefill_attn4_kernel<HD><<<grid, 352, C::SMEM, stream>>>(tq, tk, tv, a);
+  cudaError_t e = launch_k(prefill_attn4_kernel<HD>, grid, dim3(352), C::SMEM, stream, g_pdl, tq, tk, tv, a);
   prof_mark(stream, false, kProfAttnPrefill);
+  if (e != cudaSuccess) return e;
   ++g_launches;
   return cudaGetLastError();
 }
