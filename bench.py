@@ -81,6 +81,26 @@ def load_peaks():
     return dict(hbm=6650.0, tf=1590.0, tf_sus=1400.0, src="fallback")
 
 
+# ------------------------------------------------------------------------------------ algorithmic work
+# SURVEY.md §8(d) "Algorithmic counts": FLOPs at the plan ranks (causal attention over the
+# S(S+1)/2 pairs; no padding, masked tiles or exp), bytes = packed weights read once + K'/V' at the
+# packed widths + append + x/y.  Pinned by tests/test_bench_work.py against §8(d)'s figures.
+def prefill_layer_flops(d, nh, nkv, r, B, S):
+    """{'a1', 'a3', 'a5'} FLOPs of one prefill layer (uniform rank r = r_k = r_v)."""
+    n_qkv = nh * r + 2 * nkv * r
+    return {"a1": 2.0 * B * S * n_qkv * d, "a3": 4.0 * r * nh * B * S * (S + 1) / 2.0, "a5": 2.0 * B * S * nh * r * d}
+
+
+def decode_layer_bytes(d, nh, nkv, r, B, ctx, ko=None):
+    """{'a1', 'a3', 'a5'} algorithmic bytes of one decode layer-step at context `ctx` (uniform rank):
+    the packed weights, K'/V' of ctx cached tokens, Q'/O' and x/y rows (bf16)."""
+    ko = nh * r if ko is None else ko
+    n_qkv = nh * r + 2 * nkv * r
+    return {"a1": n_qkv * d * 2 + B * d * 2 + B * n_qkv * 2,
+            "a3": B * nkv * ctx * 2 * r * 2 + 2 * B * nh * r * 2,
+            "a5": d * ko * 2 + B * ko * 2 + B * d * 2}
+
+
 # ------------------------------------------------------------------------------------ clocks
 class ClockSampler:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -208,7 +228,8 @@ def isolated_kernels(zdc, torch, stream, dev, d, nh, nkv, r, S, T, B, L, step_ms
         x = torch.randn(B, K, device=dev, generator=g).to(bf)
         y = torch.empty(B, N, device=dev, dtype=bf)
         ms = _time_graph(torch, stream, lambda i: zdc.gemv_bf16(ws[i % 8], x, y), 64)
-        res[name] = ("hbm", N * K * 2 + B * K * 2 + B * N * 2, ms, L * T)
+        res[name] = ("hbm", decode_layer_bytes(d, nh, nkv, r, B, avg_ctx, ko)["a1" if name.startswith("a1") else "a5"],
+                     ms, L * T)
         del ws
     # decode attention at the average context of the 256 decode steps: 8 caches rotate
     caches = [(torch.randn(B, nkv, cap, r, device=dev, generator=g).to(bf),
@@ -219,19 +240,20 @@ def isolated_kernels(zdc, torch, stream, dev, d, nh, nkv, r, S, T, B, L, step_ms
     wsp = zdc.decode_attention_bf16(q, caches[0][0], caches[0][1], o, avg_ctx, lse)
     ms = _time_graph(torch, stream, lambda i: zdc.decode_attention_bf16(
         q, caches[i % 8][0], caches[i % 8][1], o, avg_ctx, lse, workspace=wsp), 64)
-    res["a3_decode_attention"] = ("hbm", B * nkv * avg_ctx * (r + r) * 2 + 2 * B * nh * r * 2, ms, L * T)
+    res["a3_decode_attention"] = ("hbm", decode_layer_bytes(d, nh, nkv, r, B, avg_ctx, ko)["a3"], ms, L * T)
     del caches
     # prefill (tensor-bound): the two projection GEMMs and the causal attention
     xa = torch.randn(B * S, d, device=dev, generator=g).to(bf)
     wq = torch.randn(Nqkv, d, device=dev, generator=g).to(bf)
     yq = torch.empty(B * S, Nqkv, device=dev, dtype=bf)
     ms = _time_graph(torch, stream, lambda i: zdc.gemm_bf16(xa, wq, yq), 10)
-    res["a1_prefill_gemm"] = ("tensor", 2.0 * B * S * Nqkv * d, ms, L)
+    pf = prefill_layer_flops(d, nh, nkv, r, B, S)
+    res["a1_prefill_gemm"] = ("tensor", pf["a1"], ms, L)
     oa = torch.randn(B * S, ko, device=dev, generator=g).to(bf)
     wo = torch.randn(d, ko, device=dev, generator=g).to(bf)
     yo = torch.empty(B * S, d, device=dev, dtype=bf)
     ms = _time_graph(torch, stream, lambda i: zdc.gemm_bf16(oa, wo, yo), 10)
-    res["a5_prefill_gemm"] = ("tensor", 2.0 * B * S * d * nh * r, ms, L)
+    res["a5_prefill_gemm"] = ("tensor", pf["a5"], ms, L)
     qa = torch.randn(B, S, nh * r, device=dev, generator=g).to(bf)
     ka = torch.randn(B, nkv, S, r, device=dev, generator=g).to(bf)
     va = torch.randn(B, nkv, S, r, device=dev, generator=g).to(bf)
@@ -239,7 +261,7 @@ def isolated_kernels(zdc, torch, stream, dev, d, nh, nkv, r, S, T, B, L, step_ms
     la = torch.empty(B, nh, S, device=dev)
     ms = _time_graph(torch, stream, lambda i: zdc.prefill_attention_bf16(qa, ka, va, pa, la,
                                                                          scale=1.0 / math.sqrt(128)), 10)
-    res["a3_prefill_attention"] = ("tensor", 4.0 * r * nh * B * S * (S + 1) / 2.0, ms, L)
+    res["a3_prefill_attention"] = ("tensor", pf["a3"], ms, L)
     kernels, shares = {}, {}
     for k, (bound, work, ms, per_step) in res.items():
         s = ms / 1e3
@@ -449,7 +471,7 @@ def config_bench(args, zdc, torch, dev, stream, cid, n_layers=4, T=48):
     # algorithmic work: unpadded ranks (multiples of 16 here: padding = 0)
     nq, nkvr = nh * r, nkv * r
     n_qkv = nq + 2 * nkvr
-    flop = 2.0 * B * S * d * n_qkv + 4.0 * r * nh * B * S * (S + 1) / 2 + 2.0 * B * S * nq * d
+    flop = sum(prefill_layer_flops(d, nh, nkv, r, B, S).values())
     wbytes = (n_qkv * d + d * nq) * 2
     wI, wU = 2 * nkv * r * 2, 2 * nkv * ru * 2  # bytes per cached token per layer (K' + V')
     if cid == 3:
