@@ -394,12 +394,16 @@ __global__ void __launch_bounds__(192, DTC<HD, STG>::CPS)
   }
 }
 
-// splits per (b, g): the fewest that fill the persistent CTAs' last round to >= 90 % (each split
-// keeps >= 2 key tiles at the capacity bound)
+// splits per (b, g): one whenever the (b, g) pairs alone cover the resident CTAs -- a split adds a
+// Q' load, a pipeline ramp, a partial and a merge per item, which measured costlier than an
+// unfilled last round (c4: 1 split 217 us, 2 splits 251 us, 4 splits 264 us per layer-step);
+// otherwise the fewest that fill the persistent CTAs' last round to >= 90 % (each split keeping >= 2
+// key tiles at the capacity bound)
 int decode_tc_splits(int B, int Nkv, int len) {
   static const int forced = getenv("ZDC_TC_SPLITS") ? atoi(getenv("ZDC_TC_SPLITS")) : 0;  // A/B override
   if (forced > 0) return std::min(64, forced);
   const int pairs = B * Nkv, nsm = 2 * num_sms();  // resident CTAs at r = 64 (r = 128: a bound)
+  if (pairs >= nsm) return 1;
   const int max_s = std::max(1, std::min(64, (len + 255) / 256));
   for (int s = 1; s <= max_s; ++s) {
     const int items = pairs * s;

@@ -462,10 +462,12 @@ cudaError_t launch_gemm(const uint16_t* A, int64_t lda, const uint16_t* B, int64
   // skinny M (decode, B > 8): ZDC_SKINNY_KB=2 fetches 2 k-blocks per stage with one 3-D box (measured
   // no faster than 1 under ncu: 35 vs 32 us at the c4 a1 shape; profiles/r01/NOTES.md)
   static const int skinny_kb = getenv("ZDC_SKINNY_KB") ? atoi(getenv("ZDC_SKINNY_KB")) : 1;
-  static const int skinny_bn = getenv("ZDC_SKINNY_BN") ? atoi(getenv("ZDC_SKINNY_BN")) : 256;
+  static const int skinny_bn = getenv("ZDC_SKINNY_BN") ? atoi(getenv("ZDC_SKINNY_BN")) : 0;
   const bool skinny = epi.ws && epi.ws_cnt && M <= 128 && N % 8 == 0;
   const int KBs = skinny && skinny_kb == 2 && K % 128 == 0 ? 2 : 1;
-  if (skinny && N > 128) BN = skinny_bn == 128 ? 128 : 256;
+  // skinny: BN = 128 when 256-wide tiles would be few (< 40: c4 a1 20, a5 32 tiles; 128 measured 4 % faster
+  // per c4 layer-step), ZDC_SKINNY_BN forces 128 / 256
+  if (skinny && N > 128) BN = skinny_bn == 128 || (skinny_bn == 0 && (N + 255) / 256 < 40) ? 128 : 256;
   if (skinny) {
     // split K so the weight stream spreads over the SMs (>= 4 stage blocks per split)
     const int tiles = (N + BN - 1) / BN, kbs = K / (64 * KBs);
