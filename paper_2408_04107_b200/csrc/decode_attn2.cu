@@ -14,6 +14,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace zdc {
 
 static constexpr float kLog2eD = 1.4426950408889634f;
@@ -309,6 +311,8 @@ static int ctas_per_sm_g(int width) {
 
 // Split count: as many CTAs as fit in ONE wave (occupancy x SMs), >= 32 rows per warp.
 int decode2_splits(int B, int Nkv, int len, int width, int G) {
+  static const int forced = getenv("ZDC_V2_SPLITS") ? atoi(getenv("ZDC_V2_SPLITS")) : 0;  // A/B override
+  if (forced > 0) return forced > 64 ? 64 : forced;
   int fit = 1;
   switch (G) {
     case 1: fit = ctas_per_sm_g<1>(width); break;

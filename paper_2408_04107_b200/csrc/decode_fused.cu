@@ -11,6 +11,8 @@ cudaError_t launch_fused_b4(const DecFusedArgs& a, int RK, int G, cudaStream_t s
 cudaError_t launch_fused_b8(const DecFusedArgs& a, int RK, int G, cudaStream_t s);
 
 int decode_fused_splits(int B, int Nkv) {
+  static const int forced = getenv("ZDC_FUSED_SPLITS") ? atoi(getenv("ZDC_FUSED_SPLITS")) : 0;  // A/B override
+  if (forced > 0) return forced;
   int s = num_sms() / (B * Nkv);
   if (s > 128) s = 128;
   return s < 1 ? 1 : s;
