@@ -187,6 +187,23 @@ __device__ __forceinline__ void tma_load_op(void* dst, const CUtensorMap* map, u
     tma_load_3d(dst, map, bar, 0, row, kstage * KB);
 }
 
+// Output tile -> (M-block, N-block).  band == 0: M fastest.  band > 0: grouped raster -- bands of
+// `band` N-blocks, each swept over every M-block with the band's N fastest, so concurrent CTAs share
+// A rows (read once per band) while the band's weight tiles stay L2-resident.
+__device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, int band, int& mb, int& nb) {
+  if (band <= 0) {
+    mb = tile % m_tiles;
+    nb = tile / m_tiles;
+    return;
+  }
+  const int per_band = m_tiles * band;
+  const int bi = tile / per_band, n0 = bi * band;
+  const int w = min(band, n_tiles - n0);  // the last band may be narrower
+  const int idx = tile - bi * per_band;
+  mb = idx / w;
+  nb = n0 + idx % w;
+}
+
 template <int BN, int KB>
 __global__ void __launch_bounds__(256, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, int M,
@@ -244,9 +261,11 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t phase = 0;
       int issued = 0;
       bool waited = false;
+      const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
       for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
         const int tile = w % num_tiles, sp = w / num_tiles;
-        const int mb = tile % m_tiles, nb = tile / m_tiles;
+        int mb, nb;
+        tile_coords(tile, m_tiles, n_tiles, epi.raster_n, mb, nb);
         const int kb1 = min(k_blocks, (sp + 1) * kpb);
         if (!waited && w == static_cast<int>(blockIdx.x)) {
           // prologue: B of the first stages, then the dependency wait, then their A
@@ -267,8 +286,13 @@ __global__ void __launch_bounds__(256, 1)
         for (int kb = sp * kpb + issued; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-          tma_load_op<KB>(sA + stage * C::A_BYTES, &tma_a, &full[stage], kb, mb * C::BM);
-          tma_load_op<KB>(sB + stage * C::B_BYTES, &tma_b, &full[stage], kb, nb * BN);
+          if (KB == 1 && epi.raster_n) {  // A streams through L2 once; B (the weights) stays resident
+            tma_load_2d_hint(sA + stage * C::A_BYTES, &tma_a, &full[stage], kb * C::BK, mb * C::BM, pol_first);
+            tma_load_2d_hint(sB + stage * C::B_BYTES, &tma_b, &full[stage], kb * C::BK, nb * BN, pol_last);
+          } else {
+            tma_load_op<KB>(sA + stage * C::A_BYTES, &tma_a, &full[stage], kb, mb * C::BM);
+            tma_load_op<KB>(sB + stage * C::B_BYTES, &tma_b, &full[stage], kb, nb * BN);
+          }
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -322,7 +346,8 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t acc_phase = 0;
     for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
       const int tile = w % num_tiles;
-      const int mb = tile % m_tiles, nb = tile / m_tiles;
+      int mb, nb;
+      tile_coords(tile, m_tiles, n_tiles, epi.raster_n, mb, nb);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = mb * C::BM + q * 32 + lane;
@@ -478,6 +503,18 @@ cudaError_t launch_gemm(const uint16_t* A, int64_t lda, const uint16_t* B, int64
       ep.k_splits = (kbs + kpb - 1) / kpb;  // every split keeps >= 1 k-block
     }
   }
+  // N-fastest raster for a large A: concurrent CTAs share A rows (read once from HBM) while the
+  // weights B stay L2-resident; the default M-fastest order re-reads A once per N-tile (c4 prefill
+  // a1: 174 GB of DRAM reads for 8.7 GB of operands, ncu).  ZDC_GEMM_RASTER=0/1 forces it.
+  static const int raster_env = getenv("ZDC_GEMM_RASTER") ? atoi(getenv("ZDC_GEMM_RASTER")) : -1;
+  const double a_bytes = static_cast<double>(M) * K * 2, b_bytes = static_cast<double>(N) * K * 2;
+  // band: the N-blocks whose weight tiles fit ~40 MB of L2 (ZDC_GEMM_RASTER=0 keeps M-fastest,
+  // = n forces a band of n)
+  const int n_tiles_all = (N + BN - 1) / BN;
+  int band = std::max(1, static_cast<int>(40e6 / (static_cast<double>(BN) * K * 2)));
+  if (band > n_tiles_all) band = n_tiles_all;
+  ep.raster_n = raster_env >= 0 ? raster_env : (a_bytes > 128e6 && N > BN ? band : 0);
+  (void)b_bytes;
   CUtensorMap ta, tb;
   if (KBs == 2 && make_tmap_3d_kblocks(&ta, A, K, M, lda * 2, 128, 2) && make_tmap_3d_kblocks(&tb, B, K, N, ldb * 2, BN, 2))
     return BN == 256 ? launch_gemm_bn<256, 2>(ta, tb, M, N, K, ep, stream)

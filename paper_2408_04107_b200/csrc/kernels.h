@@ -38,6 +38,7 @@ struct Epilogue {
   int* ws_cnt = nullptr;
   int k_splits = 1;
   int pdl = 0;  // launch with programmatic dependent launch (decode chains)
+  int raster_n = 0;  // tile order: 0 M-fastest; n > 0 bands of n N-blocks, N fastest (launch_gemm, large A)
 };
 
 // ---- tensor maps (driver entry point resolved at runtime; no -lcuda link)
