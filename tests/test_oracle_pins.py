@@ -354,10 +354,7 @@ def test_P9_selection_golden():
         imp, tau, k = O.select_important(np.array(c["scores"], dtype=np.float32), c["g_bp"])
         assert k == c["k"]
         assert np.nonzero(imp)[0].tolist() == c["important"]
-        if k == len(c["scores"]):
-            assert tau == -math.inf
-        elif k == 0:
-            assert tau == math.inf
+        assert tau == float(c["tau"]), (c, tau)
     with pytest.raises(ValueError):
         O.select_important(np.array([1.0, np.nan]), 5000)
 
@@ -459,3 +456,91 @@ def test_P9_count_rule_exact_rational():
     for g_bp in list(range(0, 10001, 37)) + [1, 9999, 10000, 1400, 1500]:
         for S in (1, 2, 3, 7, 10, 100, 1024, 2049):
             assert O.important_count(g_bp, S) == math.ceil(Fraction(g_bp, 10000) * S)
+
+
+# ---------------------------------------------------------------- BF16-faithful rounding points
+def _bits_to_f32(h):
+    return float(np.array([int(h, 16)], dtype=np.uint32).view(np.float32)[0])
+
+
+def test_bf16_round_to_nearest_even_golden():
+    """The oracle's bf16() against hand-worked roundTiesToEven cases (golden/bf16_rne_examples.json)."""
+    spec = json.load(open(os.path.join(GOLDEN, "bf16_rne_examples.json")))
+    for c in spec["cases"]:
+        x = _bits_to_f32(c["f32"])
+        want = _bits_to_f32(c["bf16"] + "0000")
+        got = float(O.bf16(np.array([x]))[0])
+        assert got == want, (c, got, want)
+
+
+def _attend_model(faithful):
+    m = O.OracleModel.__new__(O.OracleModel)
+    m.dims, m.faithful = Dims(1, 1, 1, 1, 1), faithful
+    return m
+
+
+def test_faithful_attend_worked_example():
+    """P rounded to bf16 before PV, l from the UNROUNDED P, O' rounded after the division
+    (golden/faithful_examples.json 'attend'; Eq. 3, PAPER.md:254-260)."""
+    c = json.load(open(os.path.join(GOLDEN, "faithful_examples.json")))["attend"]
+    q = np.array(c["q"])
+    k = np.array([[0.0], [math.log(1.0 / 3.0)]])
+    v = np.array(c["v"])
+    for faithful, key in ((True, "faithful_O"), (False, "plain_O")):
+        o, lse = _attend_model(faithful)._attend(q, k, v, np.array([1]))
+        assert abs(o[0, 0] - c[key]) <= 1e-12, (faithful, o[0, 0], c[key])
+        assert abs(lse[0] - math.log(4.0 / 3.0)) <= 1e-12, (faithful, lse[0])
+
+
+def test_faithful_layer_worked_example():
+    """Weights and Q'/K' rounded to bf16 at the projection (golden/faithful_examples.json 'layer')."""
+    c = json.load(open(os.path.join(GOLDEN, "faithful_examples.json")))["layer"]
+    dims = Dims(1, 1, 1, 1, 1)
+    folded = [dict(wq_f=np.array([[c["wq"]]]), wk_f=np.array([[c["wk"]]]),
+                   wv_f=np.array([[c["wv"]]]), wo_f=np.array([[c["wo"]]]))]
+    x = np.array(c["x"]).reshape(1, 2, 1)
+    want = {True: [0.0, math.log1p(math.exp(3.03125 ** 2))],
+            False: [0.0, math.log1p(math.exp(3.0205078125 ** 2))]}
+    for faithful in (True, False):
+        m = O.OracleModel(dims, plan_uniform(1, 1), folded, faithful=faithful)
+        m.prefill_layer(0, x)
+        assert np.allclose(m.lse[0][0, 0], want[faithful], rtol=0, atol=1e-12), (faithful, m.lse[0])
+        if faithful:
+            assert m.K[0][0, 0, :, 0].tolist() == c["faithful_k"]
+
+
+def test_faithful_stored_and_emitted_values_are_bf16():
+    """Rounding points (2) and (5): cached K'/V' and y are bf16-representable in faithful mode."""
+    dims = Z.dims_of(1)
+    _, folded = _fold_all(dims, 1, n_calib=512)
+    x = Z.prompt(dims, 1, 1, 40)
+    m = O.OracleModel(dims, plan_uniform(1, 16), folded, faithful=True)
+    y = m.prefill(x[:, :32])
+    for t in range(32, 40):
+        y = m.decode(x[:, t])
+        assert np.all(O.bf16(y) == y)
+    assert np.all(O.bf16(m.K[0]) == m.K[0]) and np.all(O.bf16(m.V[0]) == m.V[0])
+
+
+def test_decode_score_equal_to_tau_is_unimportant():
+    """Reading c12: a decode token is important iff score > tau (strict; ties go to the older
+    token, as in the prefill order key).  With W_Q = 0 every logit is 0, so with the per-key mean
+    (importance_mode 1) every token's score is exactly log N_h: the prompt's first k tokens are
+    important (index ascending), tau = log N_h, and every decode token ties with tau."""
+    dims = Dims(2, 8, 2, 2, 4)
+    rng = np.random.default_rng(3)
+    folded = [dict(wq_f=np.zeros((8, 8)), wk_f=rng.standard_normal((8, 8)), wv_f=rng.standard_normal((8, 8)),
+                   wo_f=rng.standard_normal((8, 8))) for _ in range(2)]
+    plan = plan_split(2, 4, 2, [[0, 1]], [5000], importance_mode=1)
+    x = rng.standard_normal((2, 7, 8))
+    m = O.OracleModel(dims, plan, folded)
+    m.prefill(x[:, :4])
+    assert np.all(m.scores[0] == math.log(2.0))
+    assert m.classes[0].tolist() == [[True, True, False, False]] * 2
+    assert np.all(m.tau[0] == math.log(2.0))
+    for t in range(4, 7):
+        m.decode(x[:, t])
+        assert np.all(m.scores[0][:, t] == math.log(2.0))
+        assert not m.classes[0][:, t].any()
+        for l in range(2):
+            assert np.all(m.K[l][:, :, t, 2:] == 0.0) and np.all(m.V[l][:, :, t, 2:] == 0.0)
