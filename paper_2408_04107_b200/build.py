@@ -14,14 +14,18 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 INCLUDE = os.path.join(ROOT, "include")
-BUILD = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libzdc.so")
+# Same-box A/B of kernel variants: ZDC_BUILD_VARIANT=<name> ZDC_BUILD_DEFS="-DFOO=1" builds
+# libzdc_<name>.so from the same sources into its own object directory (load it with ZDC_LIB_PATH).
+VARIANT = os.environ.get("ZDC_BUILD_VARIANT", "")
+VARIANT_DEFS = os.environ.get("ZDC_BUILD_DEFS", "").split()
+BUILD = os.path.join(HERE, "_build" + ("_" + VARIANT if VARIANT else ""))
+LIB = os.path.join(HERE, "libzdc%s.so" % ("_" + VARIANT if VARIANT else ""))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUDA_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", f"-I{INCLUDE}", f"-I{CSRC}",
-                     "--expt-relaxed-constexpr"]
+                     "--expt-relaxed-constexpr"] + VARIANT_DEFS
 CXX_FLAGS = ["-O3", "-fPIC", "-std=c++17", "-fopenmp", "-march=x86-64-v3", f"-I{INCLUDE}", f"-I{CSRC}",
-             "-I/usr/local/cuda/include"]
+             "-I/usr/local/cuda/include"] + VARIANT_DEFS
 
 
 def _run(cmd):

@@ -41,9 +41,12 @@ def test_decode_tc_from_empty(dims, r, B, T):
     x = Z.prompt(dims, 1, B, T, seed=31)
     ctx = make_context(dims, plan, folded, B, T + 2)
     y = _decode(ctx, x)
-    want = O.OracleModel(dims, plan, folded, faithful=True).prefill(x)
+    m = O.OracleModel(dims, plan, folded, faithful=True)
+    want = m.prefill(x)
     assert normwise(y, want) <= TOL
     # LSE of the last step's query heads (natural log of the Eq. 3 denominator)
+    lse = ctx.last_lse(dims.n_layers - 1, B, 1)[:, :, 0]
+    assert np.max(np.abs(lse - m.lse[dims.n_layers - 1][:, :, T - 1])) <= 0.05
     ctx.close()
 
 

@@ -30,7 +30,7 @@ def _worker(rank, world, port, layout, S, B, out_q):
     import oracle as O  # noqa: F401
     import paper_2408_04107_b200 as zdc
     import zdc_synth as Z
-    from zdc_testlib import fold_stack, to_dev_bf16
+    from zdc_testlib import fold_stack, load_lib_fold, to_dev_bf16
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -40,7 +40,7 @@ def _worker(rank, world, port, layout, S, B, out_q):
     _, folded = fold_stack(dims, 1, n_calib=256)
     ctx = zdc.Context(dims, plan, B, S)
     for l, f in enumerate(folded):
-        ctx.load_folded(l, f["wq_f"], f["wk_f"], f["wv_f"], f["wo_f"])
+        load_lib_fold(ctx, l, f)
     x = Z.prompt(dims, 1, B, S, seed=41)
     pos = zdc.sp_positions(S, world, rank, layout)
     cudart = _cudart()
@@ -115,7 +115,7 @@ def test_sp_prefill_nccl_world1():
     equal zdc_prefill bit for bit; the stats report zero exchanged bytes."""
     import paper_2408_04107_b200 as zdc
     import zdc_synth as Z
-    from zdc_testlib import fold_stack, from_dev, to_dev_bf16
+    from zdc_testlib import fold_stack, from_dev, load_lib_fold, to_dev_bf16
     dims = Z.Dims(2, 256, 4, 2, 64)
     plan = Z.plan_uniform(2, 32)
     _, folded = fold_stack(dims, 1, n_calib=256)
@@ -125,7 +125,7 @@ def test_sp_prefill_nccl_world1():
     for sp in (False, True):
         ctx = zdc.Context(dims, plan, 1, S)
         for l, f in enumerate(folded):
-            ctx.load_folded(l, f["wq_f"], f["wk_f"], f["wv_f"], f["wo_f"])
+            load_lib_fold(ctx, l, f)
         y = torch.empty_like(x)
         if sp:
             ctx.comm_init(zdc.comm_unique_id(), 0, 1)

@@ -15,13 +15,26 @@ def normwise(g, o) -> float:
 
 
 def fold_stack(dims, cfg_id, n_calib=512, seed=0, **wkw):
+    """Each side folds independently (SURVEY.md §8(c) "Inputs"): the oracle with NumPy/LAPACK in
+    fp64 (the dicts returned), the library with its own host fold `zdc_fold_weights` (kept under
+    the "lib" key and loaded by make_context / load_lib_fold).  Both see the same BF16-rounded
+    unfolded weights and calibration rows; their R agree up to the fold tolerance (test_fold.py)."""
+    import paper_2408_04107_b200 as zdc
     ws, folded = [], []
     for l in range(dims.n_layers):
         w = Z.layer_weights(dims, cfg_id, l, seed, **wkw)
         xc = Z.calibration(dims, cfg_id, l, n_calib, seed)
         ws.append(w)
-        folded.append(O.fold_layer(dims, w.wq, w.wk, w.wv, w.wo, xc))
+        f = O.fold_layer(dims, w.wq, w.wk, w.wv, w.wo, xc)
+        f["lib"] = zdc.fold_weights(dims, w.wq, w.wk, w.wv, w.wo, xc)
+        folded.append(f)
     return ws, folded
+
+
+def load_lib_fold(ctx, layer, f):
+    """Load the LIBRARY's fold of this layer (never the oracle's) into a context."""
+    g = f["lib"]
+    ctx.load_folded(layer, g["wq_f"], g["wk_f"], g["wv_f"], g["wo_f"])
 
 
 def to_dev_bf16(a):
@@ -38,5 +51,5 @@ def make_context(dims, plan, folded, max_batch, max_seq):
     import paper_2408_04107_b200 as zdc
     ctx = zdc.Context(dims, plan, max_batch, max_seq)
     for l, f in enumerate(folded):
-        ctx.load_folded(l, f["wq_f"], f["wk_f"], f["wv_f"], f["wo_f"])
+        load_lib_fold(ctx, l, f)
     return ctx
