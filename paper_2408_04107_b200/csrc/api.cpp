@@ -80,7 +80,7 @@ int64_t zdc_kernel_launch_count(void) { return g_launches; }
 
 
 // ------------------------------------------------------------------ context
-static int g_decode_mode = getenv("ZDC_DECODE_MODE") ? atoi(getenv("ZDC_DECODE_MODE")) : 0;
+static int g_decode_mode = knob("ZDC_DECODE_MODE", 0);
 int zdc_decode_mode(int mode) {
   if (mode < 0 || mode > 3) return -1;
   const int old = g_decode_mode;
@@ -211,8 +211,8 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
     if (L.n_qkv > max_nqkv) max_nqkv = L.n_qkv;
     if (L.rv_p > max_rv) max_rv = L.rv_p;
   }
-  c->len_dev_off = coff;
-  coff = align_up(coff + static_cast<int64_t>(d.n_layers) * 4, 256);
+  c->len_dev_off = coff;  // [n_layers] device lengths + the decode overflow flag
+  coff = align_up(coff + static_cast<int64_t>(d.n_layers + 1) * 4, 256);
   c->weight_bytes = woff;
   c->cache_bytes = coff;
   const int64_t rows = static_cast<int64_t>(max_batch) * max_seq;
@@ -543,6 +543,7 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
     e1.mode = 1;
     e1.qkv = qkv_dest(c, L, 1, 0, nullptr);
     e1.qkv.pos_ptr = len_dev;
+    e1.qkv.pos_cap = c->max_seq;
     uint16_t* knew = reinterpret_cast<uint16_t*>(c->scratch + c->s_new);
     uint16_t* vnew = knew + static_cast<int64_t>(B) * Nkv * L.rk_p;
     if (L.split) {  // stage the new row; the class-aware append places it below
@@ -558,7 +559,7 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
     const uint16_t* wqkv = reinterpret_cast<const uint16_t*>(c->w + L.w_qkv);
     const uint16_t* wo = reinterpret_cast<const uint16_t*>(c->w + L.w_o);
     const int mode = g_decode_mode;
-    const bool fused_on = mode != 3 && !(getenv("ZDC_DEC_FUSED") && atoi(getenv("ZDC_DEC_FUSED")) == 0);
+    const bool fused_on = mode != 3 && knob("ZDC_DEC_FUSED", 1) != 0;
     if (fused_on && mode != 1 && !L.split && L.w_od >= 0 && L.w_qd >= 0) {
       // the cluster layer-step: one cluster per KV group, no grid barrier (decode_cluster.cuh)
       const int C = decode_cluster_size(B, L.rk_p, c->G, Nkv, d);
@@ -571,6 +572,7 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
         f.kc = reinterpret_cast<uint16_t*>(c->cache + L.k_off);
         f.vc = reinterpret_cast<uint16_t*>(c->cache + L.v_off);
         f.len_ptr = len_dev;
+        f.err = c->len_dev() + c->dims.n_layers;
         f.x = xin;
         f.ldx = d;
         f.y = y;
@@ -586,7 +588,7 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
         f.Nkv = Nkv;
         f.S_cap = c->max_seq;
         f.C = C;
-        static const int l2pf = getenv("ZDC_CL_PF") ? atoi(getenv("ZDC_CL_PF")) : 6;
+        static const int l2pf = knob("ZDC_CL_PF", 6);
         f.l2_prefetch = l2pf;
         f.trace = fused_trace_buffer();
         f.scale = 1.0f / std::sqrt(static_cast<float>(c->dims.d_head));
@@ -632,6 +634,7 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
       f.splits = decode_fused_splits(B, Nkv);
       f.ko_p = L.ko_p;
       f.scale = 1.0f / std::sqrt(static_cast<float>(c->dims.d_head));
+      f.err = c->len_dev() + c->dims.n_layers;
       g_prof_class = kProfDecodeLayer;
       cudaError_t e = launch_decode_fused(f, L.rk_p, s);
       g_prof_class = kProfOther;
@@ -680,7 +683,7 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
     a.part = reinterpret_cast<float*>(c->scratch + c->s_part);
     a.counters = reinterpret_cast<int*>(c->scratch + c->s_cnt);
     // cached K'/V' rows before the PDL wait: 2 = into shared memory, 1 = into L2, 0 = none
-    a.prefetch_before_wait = getenv("ZDC_ATTN_PREWAIT") ? atoi(getenv("ZDC_ATTN_PREWAIT")) : 2;
+    a.prefetch_before_wait = knob("ZDC_ATTN_PREWAIT", 2);
     a.B = B;
     a.Nh = Nh;
     a.Nkv = Nkv;
@@ -692,7 +695,7 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
       // L2 prefetch of the weights read next (bit 0: this layer's W_O^R, bit 1: the next layer's
       // W_QKV^R, wrapping to layer 0 for the next step); off by default (ZDC_DEC_L2PF=3 enables it):
       // measured slower in round 1, the prefetches delay the attention's own bulk copies
-      static const int pf_mode = getenv("ZDC_DEC_L2PF") ? atoi(getenv("ZDC_DEC_L2PF")) : 0;
+      static const int pf_mode = knob("ZDC_DEC_L2PF", 0);
       const LayerInfo& N = c->layers[(l + 1) % c->dims.n_layers];
       if (pf_mode & 1) {
         a.pf_ptr[0] = wo;
@@ -715,7 +718,7 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
       a.rk1 = L.rku_p;
       a.rv1 = L.rvu_p;
     }
-    static const bool attn_tc_on = !(getenv("ZDC_DEC_ATTN_TC") && atoi(getenv("ZDC_DEC_ATTN_TC")) == 0);
+    static const bool attn_tc_on = knob("ZDC_DEC_ATTN_TC", 1) != 0;
     cudaError_t ea = cudaErrorNotSupported;
     if (attn_tc_on && !L.split && decode_attention_tc_supported(L.rk_p, L.rv_p, c->G)) {
       // grouped-query heads: the tensor-core kernel (decode_attn_tc.cu)
@@ -746,6 +749,8 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
     e5.d = y;
     e5.ldd = d;
     e5.len_inc = len_dev;
+    e5.len_cap = c->max_seq;
+    e5.err = c->len_dev() + c->dims.n_layers;
     g_prof_class = kProfGemvO;
     if (gemv_supported(B, L.ko_p))
       ZDC_CUDA_TRY(launch_gemv(wo, a.o, L.ko_p, B, d, L.ko_p, e5, s));
@@ -833,10 +838,14 @@ zdc_status zdc_cache_sync(zdc_ctx* c, void* stream) {
   if (!c) return fail(ZDC_ERR_INVALID_ARG, "zdc_cache_sync: null ctx");
   if (!c->cache) return fail(ZDC_ERR_STATE, "zdc_cache_sync: ctx not bound");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  std::vector<int> h(c->dims.n_layers);
+  std::vector<int> h(c->dims.n_layers + 1);
   ZDC_CUDA_TRY(cudaMemcpyAsync(h.data(), c->len_dev(), h.size() * 4, cudaMemcpyDeviceToHost, s));
   ZDC_CUDA_TRY(cudaStreamSynchronize(s));
   for (int l = 0; l < c->dims.n_layers; ++l) c->len[l] = h[l];
+  if (h[c->dims.n_layers])
+    return fail(ZDC_ERR_CAPACITY, "zdc_cache_sync: decode steps replayed past max_seq = %d (each step uses one "
+                "row; the overflowing steps rewrote the last row and their outputs are invalid; zdc_cache_reset clears)",
+                c->max_seq);
   return ZDC_OK;
 }
 
@@ -844,7 +853,7 @@ zdc_status zdc_cache_reset(zdc_ctx* c, void* stream) {
   if (!c) return fail(ZDC_ERR_INVALID_ARG, "zdc_cache_reset: null ctx");
   if (!c->cache) return fail(ZDC_ERR_STATE, "zdc_cache_reset: ctx not bound");
   // Only the lengths are reset: no kernel ever reads a cache row at or beyond its layer's length.
-  ZDC_CUDA_TRY(cudaMemsetAsync(c->len_dev(), 0, static_cast<size_t>(c->dims.n_layers) * 4,
+  ZDC_CUDA_TRY(cudaMemsetAsync(c->len_dev(), 0, static_cast<size_t>(c->dims.n_layers + 1) * 4,
                                static_cast<cudaStream_t>(stream)));
   c->len.assign(c->dims.n_layers, 0);
   c->sp_layer.assign(c->dims.n_layers, 0);

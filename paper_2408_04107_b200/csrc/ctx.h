@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include "zdc.h"
+#include "knobs.h"
 
 namespace zdc {
 
@@ -64,7 +65,7 @@ struct zdc_ctx {
     int64_t kernels = 0;
   };
   std::map<std::tuple<int, int, int, const void*, void*, cudaStream_t>, GraphEntry> graphs;
-  bool use_graphs = getenv("ZDC_NO_GRAPH") == nullptr;  // zdc_decode replays one CUDA graph per call shape
+  bool use_graphs = zdc::knob("ZDC_NO_GRAPH", 0) == 0;  // zdc_decode replays one CUDA graph per call shape
   int* len_dev() { return reinterpret_cast<int*>(cache + len_dev_off); }
 };
 

@@ -36,7 +36,7 @@ __device__ __forceinline__ void store_scalar(const Epilogue& e, int m, int n, ui
       dst = q.q + static_cast<int64_t>(m) * q.ldq + n;
     } else {
       const int b = m / q.S, t = m - b * q.S;
-      const int pos = q.posmap ? q.posmap[t] : (q.pos_ptr ? *q.pos_ptr : q.pos0) + t;
+      const int pos = q.posmap ? q.posmap[t] : (q.pos_ptr ? min(*q.pos_ptr, q.pos_cap - 1) : q.pos0) + t;
       if (n < q.nq + q.nk) {
         const int nn = n - q.nq, g = nn / q.rk, c = nn - g * q.rk;
         dst = q.k + b * q.kb + g * q.kg + static_cast<int64_t>(pos) * q.rk + c;
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(256) gemv_kernel(const uint16_t* __restrict__ 
       l2_prefetch(W + static_cast<int64_t>(n) * K, static_cast<uint32_t>(K) * 2u);
   pdl_wait();
   if (pdl_mode & 1) pdl_trigger();
-  if (epi.len_inc && blockIdx.x == 0 && threadIdx.x == 0) *epi.len_inc += 1;
+  if (epi.len_inc && blockIdx.x == 0 && threadIdx.x == 0) advance_len(epi);
   for (int i = threadIdx.x; i < NB * kc; i += blockDim.x) {
     const int b = i / kc, c = i - b * kc;
     xs[i] = *reinterpret_cast<const uint4*>(x + b * ldx + c * 8);
@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(288, 1)
   // ---- consumers
   pdl_wait();
   if (pdl_mode & 1) pdl_trigger();
-  if (epi.len_inc && blockIdx.x == 0 && threadIdx.x == 0) *epi.len_inc += 1;
+  if (epi.len_inc && blockIdx.x == 0 && threadIdx.x == 0) advance_len(epi);
   for (int i = threadIdx.x; i < NB * kc; i += 256) {
     const int b = i / kc, c = i - b * kc;
     xs[i] = *reinterpret_cast<const uint4*>(x + b * ldx + c * 8);
@@ -194,9 +194,9 @@ __global__ void __launch_bounds__(288, 1)
 }
 
 // ring bytes per CTA (tunable with ZDC_GEMV_RING_KB); 96 KB leaves room for the next kernel's CTAs
-static const int kGemvRingBytes = getenv("ZDC_GEMV_RING_KB") ? atoi(getenv("ZDC_GEMV_RING_KB")) * 1024 : 128 * 1024;
+static const int kGemvRingBytes = knob("ZDC_GEMV_RING_KB", 128) * 1024;
 // CTAs per SM for the projection GEMV (tunable with ZDC_GEMV_CTAS)
-static const int kGemvCtasPerSm = getenv("ZDC_GEMV_CTAS") ? atoi(getenv("ZDC_GEMV_CTAS")) : 1;
+static const int kGemvCtasPerSm = knob("ZDC_GEMV_CTAS", 1);
 
 template <int NB>
 static cudaError_t launch_gemv_nb(const uint16_t* W, const uint16_t* x, int64_t ldx, int N, int K, const Epilogue& epi,
@@ -218,7 +218,7 @@ static cudaError_t launch_gemv_nb(const uint16_t* W, const uint16_t* x, int64_t 
   const size_t smem = static_cast<size_t>(slots) * K * 2 + static_cast<size_t>(NB) * K * 2 + 16 * slots + 16;
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   // the a1 projection (writes the staging read by attention) bounds the look-ahead
-  const int mode = (epi.mode == 1 ? 1 : 0) | (getenv("ZDC_GEMV_NO_PREWAIT") ? 2 : 0);
+  const int mode = (epi.mode == 1 ? 1 : 0) | (knob("ZDC_GEMV_NO_PREWAIT", 0) ? 2 : 0);
   prof_mark(stream, true, g_prof_class);
   cudaError_t e = launch_k(gemv_ring_kernel<NB>, dim3(blocks), dim3(288), smem, stream, g_pdl && (g_pdl_mask & 1), W,
                            x, ldx, N, K, epi,
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
     // uniform cache: the length is final before the predecessor (the a1 projection) runs, so every
     // cached row of the chunk can stream in while it finishes (the new row is excluded):
     // mode 2 stages them straight into shared memory, mode 1 only into L2.
-    const int len0 = a.len_ptr ? *a.len_ptr + 1 : a.len;
+    const int len0 = a.len_ptr ? min(*a.len_ptr + 1, a.S_cap) : a.len;
     const int ch0 = (len0 + a.splits - 1) / a.splits;
     const int p0 = split * ch0;
     const int np = max(0, min(min(len0, p0 + ch0), len0 - 1) - p0);
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(128) decode_attn_partial(const DecodeAttnArgs 
   pdl_wait();
   int len;
   if (pool == 0)
-    len = a.n0_ptr ? a.n0_ptr[b] : (a.len_ptr ? *a.len_ptr + 1 : a.len);
+    len = a.n0_ptr ? a.n0_ptr[b] : (a.len_ptr ? min(*a.len_ptr + 1, a.S_cap) : a.len);
   else
     len = a.n1_ptr[b];
   const int chunk = (len + a.splits - 1) / a.splits;
@@ -581,7 +581,7 @@ static cudaError_t launch_partial(const DecodeAttnArgs& a, int width, const uint
 // v2 (decode_attn2.cu) is the default for the separate-kernel decode path (B > 8, token-split
 // layers): 8-warp pipelined CTAs, ~30 % faster than v1 at config 3 (profiles/r01/NOTES.md);
 // ZDC_DEC_ATTN_V2=0 selects v1
-static const bool g_dec_attn_v2 = !(getenv("ZDC_DEC_ATTN_V2") && atoi(getenv("ZDC_DEC_ATTN_V2")) == 0);
+static const bool g_dec_attn_v2 = knob("ZDC_DEC_ATTN_V2", 1) != 0;
 static bool v2_width(int w) { return w == 32 || w == 64 || w == 96 || w == 128; }
 
 cudaError_t launch_decode_attention(const DecodeAttnArgs& a_in, cudaStream_t stream) {

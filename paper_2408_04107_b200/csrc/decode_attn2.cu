@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kNW * 32)
   const bool uniform = a.n0_ptr == nullptr;
   int pre_tiles = 0;
   if (uniform && a.prefetch_before_wait) {
-    const int len0 = a.len_ptr ? *a.len_ptr + 1 : a.len;
+    const int len0 = a.len_ptr ? min(*a.len_ptr + 1, a.S_cap) : a.len;
     int w0, w1;
     ranges(len0, w0, w1);
     const int ntile = (w1 - w0 + C::TR - 1) / C::TR;
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(kNW * 32)
   pdl_wait();
   int len;
   if (pool == 0)
-    len = a.n0_ptr ? a.n0_ptr[b] : (a.len_ptr ? *a.len_ptr + 1 : a.len);
+    len = a.n0_ptr ? a.n0_ptr[b] : (a.len_ptr ? min(*a.len_ptr + 1, a.S_cap) : a.len);
   else
     len = a.n1_ptr[b];
   int w0, w1;
@@ -311,7 +311,7 @@ static int ctas_per_sm_g(int width) {
 
 // Split count: as many CTAs as fit in ONE wave (occupancy x SMs), >= 32 rows per warp.
 int decode2_splits(int B, int Nkv, int len, int width, int G) {
-  static const int forced = getenv("ZDC_V2_SPLITS") ? atoi(getenv("ZDC_V2_SPLITS")) : 0;  // A/B override
+  static const int forced = knob("ZDC_V2_SPLITS", 0);  // A/B override
   if (forced > 0) return forced > 64 ? 64 : forced;
   int fit = 1;
   switch (G) {

@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(192, DTC<HD, STG>::CPS)
   // Q' (written by the a1 projection) and the cache length are only read after the PDL wait
   pdl_wait();
   pdl_trigger();
-  const int len1 = *a.len_ptr + 1;  // cached rows incl. the new token's (appended by a1)
+  const int len1 = min(*a.len_ptr + 1, a.S_cap);  // cached rows incl. the new token's (appended by a1)
   int chunk = (len1 + a.splits - 1) / a.splits;
   chunk = (chunk + 127) / 128 * 128;
   const int n_items = a.B * a.Nkv * a.splits;
@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(192, DTC<HD, STG>::CPS)
 // otherwise the fewest that fill the persistent CTAs' last round to >= 90 % (each split keeping >= 2
 // key tiles at the capacity bound)
 int decode_tc_splits(int B, int Nkv, int len) {
-  static const int forced = getenv("ZDC_TC_SPLITS") ? atoi(getenv("ZDC_TC_SPLITS")) : 0;  // A/B override
+  static const int forced = knob("ZDC_TC_SPLITS", 0);  // A/B override
   if (forced > 0) return std::min(64, forced);
   const int pairs = B * Nkv, nsm = 2 * num_sms();  // resident CTAs at r = 64 (r = 128: a bound)
   if (pairs >= nsm) return 1;
@@ -443,7 +443,7 @@ static cudaError_t launch_tc_s(const DecodeAttnArgs& a, cudaStream_t stream) {
 }
 
 // stages per CTA (two CTAs per SM at r = 64): ZDC_TC_STAGES = 2 or 3 (default 2: c4 207.2 vs 209.0 us)
-static const int g_tc_stages = getenv("ZDC_TC_STAGES") ? atoi(getenv("ZDC_TC_STAGES")) : 2;
+static const int g_tc_stages = knob("ZDC_TC_STAGES", 2);
 template <int HD, int G>
 static cudaError_t launch_tc_t(const DecodeAttnArgs& a, cudaStream_t stream) {
   return g_tc_stages == 3 ? launch_tc_s<HD, G, 3>(a, stream) : launch_tc_s<HD, G, 2>(a, stream);

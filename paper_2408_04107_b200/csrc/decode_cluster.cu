@@ -35,7 +35,7 @@ int decode_cluster_size(int B, int RK, int G, int Nkv, int d) {
   if (!decode_cluster_supported(B, RK, G) || Nkv < 1) return 0;
   static std::mutex mu;
   static std::map<std::tuple<int, int, int, int, int, int>, int> cap;  // (NB, RK, G, C, Nkv, d) -> resident clusters
-  const int forced = getenv("ZDC_DEC_CLUSTER_C") ? atoi(getenv("ZDC_DEC_CLUSTER_C")) : 0;
+  const int forced = knob("ZDC_DEC_CLUSTER_C", 0);
   std::lock_guard<std::mutex> lk(mu);
   for (int C = 8; C >= 1; C >>= 1) {
     if (forced > 0 && C != forced) continue;

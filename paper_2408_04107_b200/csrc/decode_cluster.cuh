@@ -406,7 +406,9 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     pdl_trigger();
     if (tid == 0) {
       ZDC_STAMP(14);
-      *s_len = *a.len_ptr;
+      const int L0 = *a.len_ptr;
+      *s_len = min(L0, a.S_cap - 1);  // a full cache rewrites its last row (flagged)
+      if (L0 >= a.S_cap && a.err) *a.err = 1;
       mbar_arrive(lenbar);
       mbar_arrive_expect_tx(xbar1, static_cast<uint32_t>(C * a.B * NV1 * 4));
       mbar_arrive_expect_tx(xbar2, static_cast<uint32_t>(C * a.B * G * (RK + 2) * 4));

@@ -11,8 +11,8 @@ cudaError_t launch_fused_b4(const DecFusedArgs& a, int RK, int G, cudaStream_t s
 cudaError_t launch_fused_b8(const DecFusedArgs& a, int RK, int G, cudaStream_t s);
 
 int decode_fused_splits(int B, int Nkv) {
-  static const int forced = getenv("ZDC_FUSED_SPLITS") ? atoi(getenv("ZDC_FUSED_SPLITS")) : 0;  // A/B override
-  if (forced > 0) return forced;
+  static const int forced = knob("ZDC_FUSED_SPLITS", 0);  // A/B override (capped like the default)
+  if (forced > 0) return forced > 128 ? 128 : forced;
   int s = num_sms() / (B * Nkv);
   if (s > 128) s = 128;
   return s < 1 ? 1 : s;
@@ -28,7 +28,7 @@ unsigned long long* fused_trace_buffer() {
   static bool init = false;
   if (!init) {
     init = true;
-    if (getenv("ZDC_FUSED_TRACE") && cudaMalloc(&buf, 1024 * 16 * 8) != cudaSuccess) buf = nullptr;
+    if (knob("ZDC_FUSED_TRACE", 0) && cudaMalloc(&buf, 1024 * 16 * 8) != cudaSuccess) buf = nullptr;
     if (buf) cudaMemset(buf, 0, 1024 * 16 * 8);
   }
   return buf;

@@ -305,6 +305,7 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
   const int tl = a.nl > 1 ? 1 : 0;  // layer whose timeline the trace records
 
   if (warp == kNW) {
+    pdl_trigger();  // every thread of the CTA triggers: the dependent launch may become resident now
     // ================= producer (one thread): every HBM byte of this CTA, in consumption order,
     // layer after layer: while the consumers finish layer l, the ring fills with layer l+1's W_QKV
     if (lane == 0) {
@@ -364,7 +365,12 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
   pdl_wait();
   pdl_trigger();
   if (tid == 0) {
-    for (int li = 0; li < a.nl; ++li) s_lens[li] = *a.layers[li].len_ptr;
+    for (int li = 0; li < a.nl; ++li) {
+      const int L0 = *a.layers[li].len_ptr;
+      // a full cache (graph replays past max_seq) rewrites its last row instead of writing past it
+      s_lens[li] = min(L0, a.S_cap - 1);
+      if (L0 >= a.S_cap && cta == 0 && a.err) *a.err = 1;
+    }
     *s_base = ld_acquire_u64(a.gbar) / ncta * ncta;
     mbar_arrive(lenbar);
   }
@@ -462,6 +468,7 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
       for (int t = (warp - kb % kNW + kNW) % kNW; t < ns; t += kNW) {
         const int s = cc.slot();
         mbar_wait(&full[s], cc.ph);
+        if (tid == 0 && li == tl && it == cta && t < kNW) ZDC_STAMP(14);
         cc.next();
         const uint16_t* Ks = reinterpret_cast<const uint16_t*>(ring + static_cast<size_t>(s) * SB);
         const int nr = min(RPS, e0 - (s0 + t * RPS));
@@ -612,6 +619,7 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
     for (int t = (warp - kb % kNW + kNW) % kNW; t < n3; t += kNW) {
       const int s = cc.slot();
       mbar_wait(&full[s], cc.ph);
+      if (tid == 0 && li == tl && t < kNW) ZDC_STAMP(15);
       cc.next();
       const int rb = r3a + t * rps3, nr = min(rps3, r3b - rb);
       int r = 0;
@@ -652,14 +660,14 @@ __global__ void __launch_bounds__(kNC + 32, 1) decode_fused_kernel(const DecFuse
 
 // ------------------------------------------------------------------ host
 // ring cap (ZDC_FUSED_RING_KB); the launcher fits as many slots as the 227 KB of shared memory allow
-static const int kFusedRingBytes = getenv("ZDC_FUSED_RING_KB") ? atoi(getenv("ZDC_FUSED_RING_KB")) * 1024 : 224 * 1024;
+static const int kFusedRingBytes = knob("ZDC_FUSED_RING_KB", 224) * 1024;
 
 template <int NB, int RK, int G>
 inline cudaError_t launch_fused_t(DecFusedArgs a, cudaStream_t stream) {
   // slot: a multiple of the a1 row, of 32 K'+V' rows and of the a5 row; larger slots (fewer, bigger
   // bulk copies in flight) stream faster from HBM (tools/stream_probe.cu)
   int slot = std::max(std::max(a.d * 2, 4 * 32 * RK), a.ko_p * 2);
-  static const int slot_kb = getenv("ZDC_FUSED_SLOT_KB") ? atoi(getenv("ZDC_FUSED_SLOT_KB")) : 0;
+  static const int slot_kb = knob("ZDC_FUSED_SLOT_KB", 0);
   if (slot_kb * 1024 > slot) {
     const int unit = std::max(std::max(a.d * 2, a.ko_p * 2), 4 * 32 * RK);
     slot = std::max(slot, slot_kb * 1024 / unit * unit);

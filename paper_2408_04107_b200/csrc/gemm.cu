@@ -22,9 +22,9 @@
 namespace zdc {
 
 int64_t g_launches = 0;
-bool g_pdl = getenv("ZDC_NO_PDL") == nullptr;  // A/B switch for programmatic dependent launch
+bool g_pdl = knob("ZDC_NO_PDL", 0) == 0;  // A/B switch for programmatic dependent launch
 // which decode kernels launch with PDL: bit 0 projections (GEMV), bit 1 attention
-int g_pdl_mask = getenv("ZDC_PDL_MASK") ? atoi(getenv("ZDC_PDL_MASK")) : 3;
+int g_pdl_mask = knob("ZDC_PDL_MASK", 3);
 int g_prof_class = kProfOther;
 
 // ------------------------------------------------------------------ host: per-class event timing
@@ -144,7 +144,7 @@ __device__ __forceinline__ void store_unit(const Epilogue& e, int m, int n, uint
       dst = q.q + static_cast<int64_t>(m) * q.ldq + n;
     } else {
       const int b = m / q.S, t = m - (m / q.S) * q.S;
-      const int pos = q.posmap ? q.posmap[t] : (q.pos_ptr ? *q.pos_ptr : q.pos0) + t;
+      const int pos = q.posmap ? q.posmap[t] : (q.pos_ptr ? min(*q.pos_ptr, q.pos_cap - 1) : q.pos0) + t;
       if (n < q.nq + q.nk) {
         const int nn = n - q.nq, g = nn / q.rk, c = nn - g * q.rk;
         dst = q.k + b * q.kb + g * q.kg + static_cast<int64_t>(pos) * q.rk + c;
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(256, 1)
   // output waits for it; the producer first requests the weight (B) tiles of the ring's first
   // stages, which do not depend on it (griddepcontrol.wait is a no-op without PDL).
   if (warp != 0) pdl_wait();
-  if (epi.len_inc && blockIdx.x == 0 && threadIdx.x == 4 * 32) *epi.len_inc += 1;
+  if (epi.len_inc && blockIdx.x == 0 && threadIdx.x == 4 * 32) advance_len(epi);
   if (warp == 0) {
     // ---------------- TMA producer
     if (elect_one()) {
@@ -486,8 +486,8 @@ cudaError_t launch_gemm(const uint16_t* A, int64_t lda, const uint16_t* B, int64
   ep.k_splits = 1;
   // skinny M (decode, B > 8): ZDC_SKINNY_KB=2 fetches 2 k-blocks per stage with one 3-D box (measured
   // no faster than 1 under ncu: 35 vs 32 us at the c4 a1 shape; profiles/r01/NOTES.md)
-  static const int skinny_kb = getenv("ZDC_SKINNY_KB") ? atoi(getenv("ZDC_SKINNY_KB")) : 1;
-  static const int skinny_bn = getenv("ZDC_SKINNY_BN") ? atoi(getenv("ZDC_SKINNY_BN")) : 0;
+  static const int skinny_kb = knob("ZDC_SKINNY_KB", 1);
+  static const int skinny_bn = knob("ZDC_SKINNY_BN", 0);
   const bool skinny = epi.ws && epi.ws_cnt && M <= 128 && N % 8 == 0;
   const int KBs = skinny && skinny_kb == 2 && K % 128 == 0 ? 2 : 1;
   // skinny: BN = 128 when 256-wide tiles would be few (< 40: c4 a1 20, a5 32 tiles; 128 measured 4 % faster
@@ -506,7 +506,7 @@ cudaError_t launch_gemm(const uint16_t* A, int64_t lda, const uint16_t* B, int64
   // N-fastest raster for a large A: concurrent CTAs share A rows (read once from HBM) while the
   // weights B stay L2-resident; the default M-fastest order re-reads A once per N-tile (c4 prefill
   // a1: 174 GB of DRAM reads for 8.7 GB of operands, ncu).  ZDC_GEMM_RASTER=0/1 forces it.
-  static const int raster_env = getenv("ZDC_GEMM_RASTER") ? atoi(getenv("ZDC_GEMM_RASTER")) : -1;
+  static const int raster_env = knob("ZDC_GEMM_RASTER", -1);
   const double a_bytes = static_cast<double>(M) * K * 2, b_bytes = static_cast<double>(N) * K * 2;
   // band: the N-blocks whose weight tiles fit ~40 MB of L2 (ZDC_GEMM_RASTER=0 keeps M-fastest,
   // = n forces a band of n)

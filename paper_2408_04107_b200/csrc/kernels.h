@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "knobs.h"
+
 namespace zdc {
 
 // Where the a1 projection writes its outputs: Q' to a staging matrix,
@@ -22,6 +24,7 @@ struct QkvDest {
   int64_t kb = 0, kg = 0, vb = 0, vg = 0;  // element strides per sequence / per KV head
   int pos0 = 0;
   const int* pos_ptr = nullptr;  // if set, pos0 is read from device memory (graph-replayable decode)
+  int pos_cap = 0;               // with pos_ptr: rows per (sequence, KV head); *pos_ptr is clamped to pos_cap - 1
   const int* posmap = nullptr;
 };
 
@@ -31,6 +34,8 @@ struct Epilogue {
   int64_t ldd = 0;
   QkvDest qkv;
   int* len_inc = nullptr;  // if set, the kernel increments *len_inc once (decode: advances the layer length)
+  int len_cap = 0;         // ... saturating at len_cap: a step with *len_inc >= len_cap sets *err instead
+  int* err = nullptr;      // device overflow flag (reported by zdc_cache_sync)
   // split-K for skinny M (M <= 128, few output tiles: decode at B > 8): fp32 workspace [M][N] and
   // per-tile arrival counters, both zero between launches; the last split of a tile applies the
   // epilogue above to the summed tile.  k_splits is chosen by launch_gemm when ws is set.
@@ -40,6 +45,19 @@ struct Epilogue {
   int pdl = 0;  // launch with programmatic dependent launch (decode chains)
   int raster_n = 0;  // tile order: 0 M-fastest; n > 0 bands of n N-blocks, N fastest (launch_gemm, large A)
 };
+
+#ifdef __CUDACC__
+// Decode length advance (one thread, after every reader of the old length): saturates at len_cap;
+// a step that found the cache full sets the overflow flag instead (zdc_cache_sync reports it).
+__device__ __forceinline__ void advance_len(const Epilogue& e) {
+  const int v = *e.len_inc;
+  if (e.len_cap > 0 && v >= e.len_cap) {
+    if (e.err) *e.err = 1;
+  } else {
+    *e.len_inc = v + 1;
+  }
+}
+#endif
 
 // ---- tensor maps (driver entry point resolved at runtime; no -lcuda link)
 bool make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner_elems, uint64_t outer_rows,
@@ -156,6 +174,7 @@ struct DecFusedArgs {
   int slot_bytes = 0, spw = 0, ring_extra = 0, xw = 0, rps = 32;
   int stage_part = 0, pst_floats = 0;
   int64_t pst_bytes = 0;
+  int* err = nullptr;                   // device overflow flag: a step found *len_ptr >= S_cap
 };
 bool decode_fused_supported(int B, int RK, int G);
 int decode_fused_splits(int B, int Nkv);
@@ -173,6 +192,7 @@ struct DecClusterArgs {
   uint16_t* kc = nullptr;          // K'/V' cache: row (b, g, p) at ((b*Nkv+g)*S_cap + p)*RK
   uint16_t* vc = nullptr;
   int* len_ptr = nullptr;          // cached rows before this step; advanced by the kernel
+  int* err = nullptr;              // device overflow flag: a step found *len_ptr >= S_cap
   const uint16_t* x = nullptr;     // [B][ldx]
   int64_t ldx = 0;
   uint16_t* y = nullptr;           // [B][ldy]

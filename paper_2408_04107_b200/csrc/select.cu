@@ -209,6 +209,7 @@ __global__ void append_kernel(const uint16_t* __restrict__ knew, const uint16_t*
                               int is_rep) {
   const int b = blockIdx.x;
   const int t = *len_ptr;
+  if (t >= S_cap) return;  // cache full (graph replays past max_seq): the a5 length advance flags it
   const bool imp = is_rep || rep_cls[b * ld_cls + t];
   const int idx = imp ? n_i[b] : n_u[b];
   __syncthreads();
@@ -253,6 +254,7 @@ __global__ void classify_kernel(const float* __restrict__ lse, int Nh, int mode,
                                 int* __restrict__ pos_i, int* __restrict__ pos_u, const int* __restrict__ len_ptr) {
   const int b = blockIdx.x;
   const int t = *len_ptr;
+  if (t >= S_cap) return;  // cache full: nothing was appended
   __shared__ int s_imp;
   if (threadIdx.x == 0) {
     const float adj = mode == 1 ? logf(static_cast<float>(t) + 1.0f) : 0.f;

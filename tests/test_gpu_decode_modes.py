@@ -158,3 +158,47 @@ def test_decode_in_caller_graph_and_cache_sync(mode):
     ctx.cache_sync(s)
     assert ctx.cache_length(0) == T and ctx.cache_length(1) == T
     ctx.close()
+
+
+@pytest.mark.parametrize("mode,dims,B", [("fused", Dims(1, 256, 4, 4, 64), 2), ("cluster", Dims(1, 256, 4, 4, 64), 2),
+                                         ("separate", Dims(1, 256, 4, 4, 64), 2),
+                                         ("auto", Dims(1, 512, 16, 2, 64), 10)],   # GEMM + TC attention path
+                         indirect=["mode"])
+def test_decode_graph_replays_past_max_seq_are_flagged(mode, dims, B):
+    """Each replay of a caller-captured decode graph uses one cache row.  Replaying past max_seq
+    must not write outside the layer's rows: the overflowing steps rewrite the last row, the length
+    saturates at max_seq and zdc_cache_sync reports ZDC_ERR_CAPACITY."""
+    import paper_2408_04107_b200 as zdc
+    r = 64 if dims.n_kv_heads == 2 else 32
+    plan = plan_uniform(1, r)
+    _, folded = fold_stack(dims, 1, n_calib=256)
+    cap = 6
+    x = Z.prompt(dims, 1, B, cap + 6, seed=25)
+    ctx = make_context(dims, plan, folded, B, cap)
+    s = torch.cuda.Stream()
+    xb = torch.empty(B, dims.d_model, device="cuda", dtype=torch.bfloat16)
+    yb = torch.empty_like(xb)
+    with torch.cuda.stream(s):
+        xb.copy_(to_dev_bf16(x[:, 0]))
+        ctx.decode(xb, yb)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            ctx.decode(xb, yb)
+        for t in range(1, cap + 6):
+            xb.copy_(to_dev_bf16(x[:, t]))
+            g.replay()
+    s.synchronize()
+    with pytest.raises(zdc.ZdcError) as e:
+        ctx.cache_sync(s)
+    assert e.value.status == -5
+    assert ctx.cache_length(0) == cap
+    # rows 0 .. cap-2 still hold tokens 0 .. cap-2 of every (sequence, KV head): nothing spilled
+    # into a neighbouring block
+    k, v, _, _ = ctx.cache_export(0, B)
+    m = O.OracleModel(dims, plan, folded, faithful=True)
+    m.prefill(x[:, :cap - 1])
+    assert normwise(k[:, :cap - 1].transpose(0, 2, 1, 3), m.K[0]) <= 1e-2
+    assert normwise(v[:, :cap - 1].transpose(0, 2, 1, 3), m.V[0]) <= 1e-2
+    ctx.reset(s)
+    ctx.cache_sync(s)
+    ctx.close()

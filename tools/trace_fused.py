@@ -1,7 +1,10 @@
 """Timeline of the fused decode kernel (ZDC_FUSED_TRACE=1): per-CTA globaltimer stamps of the
 last launch, summarised as min / median / max microseconds after the earliest CTA start.
+Needs the diagnostic build (knobs read from the environment, csrc/knobs.h):
 
-    ZDC_FUSED_TRACE=1 python tools/trace_fused.py [--layers 4] [--ctx 2048] [--batch 1]
+    ZDC_BUILD_VARIANT=debug ZDC_BUILD_DEFS=-DZDC_DEBUG_KNOBS python -m paper_2408_04107_b200.build
+    ZDC_LIB_PATH=$PWD/paper_2408_04107_b200/libzdc_debug.so ZDC_FUSED_TRACE=1 \
+        python tools/trace_fused.py [--layers 4] [--ctx 2048] [--batch 1]
 """
 import argparse
 import math
@@ -17,7 +20,7 @@ import zdc_synth as Z  # noqa: E402
 
 NAMES = {0: "kernel start", 13: "layer start", 1: "x staged", 2: "phase1 done", 3: "barrier1 out", 4: "phase2 done", 5: "barrier2 out",
          6: "merge done", 7: "end", 8: "prod: ph1 issued", 9: "prod: ph2 issued", 10: "prod: all issued",
-         11: "ph2 rows done / cl: ph3 done", 12: "partials staged", 13: "layer start", 14: "cl: after pdl wait"}
+         11: "ph2 rows done / cl: ph3 done", 12: "partials staged", 13: "layer start", 14: "first KV slot ready", 15: "first W_O slot ready"}
 
 
 def main():
