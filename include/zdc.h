@@ -208,7 +208,12 @@ zdc_status zdc_cache_length(const zdc_ctx* ctx, int32_t layer, int32_t* len);
  * every position); the host keeps a copy for argument checks and the inspection calls, advanced by
  * each zdc_prefill / zdc_decode call.  A caller that replays zdc_decode calls inside its OWN captured
  * CUDA graph calls zdc_cache_sync afterwards: it copies the device lengths back (synchronises
- * `stream`).  ZDC_ERR_STATE if the ctx is not bound. */
+ * `stream`).  ZDC_ERR_STATE if the ctx is not bound.
+ * Capacity: every replayed decode step uses one cache row; only the host-side check at capture time
+ * sees max_seq, so the caller bounds its replay count.  A step that finds the cache full does not
+ * write outside the layer's rows: it rewrites the last row, the length stays at max_seq and a
+ * device overflow flag is set; zdc_cache_sync then returns ZDC_ERR_CAPACITY (the outputs of the
+ * overflowing steps are invalid) until zdc_cache_reset clears it. */
 zdc_status zdc_cache_sync(zdc_ctx* ctx, void* stream);
 /* Importance scores (reading c9: log of sum_h sum_{k<=t} exp(s_k^h), f32 as computed on the GPU)
  * of every cached token of a representative layer of a split group: scores [B][len], host. */
@@ -254,7 +259,7 @@ zdc_status zdc_gemv_bf16(const uint16_t* w, const uint16_t* x, uint16_t* y, int3
  * attention, GEMV).  Returns the previous mode; -1 for an invalid mode.
  * Mode 2 must be selected before zdc_ctx_create: the cluster kernel streams decode copies of the
  * weights (pre-tiled W_QKV, group-major W_O) that zdc_ctx_sizes then counts and zdc_load_folded
- * fills.  Env ZDC_DECODE_MODE sets the initial mode. */
+ * fills.  The initial mode is 0 (release builds read no environment variables). */
 int zdc_decode_mode(int mode);
 
 /* Number of kernels the last prefill / decode call enqueued (for bench.py's gpu_launches). */
@@ -269,7 +274,8 @@ int64_t zdc_kernel_launch_count(void);
  * 8 fused decode layer-step (a1+a2+a3+a5 in one kernel, B <= 8 uniform-rank layers). */
 void zdc_profile(int enable);
 int zdc_profile_read(float* ms, int64_t* count, int n);
-/* Diagnostics: with ZDC_FUSED_TRACE set in the environment, the fused decode kernel records
+/* Diagnostics (diagnostic builds only, -DZDC_DEBUG_KNOBS, csrc/knobs.h; release builds return 0):
+ * with ZDC_FUSED_TRACE set in the environment, the fused decode kernel records
  * per-CTA %globaltimer stamps (ns) of its last launch, [CTA][16]: 0 start, 1 input staged,
  * 2 phase-1 done, 3 after grid barrier 1, 4 phase-2 done, 5 after grid barrier 2, 6 merge done,
  * 7 end, 8/9/10 producer finished issuing phase 1/2/3.  Copies n values (synchronising the
