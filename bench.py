@@ -47,7 +47,9 @@ CONFIG_NAME = "c2_llama2_7b"
 
 def parse():
     p = argparse.ArgumentParser()
-    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--gpus", type=int, default=1,
+                   help="GPUs of this node; without WORLD_SIZE in the environment bench.py launches itself "
+                        "once per GPU through torch.distributed.run (127.0.0.1 rendezvous)")
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="zdc", choices=["zdc", "reference"])
@@ -58,7 +60,8 @@ def parse():
     p.add_argument("--decode-calls", default="layer", choices=["layer", "chain"],
                    help="decode step as 32 per-layer zdc_decode calls (same x per layer) or one chained call")
     p.add_argument("--decode-mode", default="auto", choices=["auto", "fused", "cluster", "separate"],
-                   help="decode kernels for B <= 8 (zdc_decode_mode): auto = cluster layer-step when it fits")
+                   help="decode kernels for B <= 8 (zdc_decode_mode): auto = persistent fused layer-step where "
+                        "supported")
     p.add_argument("--configs", default="c3,c4",
                    help="per-layer prefill/decode measurements of these configs at N = 1 ('' to skip)")
     p.add_argument("--sp-seq", type=int, default=32768, help="SP prefill prompt length (c5), run when N > 1")
@@ -66,8 +69,12 @@ def parse():
     p.add_argument("--sp", action="store_true", help="also run the SP prefill at N = 1 (P = 1, no exchange)")
     p.add_argument("--no-sp", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-uncompressed", action="store_true",
+                   help="skip the r = d_h (R = I) baseline and the torch SDPA / matmul comparison")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--profile-only", action="store_true", help="one eager step (for ncu), no JSON")
+    p.add_argument("--launch-probe", action="store_true",
+                   help="test hook: each rank joins a gloo group, all-reduces its rank and prints one JSON line")
     return p.parse_args()
 
 
@@ -158,7 +165,9 @@ class ClockSampler:
 def oracle_sample(n_decode: int = 16, prompt: int = 2048):
     """The fp64 oracle as it stands, on a bounded sample of the c2 workload: one layer's fold
     (untimed, like the GPU path's), one layer prefill of the full prompt, n_decode decode steps.
-    Returns (seconds_prefill_layer, seconds_per_decode_layer_step, cores)."""
+    BLAS threads are pinned (threadpoolctl) to the CPUs this process may run on.
+    Returns (seconds_prefill_layer, seconds_per_decode_layer_step, cores) with cores =
+    {"threads": BLAS threads used, "affinity": len(sched_getaffinity), "cpu_count": os.cpu_count()}."""
     import numpy as np
     import oracle as O
     import zdc_synth as Z
@@ -169,19 +178,17 @@ def oracle_sample(n_decode: int = 16, prompt: int = 2048):
     folded = O.fold_layer(dims, w.wq, w.wk, w.wv, w.wo, xc)
     x = Z.prompt(dims, 2, 1, prompt, seed=21)
     m = O.OracleModel(dims, plan, [folded])
-    t0 = time.perf_counter()
-    m.prefill(x)
-    t1 = time.perf_counter()
-    for s in range(n_decode):
-        m.decode(Z.decode_input(dims, 2, 1, s))
-    t2 = time.perf_counter()
-    cores = len(os.sched_getaffinity(0))
-    try:
-        from threadpoolctl import threadpool_info
+    aff = len(os.sched_getaffinity(0))
+    from threadpoolctl import threadpool_info, threadpool_limits
+    with threadpool_limits(limits=aff):
         nthreads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
-        cores = nthreads
-    except Exception:
-        pass
+        t0 = time.perf_counter()
+        m.prefill(x)
+        t1 = time.perf_counter()
+        for s in range(n_decode):
+            m.decode(Z.decode_input(dims, 2, 1, s))
+        t2 = time.perf_counter()
+    cores = {"threads": nthreads, "affinity": aff, "cpu_count": os.cpu_count()}
     return t1 - t0, (t2 - t1) / n_decode, cores
 
 
@@ -292,12 +299,20 @@ def run_reference(args):
     tp = statistics.median(v[0] for v in vals)
     td = statistics.median(v[1] for v in vals)
     v, step_s = oracle_step_tok_s(tp, td, L, S, T)
-    sample = "per step: 1 layer fp64 prefill of S=%d + 4 decode steps (oracle/), extrapolated x%d layers, %d decode steps" % (S, L, T)
+    sample = ("per step: 1 layer fp64 prefill of S=%d + 4 decode steps (oracle/); value extrapolated to %d layers "
+              "x (prefill + %d decode steps) = %.1f s per full-workload step" % (S, L, T, step_s))
+    sample_ms = (tp + 4 * td) * 1e3  # the timed part of one sample (prefill + 4 decode steps)
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tok/s", "n_gpus": args.gpus,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+           "steps": args.steps, "warmup": args.warmup,
+           # what was actually timed per step (the bounded sample, incl. its untimed fold); the
+           # full-workload step time behind `value` is an extrapolation, labelled as such
+           "ms_per_step": sample_ms,
+           "ms_per_step_kind": "measured: the timed part of one bounded sample (1 layer prefill + 4 decode steps)",
+           "ms_per_full_step_extrapolated": step_s * 1e3, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": CONFIG_NAME, "layers": L, "prompt": S, "decode_steps": T, "batch": 1, "rank": 64},
-           "cpu_baseline": {"value": v, "unit": "tok/s", "cores": cores, "kind": "oracle", "sample": sample},
+           "cpu_baseline": {"value": v, "unit": "tok/s", "cores": cores["threads"], "cores_detail": cores,
+                            "kind": "oracle", "sample": sample},
            "e2e": {"value": v, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -518,6 +533,142 @@ def config_bench(args, zdc, torch, dev, stream, cid, n_layers=4, T=48):
     del x, y, xd
     torch.cuda.empty_cache()
     return out
+
+
+# ------------------------------------------------------------------------------------ r = d_h baseline
+def _timing_weights(torch, dev, g, d, nh, nkv, dh):
+    """Timing-only unfolded weights (the decaying-spectrum recipe of zdc_synth, generated on the device)."""
+    sv = torch.tensor([10.0 ** (-2.0 * j / (dh - 1)) for j in range(dh)], device=dev)
+    a = (4.0 * dh / float((sv ** 4).sum())) ** 0.25
+    bta = math.sqrt(dh / float((sv ** 2).sum()))
+    gam = math.sqrt(dh / (nh * float((sv ** 2).sum())))
+    wq = (torch.randn(d, nh, dh, device=dev, generator=g) * (a * sv / math.sqrt(d))).reshape(d, nh * dh)
+    wk = (torch.randn(d, nkv, dh, device=dev, generator=g) * (a * sv / math.sqrt(d))).reshape(d, nkv * dh)
+    wv = (torch.randn(d, nkv, dh, device=dev, generator=g) * (bta * sv / math.sqrt(d))).reshape(d, nkv * dh)
+    wo = (torch.randn(nh, dh, d, device=dev, generator=g) * (gam * sv[:, None] / math.sqrt(d))).reshape(nh * dh, d)
+    return [t.to(torch.bfloat16).contiguous() for t in (wq, wk, wv, wo)]
+
+
+def uncompressed_bench(args, zdc, torch, dev, stream, pre_ms_r, dec_ms_r, dec_bytes_r):
+    """SURVEY.md §8(d) "Uncompressed baseline": the same kernels at r = d_h with R = I (folding with
+    the identity is exact, pin P10), i.e. the uncompressed model run through the library, timed the
+    same way as the c2 step (CUDA graphs of per-layer calls); plus each attention kernel alone at
+    r and at d_h -- the B200 analogue of the paper's "attention time saved".
+    Library comparison (report only, never on the product path): torch SDPA at head dim r / d_h and
+    torch.matmul at the c2 projection shapes."""
+    import torch.nn.functional as F
+    import zdc_synth as Z
+    L, S, T, r = args.layers, args.prompt, args.decode_steps, args.rank
+    base = Z.dims_of(2)
+    dims = Z.Dims(L, base.d_model, base.n_heads, base.n_kv_heads, base.d_head)
+    d, nh, nkv, dh = dims.d_model, dims.n_heads, dims.n_kv_heads, dims.d_head
+    ctx = zdc.Context(dims, Z.plan_uniform(L, dh), 1, S + T)
+    g = torch.Generator(device=dev).manual_seed(999)
+    for l in range(L):
+        ctx.load_folded_device(l, *_timing_weights(torch, dev, g, d, nh, nkv, dh))
+    xp = torch.randn(1, S, d, device=dev, generator=g).to(torch.bfloat16)
+    xd = torch.randn(T, 1, d, device=dev, generator=g).to(torch.bfloat16)
+    y = torch.empty_like(xp)
+    xb = torch.empty(1, d, device=dev, dtype=torch.bfloat16)
+    yb = torch.empty_like(xb)
+    for l in range(L):  # warm-up (kernel attributes, decode graphs)
+        ctx.prefill(xp, y, l, l + 1)
+    for l in range(L):
+        ctx.decode(xd[0], yb, l, l + 1)
+    ctx.reset()
+    gp = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gp, stream=stream):
+        for l in range(L):
+            ctx.prefill(xp, y, l, l + 1)
+    gd = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gd, stream=stream):
+        for l in range(L):
+            ctx.decode(xb, yb, l, l + 1)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    pre, dec = [], []
+    for i in range(1 + max(1, args.steps)):
+        ctx.reset()
+        torch.cuda.synchronize()
+        ev[0].record(stream)
+        gp.replay()
+        ev[1].record(stream)
+        for t in range(T):
+            xb.copy_(xd[t])
+            gd.replay()
+        ev[2].record(stream)
+        torch.cuda.synchronize()
+        if i:
+            pre.append(ev[0].elapsed_time(ev[1]))
+            dec.append(ev[1].elapsed_time(ev[2]))
+    ctx.close()
+    pre_ms, dec_ms = statistics.median(pre), statistics.median(dec)
+    avg_ctx = int(S + (T + 1) / 2.0)
+    dec_bytes_u = sum(decode_layer_bytes(d, nh, nkv, dh, 1, avg_ctx).values())
+    # each attention kernel alone at r and at d_h (CUDA graph of back-to-back launches)
+    attn = {}
+    for rr in sorted({r, dh}):
+        qa = torch.randn(1, S, nh * rr, device=dev, generator=g).to(torch.bfloat16)
+        ka = torch.randn(1, nkv, S + T, rr, device=dev, generator=g).to(torch.bfloat16)
+        va = torch.randn(1, nkv, S + T, rr, device=dev, generator=g).to(torch.bfloat16)
+        pa = torch.empty_like(qa)
+        la = torch.empty(1, nh, S, device=dev)
+        ks, vs = ka[:, :, :S].contiguous(), va[:, :, :S].contiguous()
+        t_pre = _time_graph(torch, stream, lambda i: zdc.prefill_attention_bf16(qa, ks, vs, pa, la,
+                                                                                scale=1.0 / math.sqrt(dh)), 10)
+        qd = torch.randn(1, nh * rr, device=dev, generator=g).to(torch.bfloat16)
+        od = torch.empty_like(qd)
+        ld = torch.empty(1, nh, device=dev)
+        wsp = zdc.decode_attention_bf16(qd, ka, va, od, avg_ctx, ld)
+        t_dec = _time_graph(torch, stream, lambda i: zdc.decode_attention_bf16(qd, ka, va, od, avg_ctx, ld,
+                                                                               workspace=wsp), 64)
+        # library comparison: torch SDPA (flash / cuDNN backend), causal, same scale
+        qs = qa.view(1, S, nh, rr).transpose(1, 2).contiguous()
+        kk = ks if nkv == nh else ks.repeat_interleave(nh // nkv, dim=1).contiguous()
+        vv = vs if nkv == nh else vs.repeat_interleave(nh // nkv, dim=1).contiguous()
+        try:
+            t_sdpa = _time_graph(torch, stream, lambda i: F.scaled_dot_product_attention(
+                qs, kk, vv, is_causal=True, scale=1.0 / math.sqrt(dh)), 10)
+        except Exception as e:  # reported only
+            t_sdpa = None
+        flop = prefill_layer_flops(d, nh, nkv, rr, 1, S)["a3"]
+        attn["r%d" % rr] = {"prefill_attention_us": round(t_pre * 1e3, 2),
+                            "prefill_attention_tflops": round(flop / (t_pre / 1e3) / 1e12, 1),
+                            "decode_attention_us": round(t_dec * 1e3, 2),
+                            "torch_sdpa_prefill_us": round(t_sdpa * 1e3, 2) if t_sdpa else None,
+                            "torch_sdpa_tflops": round(flop / (t_sdpa / 1e3) / 1e12, 1) if t_sdpa else None}
+        del qa, ka, va, pa, qs, kk, vv, ks, vs
+    # torch.matmul at the c2 projection shapes (report only)
+    mm = {}
+    for name, (M, N, K) in {"a1_qkv_r%d" % r: (S, nh * r + 2 * nkv * r, d), "a5_out_r%d" % r: (S, d, nh * r)}.items():
+        A = torch.randn(M, K, device=dev, generator=g).to(torch.bfloat16)
+        Bm = torch.randn(K, N, device=dev, generator=g).to(torch.bfloat16)
+        Wt = Bm.t().contiguous()
+        Cm = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+        t_mm = _time_graph(torch, stream, lambda i: torch.matmul(A, Bm, out=Cm), 10)
+        t_z = _time_graph(torch, stream, lambda i: zdc.gemm_bf16(A, Wt, Cm), 10)
+        fl = 2.0 * M * N * K
+        mm[name] = {"shape_MNK": [M, N, K], "torch_matmul_us": round(t_mm * 1e3, 2),
+                    "torch_matmul_tflops": round(fl / (t_mm / 1e3) / 1e12, 1),
+                    "zdc_gemm_us": round(t_z * 1e3, 2), "zdc_gemm_tflops": round(fl / (t_z / 1e3) / 1e12, 1)}
+        del A, Bm, Wt, Cm
+    torch.cuda.empty_cache()
+    ar, ad = attn["r%d" % r], attn["r%d" % dh]
+    return {
+        "what": "same kernels at r = d_h = %d with R = I (uncompressed model), c2 step timed as the headline" % dh,
+        "prefill_ms": round(pre_ms, 3), "decode_ms": round(dec_ms, 3),
+        "prefill_tok_s": S / (pre_ms / 1e3), "decode_tok_s": T / (dec_ms / 1e3),
+        "step_tok_s": (S + T) / ((pre_ms + dec_ms) / 1e3),
+        "speedup_compressed_vs_uncompressed": {"prefill": round(pre_ms / pre_ms_r, 3), "decode": round(dec_ms / dec_ms_r, 3),
+                                               "step": round((pre_ms + dec_ms) / (pre_ms_r + dec_ms_r), 3)},
+        "decode_bytes_per_layer_step": {"r%d" % r: dec_bytes_r, "r%d" % dh: dec_bytes_u,
+                                        "ratio": round(dec_bytes_r / dec_bytes_u, 4)},
+        "sp_exchange_bytes_ratio": r / dh,
+        "attention_time_saved": {"prefill": round(1.0 - ar["prefill_attention_us"] / ad["prefill_attention_us"], 4),
+                                 "decode": round(1.0 - ar["decode_attention_us"] / ad["decode_attention_us"], 4),
+                                 "paper": "21-28% -> 62-64% of attention time saved at p 0.3 -> 0.7 (PAPER.md:1971, A100)"},
+        "attention_kernels": attn, "library_comparison_matmul": mm,
+        "note": "library numbers are reported only; the product path never calls torch SDPA or matmul",
+    }
 
 
 # ------------------------------------------------------------------------------------ zdc arm
@@ -750,12 +901,21 @@ def run_zdc(args):
             except Exception as e:  # reported, never hides the main line
                 other[name] = {"error": "%s: %s" % (type(e).__name__, e)}
 
+    # ---- uncompressed r = d_h baseline + library comparison (report only), N = 1
+    unc = None
+    if world == 1 and not args.no_uncompressed:
+        log("uncompressed r = d_h baseline")
+        try:
+            unc = uncompressed_bench(args, zdc, torch, dev, stream, pre_ms[-1], dec_ms[-1], decode_layer_bytes)
+        except Exception as e:  # reported, never hides the main line
+            unc = {"error": "%s: %s" % (type(e).__name__, e)}
+
     # ---- CPU baseline (oracle as it stands), rank 0 at N=1 only
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         tp, td, cores = oracle_sample(n_decode=16, prompt=S)
         v, _ = oracle_step_tok_s(tp, td, L, S, T)
-        cpu = {"value": v, "unit": "tok/s", "cores": cores, "kind": "oracle",
+        cpu = {"value": v, "unit": "tok/s", "cores": cores["threads"], "cores_detail": cores, "kind": "oracle",
                "sample": "1 c2 layer fp64 prefill S=%d (%.2f s) + 16 decode steps (%.3f s/step), extrapolated to "
                          "%d layers x (prefill + %d decode steps)" % (S, tp, td, L, T)}
 
@@ -783,7 +943,7 @@ def run_zdc(args):
                 "note": "whole decode layer-step inside the graph-replayed step: algorithmic bytes (packed "
                         "weights + K'/V' at the average context + x/y) / measured time per layer-step"},
             "clocks": clocks, "gpu_launches": kernels_per_step * args.steps,
-            "e2e": e2e, "cpu_baseline": cpu, "sp": sp, "other_configs": other,
+            "e2e": e2e, "cpu_baseline": cpu, "sp": sp, "other_configs": other, "baseline_uncompressed": unc,
         }
         print(json.dumps(out), flush=True)
     ctx.close()
@@ -791,8 +951,44 @@ def run_zdc(args):
         dist.destroy_process_group()
 
 
+# ------------------------------------------------------------------------------------ launcher
+def launch_command(argv, n_gpus, port):
+    """`python bench.py --gpus N ...` without a torchrun environment: the same command once per GPU
+    of this node through torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n_gpus),
+            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + list(argv)
+
+
+def needs_launch(args, env) -> bool:
+    return args.gpus > 1 and "WORLD_SIZE" not in env
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def main():
     args = parse()
+    if needs_launch(args, os.environ):
+        cmd = launch_command(sys.argv[1:], args.gpus, _free_port())
+        log("launching %d ranks: %s" % (args.gpus, " ".join(cmd)))
+        sys.exit(subprocess.call(cmd))
+    if args.launch_probe:
+        import torch
+        import torch.distributed as dist
+        rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+        total = rank
+        if world > 1:
+            dist.init_process_group("gloo")
+            t = torch.tensor([rank])
+            dist.all_reduce(t)
+            total = int(t[0])
+            dist.destroy_process_group()
+        print(json.dumps({"rank": rank, "world": world, "rank_sum": total}), flush=True)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

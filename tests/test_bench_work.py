@@ -1,6 +1,10 @@
 """The algorithmic work bench.py divides by ("Algorithmic counts" and the
 per-kernel budget table): pinned to the figures §8(d) derives by hand for the configs."""
+import os
+
 import bench
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_c2_prefill_flops():
@@ -32,3 +36,31 @@ def test_c3_c4_weight_and_kv_bytes():
     b3 = bench.decode_layer_bytes(5120, 40, 40, 96, 32, 1)
     w3 = b3["a1"] - 32 * 5120 * 2 - 32 * 11520 * 2 + b3["a5"] - 32 * 3840 * 2 - 32 * 5120 * 2
     assert w3 == 157286400
+
+
+def test_bench_self_launch_command():
+    """`bench.py --gpus N` without torchrun's environment relaunches itself once per GPU."""
+    import argparse
+    ns = argparse.Namespace(gpus=4)
+    assert bench.needs_launch(ns, {})
+    assert not bench.needs_launch(ns, {"WORLD_SIZE": "4"})
+    assert not bench.needs_launch(argparse.Namespace(gpus=1), {})
+    cmd = bench.launch_command(["--gpus", "4", "--steps", "2"], 4, 29555)
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert cmd[cmd.index("--nproc-per-node") + 1] == "4"
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "2"]
+
+
+def test_bench_self_launch_gloo_world2():
+    """The real launcher path: two ranks rendezvous on 127.0.0.1 and all-reduce over gloo."""
+    import json
+    import subprocess
+    import sys
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--launch-probe"],
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    import re
+    lines = [json.loads(x) for x in re.findall(r"\{[^{}]*\}", out.stdout)]
+    assert sorted(x["rank"] for x in lines) == [0, 1]
+    assert all(x["world"] == 2 and x["rank_sum"] == 1 for x in lines)
