@@ -191,6 +191,31 @@ typedef struct {
 zdc_status zdc_sp_prefill(zdc_ctx* ctx, int32_t l0, int32_t l1, const uint16_t* x_local,
                           uint16_t* y_local, int32_t B, int32_t S_total, int32_t layout,
                           zdc_sp_stats* stats, void* stream);
+/* (4b) Ulysses SP prefill, the paper's own dataflow (§5.3, Fig. bkg:fig:all2all:
+ * "the four GPUs execute an all-to-all operation to gather tokens along the sequence dimension and
+ * distribute heads ... The resulting tensors undergo a second all-to-all operation to gather heads
+ * and sequence partitions"; "transmitting compressed Q, K, and V tensors in the first all-to-all
+ * communication significantly reduces communication time").  Same arguments, layouts and result
+ * rows as zdc_sp_prefill.  Per layer on rank p: a1 on the local tokens writes the compressed
+ * Q'/K'/V' as P per-destination slabs (rank q gets the N_h/P heads h in [q N_h/P, (q+1) N_h/P) and
+ * their N_kv/P KV groups) -> all-to-all #1 -> a3 (causal, full sequence) for rank p's heads ->
+ * all-to-all #2 of O' back to the token owners -> a5 on the local rows.  Bytes received per rank
+ * and layer: (P-1)/P * B S (N_h r_k + N_kv (r_k + r_v)) * 2 (#1) + (P-1)/P * B S N_h r_v * 2 (#2).
+ * Requires N_kv % P == 0 (ZDC_ERR_SHAPE); S_total divisible by P (contiguous) or 2P (zigzag); no
+ * 128-token chunk condition.  Each rank keeps the K'/V' cache of ITS KV groups for the whole
+ * sequence ([B][N_kv/P][max_seq][r] in the layer's cache region); zdc_decode / zdc_cache_export on
+ * such a layer return ZDC_ERR_UNSUPPORTED.  The NCCL transport is grouped ncclSend/ncclRecv on the
+ * caller's stream (zdc_comm_init); the test transport below replaces it. */
+zdc_status zdc_sp_prefill_ulysses(zdc_ctx* ctx, int32_t l0, int32_t l1, const uint16_t* x_local,
+                                  uint16_t* y_local, int32_t B, int32_t S_total, int32_t layout,
+                                  zdc_sp_stats* stats, void* stream);
+/* Test transport of the all-to-all: fn(user, send, recv, chunk_bytes, rank, world, stream) must make
+ * recv[q*chunk, (q+1)*chunk) equal rank q's send[rank*chunk, (rank+1)*chunk) for every q before
+ * returning (device buffers; P processes on ONE GPU in tests).  Keeps an all-gather hook / comm of
+ * the same rank and world. */
+typedef void (*zdc_alltoall_fn)(void* user, const void* send, void* recv, int64_t chunk_bytes, int32_t rank,
+                                int32_t world, void* stream);
+zdc_status zdc_sp_set_alltoall_hook(zdc_ctx* ctx, zdc_alltoall_fn fn, void* user, int32_t rank, int32_t world);
 /* Host helper: the global token positions rank `rank` holds (n = S_total / world). */
 zdc_status zdc_sp_positions(int32_t S_total, int32_t world, int32_t rank, int32_t layout,
                             int32_t* positions);

@@ -454,3 +454,18 @@ def sp_bytes_received(P: int, B: int, S: int, n_kv: int, r_k: int, r_v: int, ele
     (P-1)/P * B * S * N_kv * (r_k + r_v) * elem_bytes."""
     assert S % P == 0
     return (P - 1) * (S // P) * B * n_kv * (r_k + r_v) * elem_bytes
+
+
+def sp_bytes_received_ulysses(P: int, B: int, S: int, n_h: int, n_kv: int, r_k: int, r_v: int,
+                              elem_bytes: int = 2) -> int:
+    """Bytes one of P ranks receives per layer in the paper's Ulysses SP (Fig.
+    bkg:fig:all2all): all-to-all #1 delivers, from each of the P-1 peers, its S/P tokens' compressed
+    Q'/K'/V' columns of this rank's N_h/P heads and N_kv/P KV groups; all-to-all #2 delivers, from
+    each peer, that peer's heads' O' (r_v columns per head) for this rank's S/P tokens:
+    (P-1) * (B S / P) * [(N_h r_k + N_kv (r_k + r_v)) / P + N_h r_v / P] * elem_bytes."""
+    assert S % P == 0 and n_kv % P == 0 and n_h % P == 0
+    rows = B * (S // P)
+    cols1 = (n_h * r_k + n_kv * (r_k + r_v)) // P
+    cols2 = n_h * r_v // P
+    return (P - 1) * rows * (cols1 + cols2) * elem_bytes
+

@@ -30,6 +30,7 @@ EXPORTED_SYMBOLS = ["zdc_last_error", "zdc_version", "zdc_fold_weights", "zdc_ct
                     "zdc_ctx_bind", "zdc_ctx_destroy", "zdc_load_folded", "zdc_load_folded_device",
                     "zdc_prefill", "zdc_decode", "zdc_comm_unique_id", "zdc_comm_init",
                     "zdc_sp_set_exchange_hook", "zdc_sp_prefill", "zdc_sp_positions",
+                    "zdc_sp_prefill_ulysses", "zdc_sp_set_alltoall_hook",
                     "zdc_cache_export", "zdc_cache_length", "zdc_cache_sync", "zdc_scores_export", "zdc_cache_reset", "zdc_last_lse",
                     "zdc_gemm_bf16", "zdc_gemv_bf16", "zdc_prefill_attention_bf16",
                     "zdc_decode_attention_workspace", "zdc_decode_attention_bf16",
@@ -64,6 +65,9 @@ class SpStats(ctypes.Structure):
 # test transport of zdc_sp_set_exchange_hook: fn(user, gather_buf, chunk_bytes, rank, world, stream)
 EXCHANGE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
                                ctypes.c_int32, ctypes.c_void_p)
+# test transport of zdc_sp_set_alltoall_hook: fn(user, send, recv, chunk_bytes, rank, world, stream)
+ALLTOALL_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                               ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p)
 
 
 def lib_path() -> str:
@@ -94,6 +98,8 @@ def lib():
             "zdc_comm_init": ([P, P, I32, I32], I32),
             "zdc_sp_set_exchange_hook": ([P, EXCHANGE_FN, P, I32, I32], I32),
             "zdc_sp_prefill": ([P, I32, I32, P, P, I32, I32, I32, ctypes.POINTER(SpStats), P], I32),
+            "zdc_sp_prefill_ulysses": ([P, I32, I32, P, P, I32, I32, I32, ctypes.POINTER(SpStats), P], I32),
+            "zdc_sp_set_alltoall_hook": ([P, ALLTOALL_FN, P, I32, I32], I32),
             "zdc_sp_positions": ([I32, I32, I32, I32, ctypes.POINTER(I32)], I32),
             "zdc_cache_export": ([P, I32, P, P, P, P, P], I32),
             "zdc_cache_length": ([P, I32, ctypes.POINTER(I32)], I32),
@@ -379,13 +385,20 @@ class Context:
         self._hook = fn
         _check(lib().zdc_sp_set_exchange_hook(self.h, fn, None, rank, world), "zdc_sp_set_exchange_hook")
 
+    def set_alltoall_hook(self, fn, rank: int, world: int):
+        """Test transport of zdc_sp_prefill_ulysses (fn is an ALLTOALL_FN); keeps a reference to fn."""
+        self._a2a_hook = fn
+        _check(lib().zdc_sp_set_alltoall_hook(self.h, fn, None, rank, world), "zdc_sp_set_alltoall_hook")
+
     def sp_prefill(self, x_local, y_local, S_total: int, layout: int = 1, l0: int = 0, l1: Optional[int] = None,
-                   stats: bool = False, stream=None):
+                   stats: bool = False, stream=None, dataflow: str = "allgather"):
+        """dataflow "allgather" (zdc_sp_prefill) or "ulysses" (zdc_sp_prefill_ulysses)."""
         l1 = self.dims.n_layers if l1 is None else l1
         st = SpStats()
-        _check(lib().zdc_sp_prefill(self.h, l0, l1, _tptr(x_local, "bf16"), _tptr(y_local, "bf16"),
+        name = {"allgather": "zdc_sp_prefill", "ulysses": "zdc_sp_prefill_ulysses"}[dataflow]
+        _check(getattr(lib(), name)(self.h, l0, l1, _tptr(x_local, "bf16"), _tptr(y_local, "bf16"),
                                     x_local.shape[0], S_total, layout, ctypes.byref(st) if stats else None,
-                                    ctypes.c_void_p(_stream(stream))), "zdc_sp_prefill")
+                                    ctypes.c_void_p(_stream(stream))), name)
         if stats:
             return {"bytes_sent": st.bytes_sent, "bytes_recv": st.bytes_recv,
                     "bytes_recv_uncompressed": st.bytes_recv_uncompressed, "exchange_ms": st.exchange_ms,

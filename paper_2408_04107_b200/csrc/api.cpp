@@ -236,6 +236,10 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
     s = align_up(s + static_cast<int64_t>(std::min(max_batch, 128)) * std::max(max_nqkv, d.d_model) * 4 + 1024 * 4,
                  256);
   }
+  // Ulysses SP (zdc_sp_prefill_ulysses): all-to-all send and receive slabs, each at most
+  // (rows / 2) x n_qkv bf16 (P >= 2 ranks hold at most half of the rows each)
+  c->s_sp = s;
+  s = align_up(s + rows * max_nqkv * 2, 256);
   c->s_ybuf = s;  // cluster decode: y accumulator [8][d] f32 then 16 arrival counters, zero between launches
   s = align_up(s + static_cast<int64_t>(8) * d.d_model * 4 + 16 * 4, 256);
   if (any_split) {  // staged K'/V' of a split layer before packing, compaction indices, new-row staging

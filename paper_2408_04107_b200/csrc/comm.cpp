@@ -9,9 +9,13 @@
 //   a3  local queries (global positions: contiguous or zigzag) attend to every key at or before
 //       them; the tcgen05 attention kernel maps key tiles to (owner rank, local row) itself
 //   a5  local rows -> y_local
+// zdc_sp_prefill_ulysses is the paper's own dataflow instead (Fig. bkg:fig:all2all): a1 writes
+// per-destination slabs of the compressed Q'/K'/V' (GEMM epilogue mode 2), all-to-all #1 gives every
+// rank ALL tokens of its N_h/P heads, a3 runs the ordinary causal kernel over the full sequence for
+// those heads (the rank keeps their K'/V' cache), all-to-all #2 returns O' to the token owners, a5.
 // NCCL is resolved at run time (dlopen of libnccl.so.2, i.e. the copy torch already loaded), so
-// the library has no link-time NCCL dependency.  zdc_sp_set_exchange_hook replaces the NCCL
-// all-gather by a caller callback for single-GPU multi-process tests.
+// the library has no link-time NCCL dependency.  zdc_sp_set_exchange_hook / _alltoall_hook replace
+// the NCCL collectives by caller callbacks for single-GPU multi-process tests.
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -26,6 +30,8 @@
 
 typedef void (*zdc_exchange_fn)(void* user, void* gather_buf, int64_t chunk_bytes, int32_t rank, int32_t world,
                                 void* stream);
+typedef void (*zdc_alltoall_fn)(void* user, const void* send, void* recv, int64_t chunk_bytes, int32_t rank,
+                                int32_t world, void* stream);
 
 namespace zdc {
 
@@ -35,6 +41,10 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   bool ok = false;
 };
@@ -54,7 +64,12 @@ static NcclApi* nccl_api() {
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(api.h, "ncclCommDestroy"));
     api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(api.h, "ncclAllGather"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(api.h, "ncclGetErrorString"));
-    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather && api.GetErrorString;
+    api.Send = reinterpret_cast<decltype(api.Send)>(dlsym(api.h, "ncclSend"));
+    api.Recv = reinterpret_cast<decltype(api.Recv)>(dlsym(api.h, "ncclRecv"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(dlsym(api.h, "ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(dlsym(api.h, "ncclGroupEnd"));
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather && api.GetErrorString &&
+             api.Send && api.Recv && api.GroupStart && api.GroupEnd;
   });
   return &api;
 }
@@ -64,6 +79,8 @@ struct CommState {
   int rank = 0, world = 1;
   zdc_exchange_fn hook = nullptr;
   void* hook_user = nullptr;
+  zdc_alltoall_fn a2a_hook = nullptr;
+  void* a2a_user = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
 };
 
@@ -134,6 +151,23 @@ zdc_status zdc_sp_set_exchange_hook(zdc_ctx* c, zdc_exchange_fn fn, void* user, 
   c->comm->hook_user = user;
   ZDC_CUDA_TRY(cudaEventCreate(&c->comm->e0));
   ZDC_CUDA_TRY(cudaEventCreate(&c->comm->e1));
+  return ZDC_OK;
+}
+
+zdc_status zdc_sp_set_alltoall_hook(zdc_ctx* c, zdc_alltoall_fn fn, void* user, int32_t rank, int32_t world) {
+  if (!c || !fn) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_set_alltoall_hook: null argument");
+  if (world < 1 || rank < 0 || rank >= world)
+    return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_set_alltoall_hook: rank %d world %d", rank, world);
+  if (c->comm && (c->comm->rank != rank || c->comm->world != world)) comm_destroy(c);
+  if (!c->comm) {
+    c->comm = new CommState();
+    c->comm->rank = rank;
+    c->comm->world = world;
+    ZDC_CUDA_TRY(cudaEventCreate(&c->comm->e0));
+    ZDC_CUDA_TRY(cudaEventCreate(&c->comm->e1));
+  }
+  c->comm->a2a_hook = fn;
+  c->comm->a2a_user = user;
   return ZDC_OK;
 }
 
@@ -288,6 +322,184 @@ zdc_status zdc_sp_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x,
     cudaEventDestroy(t_end);
     stats->bytes_recv = bytes_recv;
     stats->bytes_sent = bytes_recv;  // all-gather: each slot goes to the P-1 peers
+    stats->bytes_recv_uncompressed = bytes_recv_unc;
+    stats->exchange_ms = exch_ms;
+    stats->total_ms = tot;
+  }
+  return ZDC_OK;
+}
+
+// all-to-all of P equal chunks: recv[q] = send_q[p] (chunk q of send goes to rank q)
+static zdc_status sp_alltoall(zdc_ctx* c, const uint8_t* send, uint8_t* recv, int64_t chunk, cudaStream_t s) {
+  const int P = c->comm->world, p = c->comm->rank;
+  if (c->comm->a2a_hook) {
+    c->comm->a2a_hook(c->comm->a2a_user, send, recv, chunk, p, P, s);
+    return ZDC_OK;
+  }
+  if (!c->comm->comm) return fail(ZDC_ERR_STATE, "zdc_sp_prefill_ulysses: no NCCL communicator and no all-to-all hook");
+  NcclApi* api = nccl_api();
+  ZDC_CUDA_TRY(cudaMemcpyAsync(recv + p * chunk, send + p * chunk, static_cast<size_t>(chunk), cudaMemcpyDeviceToDevice, s));
+  ncclResult_t r = api->GroupStart();
+  for (int q = 0; q < P && r == ncclSuccess; ++q) {
+    if (q == p) continue;
+    r = api->Send(send + q * chunk, static_cast<size_t>(chunk), ncclUint8, q, c->comm->comm, s);
+    if (r == ncclSuccess) r = api->Recv(recv + q * chunk, static_cast<size_t>(chunk), ncclUint8, q, c->comm->comm, s);
+  }
+  const ncclResult_t r2 = api->GroupEnd();
+  if (r != ncclSuccess || r2 != ncclSuccess)
+    return fail(ZDC_ERR_NCCL, "ncclSend/Recv all-to-all: %s", api->GetErrorString(r != ncclSuccess ? r : r2));
+  return ZDC_OK;
+}
+
+zdc_status zdc_sp_prefill_ulysses(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, uint16_t* y, int32_t B,
+                                  int32_t S_total, int32_t layout, zdc_sp_stats* stats, void* stream) {
+  if (!c || !x || !y) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_prefill_ulysses: null argument");
+  if (x == y) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_prefill_ulysses: x and y alias");
+  if (!c->w) return fail(ZDC_ERR_STATE, "zdc_sp_prefill_ulysses: ctx not bound");
+  if (!c->comm) return fail(ZDC_ERR_STATE, "zdc_sp_prefill_ulysses: zdc_comm_init / an all-to-all hook not set");
+  if (l0 < 0 || l1 > c->dims.n_layers || l0 >= l1)
+    return fail(ZDC_ERR_SHAPE, "zdc_sp_prefill_ulysses: layer range [%d, %d)", l0, l1);
+  const int P = c->comm->world, p = c->comm->rank;
+  const int d = c->dims.d_model, Nh = c->dims.n_heads, Nkv = c->dims.n_kv_heads;
+  if (layout != 0 && layout != 1) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_prefill_ulysses: layout %d", layout);
+  if (Nkv % P != 0)
+    return fail(ZDC_ERR_SHAPE, "zdc_sp_prefill_ulysses: N_kv = %d KV heads do not split over P = %d ranks", Nkv, P);
+  const int parts = layout == 1 ? 2 * P : P;
+  if (B <= 0 || S_total <= 0 || S_total % parts != 0)
+    return fail(ZDC_ERR_SHAPE, "zdc_sp_prefill_ulysses: S_total %d not divisible by %d (%s layout)", S_total, parts,
+                layout == 1 ? "zigzag" : "contiguous");
+  if (B > c->max_batch || S_total > c->max_seq)
+    return fail(ZDC_ERR_CAPACITY, "zdc_sp_prefill_ulysses: B=%d S_total=%d exceeds max_batch=%d max_seq=%d", B,
+                S_total, c->max_batch, c->max_seq);
+  for (int l = l0; l < l1; ++l) {
+    if (c->layers[l].split)
+      return fail(ZDC_ERR_UNSUPPORTED, "zdc_sp_prefill_ulysses: token split under SP is NEXT-2 (layer %d)", l);
+    if (c->len[l] != 0) return fail(ZDC_ERR_STATE, "zdc_sp_prefill_ulysses: layer %d cache is not empty", l);
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int n_local = S_total / P;
+  const int M = B * n_local;
+  const int hpr = Nh / P, gpr = Nkv / P;  // heads / KV groups per rank
+  g_launches = 0;
+  float exch_ms = 0.f;
+  int64_t bytes_recv = 0, bytes_recv_unc = 0;
+  cudaEvent_t t_begin = nullptr, t_end = nullptr;
+  std::vector<cudaEvent_t> ev;  // exchange brackets, read after the loop (no per-layer host sync)
+  auto mark = [&](std::vector<cudaEvent_t>& v) -> cudaError_t {
+    cudaEvent_t e;
+    cudaError_t r = cudaEventCreate(&e);
+    if (r == cudaSuccess) r = cudaEventRecord(e, s);
+    v.push_back(e);
+    return r;
+  };
+  if (stats) {
+    ZDC_CUDA_TRY(cudaEventCreate(&t_begin));
+    ZDC_CUDA_TRY(cudaEventCreate(&t_end));
+    ZDC_CUDA_TRY(cudaEventRecord(t_begin, s));
+  }
+  uint8_t* sp = c->scratch + c->s_sp;
+  for (int l = l0; l < l1; ++l) {
+    const LayerInfo& L = c->layers[l];
+    const uint16_t* xin = l == l0 ? x : y;
+    const int hq = hpr * L.rk_p, kq = gpr * L.rk_p, vq = gpr * L.rv_p, cols = hq + kq + vq;
+    const int ho = hpr * L.rv_p;
+    const int64_t chunk1 = static_cast<int64_t>(M) * cols * 2, chunk2 = static_cast<int64_t>(M) * ho * 2;
+    uint8_t* send = sp;
+    uint8_t* recv = P > 1 ? sp + P * chunk1 : sp;  // one rank: nothing moves
+    // a1: compressed Q'/K'/V' of the local tokens, written as per-destination slabs (epilogue mode 2)
+    Epilogue e1;
+    e1.mode = 2;
+    e1.uly.send = reinterpret_cast<uint16_t*>(send);
+    e1.uly.nq = L.nq;
+    e1.uly.nk = L.nk;
+    e1.uly.hq = hq;
+    e1.uly.kq = kq;
+    e1.uly.vq = vq;
+    e1.uly.cols = cols;
+    e1.uly.rows = M;
+    g_prof_class = kProfGemmQkv;
+    ZDC_CUDA_TRY(launch_gemm(xin, d, reinterpret_cast<const uint16_t*>(c->w + L.w_qkv), d, M, L.n_qkv, d, e1, s));
+    g_prof_class = kProfOther;
+    // all-to-all #1: tokens gathered along the sequence, heads distributed (compressed bytes)
+    if (P > 1) {
+      if (stats) ZDC_CUDA_TRY(mark(ev));
+      if (zdc_status st = sp_alltoall(c, send, recv, chunk1, s)) return st;
+      if (stats) ZDC_CUDA_TRY(mark(ev));
+    }
+    // this rank's heads for all S tokens: Q' in position order, K'/V' into its groups' cache
+    uint16_t* qpos = reinterpret_cast<uint16_t*>(c->scratch + c->s_q);
+    uint16_t* kc = reinterpret_cast<uint16_t*>(c->cache + L.k_off);
+    uint16_t* vc = reinterpret_cast<uint16_t*>(c->cache + L.v_off);
+    ZDC_CUDA_TRY(launch_ulysses_unpack_qkv(reinterpret_cast<const uint16_t*>(recv), P, B, n_local, S_total, layout, hq,
+                                           kq, vq, L.rk_p, L.rv_p, qpos, kc, vc, c->max_seq, s));
+    // a3: ordinary causal attention over the full sequence for the rank's N_h/P heads
+    uint16_t* opos = reinterpret_cast<uint16_t*>(c->scratch + c->s_o);
+    PrefillAttnArgs a;
+    a.q = qpos;
+    a.ldq = hq;
+    a.k = kc;
+    a.v = vc;
+    a.S_cap = c->max_seq;
+    a.o = opos;
+    a.ldo = ho;
+    a.lse = reinterpret_cast<float*>(c->scratch + c->s_lse);
+    a.B = B;
+    a.S = S_total;
+    a.Nh = hpr;
+    a.Nkv = gpr;
+    a.rk = L.rk_p;
+    a.rv = L.rv_p;
+    a.scale = 1.0f / std::sqrt(static_cast<float>(c->dims.d_head));
+    a.q_pos0 = 0;
+    a.q_row0 = 0;
+    a.n_q = S_total;
+    g_prof_class = kProfAttnPrefill;
+    ZDC_CUDA_TRY(launch_prefill_attention(a, s));
+    g_prof_class = kProfOther;
+    // all-to-all #2: O' back to the token owners (heads gathered, sequence split)
+    ZDC_CUDA_TRY(launch_ulysses_pack_o(opos, P, B, n_local, S_total, layout, ho, reinterpret_cast<uint16_t*>(send), s));
+    if (P > 1) {
+      if (stats) ZDC_CUDA_TRY(mark(ev));
+      if (zdc_status st = sp_alltoall(c, send, recv, chunk2, s)) return st;
+      if (stats) ZDC_CUDA_TRY(mark(ev));
+    }
+    // O'_local [M][ko_p] reuses the position-ordered O' region (dead once packed into the send slabs)
+    uint16_t* oloc = opos;
+    ZDC_CUDA_TRY(launch_ulysses_unpack_o(reinterpret_cast<const uint16_t*>(recv), P, B, n_local, ho, oloc, L.ko_p, s));
+    // a5: y_local = O'_local W_O^R
+    Epilogue e5;
+    e5.mode = 0;
+    e5.d = y;
+    e5.ldd = d;
+    g_prof_class = kProfGemmO;
+    ZDC_CUDA_TRY(launch_gemm(oloc, L.ko_p, reinterpret_cast<const uint16_t*>(c->w + L.w_o), L.ko_p, M, d, L.ko_p, e5, s));
+    g_prof_class = kProfOther;
+    if (P > 1) {
+      bytes_recv += (P - 1) * (chunk1 + chunk2);
+      const int64_t cols_u = static_cast<int64_t>(hpr + 2 * gpr) * c->dims.d_head;  // uncompressed Q/K/V columns
+      bytes_recv_unc += (P - 1) * (static_cast<int64_t>(M) * cols_u * 2 + static_cast<int64_t>(M) * hpr * c->dims.d_head * 2);
+    }
+    c->len[l] = S_total;
+    c->sp_layer[l] = 2;
+    c->last_layer = l;
+    c->last_T = S_total;
+  }
+  c->batch = B;
+  if (stats) {
+    ZDC_CUDA_TRY(cudaEventRecord(t_end, s));
+    ZDC_CUDA_TRY(cudaEventSynchronize(t_end));
+    float tot = 0.f;
+    ZDC_CUDA_TRY(cudaEventElapsedTime(&tot, t_begin, t_end));
+    for (size_t i = 0; i + 1 < ev.size(); i += 2) {
+      float ms = 0.f;
+      ZDC_CUDA_TRY(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+      exch_ms += ms;
+    }
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    cudaEventDestroy(t_begin);
+    cudaEventDestroy(t_end);
+    stats->bytes_recv = bytes_recv;
+    stats->bytes_sent = bytes_recv;  // all-to-all: every rank sends what its peers receive from it
     stats->bytes_recv_uncompressed = bytes_recv_unc;
     stats->exchange_ms = exch_ms;
     stats->total_ms = tot;

@@ -48,6 +48,7 @@ struct zdc_ctx {
   int64_t s_ltab = 0;                                 // fused decode layer table
   int64_t s_ybuf = 0;
   int64_t s_gsk = -1;                                 // split-K decode GEMM workspace (max_batch > 8)
+  int64_t s_sp = 0;                                   // Ulysses SP all-to-all send | recv slabs
   int max_nqkv = 0;                                 // cluster decode: f32 y accumulator [8][d] + counters [16]
   int ldq = 0, ldo = 0;
   uint8_t* w = nullptr;

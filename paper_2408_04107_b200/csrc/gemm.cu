@@ -138,6 +138,22 @@ __device__ __forceinline__ void store_unit(const Epilogue& e, int m, int n, uint
   uint16_t* dst;
   if (e.mode == 0) {
     dst = e.d + static_cast<int64_t>(m) * e.ldd + n;
+  } else if (e.mode == 2) {
+    const UlyssesDest& u = e.uly;
+    int q, c;
+    if (n < u.nq) {
+      q = n / u.hq;
+      c = n - q * u.hq;
+    } else if (n < u.nq + u.nk) {
+      const int nn = n - u.nq;
+      q = nn / u.kq;
+      c = u.hq + nn - q * u.kq;
+    } else {
+      const int nn = n - u.nq - u.nk;
+      q = nn / u.vq;
+      c = u.hq + u.kq + nn - q * u.vq;
+    }
+    dst = u.send + (static_cast<int64_t>(q) * u.rows + m) * u.cols + c;
   } else {
     const QkvDest& q = e.qkv;
     if (n < q.nq) {

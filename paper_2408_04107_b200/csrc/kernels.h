@@ -28,11 +28,22 @@ struct QkvDest {
   const int* posmap = nullptr;
 };
 
+// Ulysses SP send layout (comm.cpp, zdc_sp_prefill_ulysses): column n of a local token row goes to
+// the slab of the rank that owns its head: send[q][m][cols], cols = hq (Q' of the rank's N_h/P
+// heads) + kq (K' of its N_kv/P groups) + vq (V').  hq, kq, vq are multiples of 8.
+struct UlyssesDest {
+  uint16_t* send = nullptr;
+  int nq = 0, nk = 0;          // Q' / K' columns of the full projection row
+  int hq = 0, kq = 0, vq = 0, cols = 0;
+  int64_t rows = 0;            // rows per slab (B * n_local)
+};
+
 struct Epilogue {
-  int mode = 0;  // 0 = plain bf16 D[M][ldd]; 1 = QKV scatter (QkvDest)
+  int mode = 0;  // 0 = plain bf16 D[M][ldd]; 1 = QKV scatter (QkvDest); 2 = Ulysses send slabs (UlyssesDest)
   uint16_t* d = nullptr;
   int64_t ldd = 0;
   QkvDest qkv;
+  UlyssesDest uly;
   int* len_inc = nullptr;  // if set, the kernel increments *len_inc once (decode: advances the layer length)
   int len_cap = 0;         // ... saturating at len_cap: a step with *len_inc >= len_cap sets *err instead
   int* err = nullptr;      // device overflow flag (reported by zdc_cache_sync)
@@ -97,6 +108,21 @@ struct PrefillAttnArgs {
   int64_t kv_rows_total = 0;  // rows of the K/V tensor maps (0 = B * Nkv * S_cap)
 };
 cudaError_t launch_prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream);
+
+// ---- Ulysses SP re-layouts (sp_ulysses.cu).  Global position of local row t of rank q:
+// layout 0 contiguous (q n + t), 1 zigzag (chunks q and 2P-1-q of 2P).
+// recv[src][B][n_local][cols] (this rank's heads, from every rank) -> Q' [B*S][hq] and the K'/V'
+// cache of this rank's groups [B][nkv_loc][S_cap][rk] / [rv], in global position order
+cudaError_t launch_ulysses_unpack_qkv(const uint16_t* recv, int P, int B, int n_local, int S, int layout, int hq, int kq,
+                                      int vq, int rk, int rv, uint16_t* q, uint16_t* kc, uint16_t* vc, int S_cap,
+                                      cudaStream_t s);
+// O' [B*S][ho] (this rank's heads, position order) -> send[dst][B][n_local][ho] (dst's tokens)
+cudaError_t launch_ulysses_pack_o(const uint16_t* o, int P, int B, int n_local, int S, int layout, int ho,
+                                  uint16_t* send, cudaStream_t s);
+// recv[src][B][n_local][ho] (src's heads for this rank's tokens) -> O'_local [B*n_local][ko_p]
+// (head-major columns: src * ho + c; padding columns >= P * ho zeroed)
+cudaError_t launch_ulysses_unpack_o(const uint16_t* recv, int P, int B, int n_local, int ho, uint16_t* o, int ko_p,
+                                    cudaStream_t s);
 cudaError_t launch_prefill_attention_v3(const PrefillAttnArgs& a, cudaStream_t stream);
 cudaError_t launch_prefill_attention_v4(const PrefillAttnArgs& a, cudaStream_t stream);
 bool prefill_attention_v4_supported(int rk);

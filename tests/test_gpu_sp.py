@@ -25,7 +25,10 @@ def _cudart():
     raise OSError("libcudart not found")
 
 
-def _worker(rank, world, port, layout, S, B, out_q):
+DIMS = {"mha": (2, 256, 4, 2, 64, 32), "gqa4": (2, 256, 8, 4, 64, 32)}
+
+
+def _worker(rank, world, port, layout, S, B, out_q, dataflow="allgather", shape="mha"):
     import torch.distributed as dist
     import oracle as O  # noqa: F401
     import paper_2408_04107_b200 as zdc
@@ -35,8 +38,8 @@ def _worker(rank, world, port, layout, S, B, out_q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
-    dims = Z.Dims(2, 256, 4, 2, 64)
-    plan = Z.plan_uniform(2, 32)
+    dims = Z.Dims(*DIMS[shape][:5])
+    plan = Z.plan_uniform(2, DIMS[shape][5])
     _, folded = fold_stack(dims, 1, n_calib=256)
     ctx = zdc.Context(dims, plan, B, S)
     for l, f in enumerate(folded):
@@ -56,18 +59,30 @@ def _worker(rank, world, port, layout, S, B, out_q):
         for q in range(P):
             cudart.cudaMemcpy(gbuf + q * chunk_bytes, parts[q].numpy().ctypes.data, chunk_bytes, 1)  # H2D
 
+    def alltoall(user, send, recv, chunk_bytes, r, P, stream):
+        cudart.cudaStreamSynchronize(stream)
+        mine = np.empty(P * chunk_bytes, dtype=np.uint8)
+        cudart.cudaMemcpy(mine.ctypes.data, send, P * chunk_bytes, 2)   # D2H
+        out = torch.empty(P * chunk_bytes, dtype=torch.uint8)
+        dist.all_to_all_single(out, torch.from_numpy(mine))
+        cudart.cudaMemcpy(recv, out.numpy().ctypes.data, P * chunk_bytes, 1)   # H2D
+
     cb = zdc.EXCHANGE_FN(exchange)
     ctx.set_exchange_hook(cb, rank, world)
+    cb2 = zdc.ALLTOALL_FN(alltoall)
+    ctx.set_alltoall_hook(cb2, rank, world)
     xl = to_dev_bf16(np.ascontiguousarray(x[:, pos]))
     yl = torch.empty_like(xl)
-    stats = ctx.sp_prefill(xl, yl, S_total=S, layout=layout, stats=True)
+    stats = ctx.sp_prefill(xl, yl, S_total=S, layout=layout, stats=True, dataflow=dataflow)
     torch.cuda.synchronize()
     out_q.put((rank, pos, yl.float().cpu().numpy(), stats))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,layout", [(2, 0), (2, 1), (4, 1)])
-def test_sp_prefill_equals_single_gpu_rows(world, layout):
+@pytest.mark.parametrize("world,layout,dataflow,shape", [
+    (2, 0, "allgather", "mha"), (2, 1, "allgather", "mha"), (4, 1, "allgather", "mha"),
+    (2, 0, "ulysses", "mha"), (2, 1, "ulysses", "mha"), (4, 1, "ulysses", "gqa4")])
+def test_sp_prefill_equals_single_gpu_rows(world, layout, dataflow, shape):
     import multiprocessing as pymp
     import oracle as O
     import paper_2408_04107_b200 as zdc
@@ -77,8 +92,9 @@ def test_sp_prefill_equals_single_gpu_rows(world, layout):
     S = 256 * world * (2 if layout else 1)   # chunks of 128 (zigzag) / 256 (contiguous)
     ctx_mp = pymp.get_context("spawn")
     q = ctx_mp.Queue()
-    port = 29600 + world * 10 + layout + os.getpid() % 500
-    procs = [ctx_mp.Process(target=_worker, args=(r, world, port, layout, S, B, q)) for r in range(world)]
+    port = 29600 + world * 10 + layout + (5 if dataflow == "ulysses" else 0) + os.getpid() % 500
+    procs = [ctx_mp.Process(target=_worker, args=(r, world, port, layout, S, B, q, dataflow, shape))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=600) for _ in range(world)], key=lambda t: t[0])
@@ -86,8 +102,9 @@ def test_sp_prefill_equals_single_gpu_rows(world, layout):
         p.join(timeout=120)
         assert p.exitcode == 0
     # single-process reference through zdc_prefill
-    dims = Z.Dims(2, 256, 4, 2, 64)
-    plan = Z.plan_uniform(2, 32)
+    dims = Z.Dims(*DIMS[shape][:5])
+    r = DIMS[shape][5]
+    plan = Z.plan_uniform(2, r)
     _, folded = fold_stack(dims, 1, n_calib=256)
     x = Z.prompt(dims, 1, B, S, seed=41)
     ctx = make_context(dims, plan, folded, B, S)
@@ -102,10 +119,18 @@ def test_sp_prefill_equals_single_gpu_rows(world, layout):
         assert np.array_equal(yl, y_single[:, pos]), rank      # bit-identical rows
         assert normwise(yl, want[:, pos]) <= 2e-2
         covered += pos.tolist()
-        # bytes received per rank and layer: (P-1)/P * B * S * N_kv * (r_k + r_v) * 2, two layers
-        assert stats["bytes_recv"] == 2 * O.sp_bytes_received(world, B, S, 2, 32, 32)
-        # r / d_head = 32 / 64 of the uncompressed K/V bytes
-        assert stats["bytes_recv_uncompressed"] == 2 * O.sp_bytes_received(world, B, S, 2, 64, 64)
+        nh, nkv, dh = dims.n_heads, dims.n_kv_heads, dims.d_head
+        if dataflow == "allgather":
+            # bytes received per rank and layer: (P-1)/P * B * S * N_kv * (r_k + r_v) * 2, two layers
+            want_b = O.sp_bytes_received(world, B, S, nkv, r, r)
+            want_u = O.sp_bytes_received(world, B, S, nkv, dh, dh)
+        else:
+            # both all-to-alls (compressed Q'/K'/V' of this rank's heads, then O' back)
+            want_b = O.sp_bytes_received_ulysses(world, B, S, nh, nkv, r, r)
+            want_u = O.sp_bytes_received_ulysses(world, B, S, nh, nkv, dh, dh)
+        assert stats["bytes_recv"] == 2 * want_b
+        # r / d_head = 32 / 64 of the uncompressed bytes
+        assert stats["bytes_recv_uncompressed"] == 2 * want_u
     assert sorted(covered) == list(range(S))
 
 
@@ -122,17 +147,18 @@ def test_sp_prefill_nccl_world1():
     S = 256
     x = to_dev_bf16(Z.prompt(dims, 1, 1, S, seed=43))
     outs = []
-    for sp in (False, True):
+    for sp in (None, "allgather", "ulysses"):
         ctx = zdc.Context(dims, plan, 1, S)
         for l, f in enumerate(folded):
             load_lib_fold(ctx, l, f)
         y = torch.empty_like(x)
         if sp:
             ctx.comm_init(zdc.comm_unique_id(), 0, 1)
-            st = ctx.sp_prefill(x, y, S, layout=1, stats=True)
+            st = ctx.sp_prefill(x, y, S, layout=1, stats=True, dataflow=sp)
             assert st["bytes_recv"] == 0 and st["bytes_recv_uncompressed"] == 0
         else:
             ctx.prefill(x, y)
         torch.cuda.synchronize()
         outs.append(from_dev(y))
-    assert np.array_equal(outs[0], outs[1])
+        ctx.close()
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])

@@ -48,6 +48,8 @@ MUTANTS = [
      "K, V = self._truncate_rows(l, K, V, self.classes[rep][:, :S])"),
     ("decode attends before appending", "self.length[l] = t + 1\n        O = np.zeros",
      "self.length[l] = t + 1\n        self.K[l], self.V[l] = self.K[l][:, :, :-1], self.V[l][:, :, :-1]\n        O = np.zeros"),
+    ("Ulysses bytes without all-to-all #2", "return (P - 1) * rows * (cols1 + cols2) * elem_bytes",
+     "return (P - 1) * rows * cols1 * elem_bytes"),
     ("SP bytes without (P-1)", "return (P - 1) * (S // P) * B * n_kv * (r_k + r_v) * elem_bytes",
      "return P * (S // P) * B * n_kv * (r_k + r_v) * elem_bytes"),
 ]

@@ -544,3 +544,26 @@ def test_decode_score_equal_to_tau_is_unimportant():
         assert not m.classes[0][:, t].any()
         for l in range(2):
             assert np.all(m.K[l][:, :, t, 2:] == 0.0) and np.all(m.V[l][:, :, t, 2:] == 0.0)
+
+
+def test_P12_ulysses_bytes_by_element_tagging():
+    """Ulysses SP bytes: tag every element each rank holds and count what crosses to
+    another rank in the two all-to-alls, at small sizes, against the closed form; and the c5 figure
+    of SURVEY.md §8(f) NEXT-1 (128K tokens, P = 8, MHA 32 heads, r = 64: 0.235 GB per layer)."""
+    for P, B, S, nh, nkv, rk, rv in ((2, 1, 8, 4, 2, 3, 5), (4, 2, 16, 8, 4, 2, 7), (4, 1, 8, 4, 4, 6, 6)):
+        owner_tok = np.repeat(np.arange(P), S // P)          # contiguous; the count is layout-free
+        owner_head = np.repeat(np.arange(P), nh // P)
+        owner_grp = np.repeat(np.arange(P), nkv // P)
+        for p in range(P):
+            recv = 0
+            for t in range(S):                                # #1: my heads' columns of others' tokens
+                if owner_tok[t] != p:
+                    recv += B * (np.sum(owner_head == p) * rk + np.sum(owner_grp == p) * (rk + rv))
+            for t in range(S):                                # #2: others' heads' O' of my tokens
+                if owner_tok[t] == p:
+                    recv += B * np.sum(owner_head != p) * rv
+            assert recv * 2 == O.sp_bytes_received_ulysses(P, B, S, nh, nkv, rk, rv)
+    got = O.sp_bytes_received_ulysses(8, 1, 131072, 32, 32, 64, 64)
+    assert abs(got / 1e9 - 0.235) < 0.0005
+    # the all-gather of compressed K'/V' moves 0.940 GB there: P/2 = 4x more (MHA)
+    assert O.sp_bytes_received(8, 1, 131072, 32, 64, 64) == 4 * got
