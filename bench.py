@@ -318,7 +318,7 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------------------ SP (a6)
-def sp_bench(args, zdc, torch, dist, rank, world, dev, stream):
+def sp_bench(args, zdc, torch, dist, rank, world, dev, stream, dataflow="allgather"):
     """Sequence-parallel prefill (configs[4], c5): the c2 layer stack over a S_total-token prompt
     sharded zigzag over the `world` ranks, compressed K'/V' all-gathered in place per layer with
     NCCL (zdc_sp_prefill).  Reports the SP prefill tok/s (S_total / max-over-ranks time), and the
@@ -346,7 +346,7 @@ def sp_bench(args, zdc, torch, dist, rank, world, dev, stream):
     y = torch.empty_like(x)
     for _ in range(2):  # warm-up (NCCL connection set-up, kernel attributes)
         ctx.reset()
-        ctx.sp_prefill(x, y, S_tot, layout=1, stream=stream)
+        ctx.sp_prefill(x, y, S_tot, layout=1, stream=stream, dataflow=dataflow)
     torch.cuda.synchronize()
     reps = max(1, args.steps)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -357,13 +357,13 @@ def sp_bench(args, zdc, torch, dist, rank, world, dev, stream):
         ctx.reset()
         torch.cuda.synchronize()
         e0.record(stream)
-        ctx.sp_prefill(x, y, S_tot, layout=1, stream=stream)
+        ctx.sp_prefill(x, y, S_tot, layout=1, stream=stream, dataflow=dataflow)
         e1.record(stream)
         torch.cuda.synchronize()
         ms += e0.elapsed_time(e1)
     ms /= reps
     ctx.reset()
-    st = ctx.sp_prefill(x, y, S_tot, layout=1, stats=True, stream=stream)
+    st = ctx.sp_prefill(x, y, S_tot, layout=1, stats=True, stream=stream, dataflow=dataflow)
     torch.cuda.synchronize()
     tt = torch.tensor([ms, st["exchange_ms"], -st["exchange_ms"]], device=dev)
     if world > 1:
@@ -371,7 +371,8 @@ def sp_bench(args, zdc, torch, dist, rank, world, dev, stream):
     ms, ex_max, ex_min = float(tt[0]), float(tt[1]), -float(tt[2])
     per_layer_recv = st["bytes_recv"] / Lsp
     ctx.close()
-    out = {"workload": "c5_sp_llama2_7b", "S_total": S_tot, "layers": Lsp, "P": world, "layout": "zigzag",
+    out = {"workload": "c5_sp_llama2_7b", "dataflow": dataflow, "S_total": S_tot, "layers": Lsp, "P": world,
+           "layout": "zigzag",
            "rank": r, "ms": ms, "sp_prefill_tok_s": S_tot / (ms / 1e3),
            "bytes_recv_per_gpu_per_layer": per_layer_recv,
            "bytes_recv_uncompressed_per_gpu_per_layer": st["bytes_recv_uncompressed"] / Lsp,
@@ -883,10 +884,12 @@ def run_zdc(args):
     sp = None
     if (world > 1 or args.sp) and not args.no_sp:
         log("SP prefill (c5) over %d rank(s)" % world)
-        try:
-            sp = sp_bench(args, zdc, torch, dist, rank, world, dev, stream)
-        except Exception as e:  # reported, never hides the main line
-            sp = {"error": "%s: %s" % (type(e).__name__, e)}
+        sp = {}
+        for flow in ("allgather", "ulysses"):   # compressed K'/V' all-gather; the paper's Ulysses a2a
+            try:
+                sp[flow] = sp_bench(args, zdc, torch, dist, rank, world, dev, stream, dataflow=flow)
+            except Exception as e:  # reported, never hides the main line
+                sp[flow] = {"error": "%s: %s" % (type(e).__name__, e)}
     elif world == 1:
         sp = {"note": "the K'/V' exchange needs N > 1: bench.py --gpus N under torchrun (or --sp for P = 1)"}
 
