@@ -387,10 +387,12 @@ def sp_bench(args, zdc, torch, dist, rank, world, dev, stream, dataflow="allgath
 
 
 # ------------------------------------------------------------------------------------ c3 / c4 layers
-def config_bench(args, zdc, torch, dev, stream, cid, n_layers=4, T=48):
-    """Per-layer prefill and decode of config `cid` (3: Llama-2-13B shape, batch 32, prompt 1024,
-    token split r^i = 96 / r^u = 32 at g = 0.5 over one 4-layer group; 4: Llama-2-70B shape, GQA 8 KV
-    heads, batch 64, prompt 8192, r = 64) on `n_layers` layers with timing-only weights (the ideal
+def config_bench(args, zdc, torch, dev, stream, cid, n_layers=4, T=48, importance_mode=0):
+    """Per-layer prefill and decode of config `cid` (3: the whole Llama-2-13B-shaped stack, 40 layers,
+    batch 32, prompt 1024, SURVEY.md §8(d)'s plan: 10 groups of 4 layers, g_bp = round(2500 +
+    5000 k / 9) for group k, r^i = 96 / r^u = 32, importance mode raw (0) or per-key mean (1);
+    4: Llama-2-70B shape, GQA 8 KV heads, batch 64, prompt 8192, r = 64, on `n_layers` layers) with
+    timing-only weights (the ideal
     fold of SURVEY.md §8(d)), each layer called separately with the same x (as for c2).  Prefill:
     algorithmic FLOP / time against the bf16 peak; decode: algorithmic bytes (weights at the plan
     ranks + K'/V' at the realised per-token widths + append + x/y) per layer-step / time against
@@ -404,7 +406,9 @@ def config_bench(args, zdc, torch, dev, stream, cid, n_layers=4, T=48):
     B, S, r = cfg["B"], cfg["S"], cfg["r"]
     if cid == 3:
         ru = cfg["r_u"]
-        plan = Z.plan_split(n_layers, r, ru, [list(range(n_layers))], [5000])
+        n_layers = full.n_layers
+        dims = Z.Dims(n_layers, full.d_model, full.n_heads, full.n_kv_heads, full.d_head)
+        plan = Z.c3_plan(n_layers, importance_mode)
     else:
         ru = r
         plan = Z.plan_uniform(n_layers, r)
@@ -464,7 +468,7 @@ def config_bench(args, zdc, torch, dev, stream, cid, n_layers=4, T=48):
         for l in range(n_layers):
             ctx.decode(xb, yb, l, l + 1)
     torch.cuda.synchronize()
-    clk = ClockSampler(dev.index if dev.index is not None else 0, period_ms=20)
+    clk = ClockSampler(dev.index if dev.index is not None else 0, period_ms=5)
     clk.start()
     time.sleep(0.1)
     ev[2].record(stream)
@@ -490,19 +494,27 @@ def config_bench(args, zdc, torch, dev, stream, cid, n_layers=4, T=48):
     flop = sum(prefill_layer_flops(d, nh, nkv, r, B, S).values())
     wbytes = (n_qkv * d + d * nq) * 2
     wI, wU = 2 * nkv * r * 2, 2 * nkv * ru * 2  # bytes per cached token per layer (K' + V')
+    groups = None
     if cid == 3:
-        imp = np.zeros((B, ctx.cache_length(0)), dtype=np.uint8)
-        zdc._check(zdc.lib().zdc_cache_export(ctx.h, 0, None, None, imp.ctypes.data_as(ctypes.c_void_p), None,
-                                              ctypes.c_void_p(stream.cuda_stream)), "zdc_cache_export")
-        cum = np.cumsum(imp.astype(np.int64), axis=1)  # important tokens among the first j+1
-        kv = 0.0
-        for t in range(2, T + 2):
-            n_before = S + t  # cached rows the step-t query attends to (+ its own, appended)
-            ni = cum[:, n_before - 1]
-            kv += float((ni * wI + (n_before - ni) * wU).sum())
-        kv /= T
-        frac_imp_prompt = float(imp[:, :S].mean())
-        frac_imp_decode = float(imp[:, S:S + T + 2].mean())
+        kv, groups, imps = 0.0, [], {}
+        for l in range(n_layers):
+            rl = plan.group_rep[l]
+            if rl not in imps:  # the classes the representative layer assigned (prompt + decode)
+                imp = np.zeros((B, ctx.cache_length(rl)), dtype=np.uint8)
+                zdc._check(zdc.lib().zdc_cache_export(ctx.h, rl, None, None, imp.ctypes.data_as(ctypes.c_void_p),
+                                                      None, ctypes.c_void_p(stream.cuda_stream)), "zdc_cache_export")
+                imps[rl] = imp
+                groups.append({"layers": [rl, rl + 3], "g_bp": plan.g_bp[rl],
+                               "important_prompt": round(float(imp[:, :S].mean()), 4),
+                               "important_decode": round(float(imp[:, S:S + T + 2].mean()), 4)})
+            cum = np.cumsum(imps[rl].astype(np.int64), axis=1)  # important tokens among the first j+1
+            for t in range(2, T + 2):
+                n_before = S + t  # cached rows the step-t query attends to (+ its own, appended)
+                ni = cum[:, n_before - 1]
+                kv += float((ni * wI + (n_before - ni) * wU).sum())
+        kv /= T * n_layers  # per layer-step, averaged over the layers
+        frac_imp_prompt = float(np.mean([v[:, :S].mean() for v in imps.values()]))
+        frac_imp_decode = float(np.mean([v[:, S:S + T + 2].mean() for v in imps.values()]))
     else:
         kv = float(B * (S + 2 + (T - 1) / 2.0) * wI)
         frac_imp_prompt = frac_imp_decode = None
@@ -528,8 +540,9 @@ def config_bench(args, zdc, torch, dev, stream, cid, n_layers=4, T=48):
     if per_class:
         out["decode"]["per_class_us_per_layer"] = per_class
     if cid == 3:
+        out["importance_mode"] = {0: "raw", 1: "mean"}[importance_mode]
         out["realised_important_fraction"] = {"prompt": round(frac_imp_prompt, 4),
-                                              "decode": round(frac_imp_decode, 4), "g_bp": 5000}
+                                              "decode": round(frac_imp_decode, 4), "groups": groups}
     ctx.close()
     del x, y, xd
     torch.cuda.empty_cache()
@@ -899,10 +912,14 @@ def run_zdc(args):
         other = {}
         for name in [c for c in args.configs.split(",") if c]:
             log("config %s layers" % name)
-            try:
-                other[name] = config_bench(args, zdc, torch, dev, stream, int(name.lstrip("c")))
-            except Exception as e:  # reported, never hides the main line
-                other[name] = {"error": "%s: %s" % (type(e).__name__, e)}
+            modes = (0, 1) if name == "c3" else (0,)
+            for mode in modes:   # c3: both importance modes (reading c10)
+                key = name if mode == 0 else name + "_mean"
+                try:
+                    other[key] = config_bench(args, zdc, torch, dev, stream, int(name.lstrip("c")),
+                                              importance_mode=mode)
+                except Exception as e:  # reported, never hides the main line
+                    other[key] = {"error": "%s: %s" % (type(e).__name__, e)}
 
     # ---- uncompressed r = d_h baseline + library comparison (report only), N = 1
     unc = None

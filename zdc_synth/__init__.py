@@ -23,7 +23,7 @@ from __future__ import annotations
 import dataclasses
 import numpy as np
 
-from .configs import CONFIGS, Dims, Plan, plan_uniform, plan_split, dims_of  # noqa: F401
+from .configs import CONFIGS, Dims, Plan, plan_uniform, plan_split, dims_of, c3_plan  # noqa: F401
 
 T_X, T_XC, T_BQK, T_GQ, T_GK, T_BVO, T_GV, T_HO, T_DEC = range(9)
 
