@@ -105,22 +105,6 @@ bool make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner_elems, uint
   return r == CUDA_SUCCESS;
 }
 
-// [rows][K] bf16 (row stride row_bytes) viewed as {64, rows, K/64}: k-block kb of row r at
-// r * row_bytes + kb * 128; box {64, box_rows, kb_box} lands as kb_box stacked SW128 tiles
-bool make_tmap_3d_kblocks(CUtensorMap* map, const void* base, uint64_t K, uint64_t rows, uint64_t row_bytes,
-                          uint32_t box_rows, uint32_t kb_box) {
-  PFN_tmapEncodeTiled fn = get_encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[3] = {64, rows, K / 64};
-  cuuint64_t strides[2] = {row_bytes, 128};
-  cuuint32_t box[3] = {64, box_rows, kb_box};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
 int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -174,34 +158,21 @@ __device__ __forceinline__ void store_unit(const Epilogue& e, int m, int n, uint
 }
 
 // ------------------------------------------------------------------ device: the GEMM
-// KB > 1 (split-K decode GEMMs): a stage holds KB consecutive k-blocks, fetched by ONE 3-D TMA box
-// per operand (k-block as the outer box dimension, 128 B apart in memory), so every weight row
-// contributes KB * 128 contiguous bytes per request instead of 128 B at a 2 * K byte stride
-template <int BN, int KB = 1>
+// AR < 128 (skinny decode GEMMs, M <= AR): a stage loads only AR rows of A (the activations), so
+// the ring holds more stages of weight (B) tiles -- the bytes in flight per SM set the HBM stream
+// rate of these HBM-bound GEMMs.  The MMA still runs M = 128: rows >= AR of its A operand read the
+// next stage's bytes (in-bounds shared memory) and only produce accumulator rows >= M, which the
+// epilogue never stores.
+template <int BN, int AR = 128>
 struct GemmCfg {
   static constexpr int BM = 128, BK = 64;
-  static constexpr uint32_t A_TILE = BM * BK * 2, B_TILE = BN * BK * 2;
-  static constexpr uint32_t A_BYTES = A_TILE * KB, B_BYTES = B_TILE * KB, STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = KB == 1 ? (BN == 256 ? 4 : 6) : static_cast<int>((200u * 1024u) / STAGE_BYTES);
+  static constexpr uint32_t A_TILE = AR * BK * 2, B_TILE = BN * BK * 2;
+  static constexpr uint32_t A_BYTES = A_TILE, B_BYTES = B_TILE, STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = AR == 128 ? (BN == 256 ? 4 : 6) : static_cast<int>((200u * 1024u) / STAGE_BYTES);
   static constexpr uint32_t TMEM_COLS = 2 * BN;
+  // (the last A stage's 128-row view reaches into the B stages that follow it: still in bounds)
   static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 };
-
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
-// stage-sized load of one operand: KB == 1 a 2-D box, else a 3-D box {64, rows, KB}
-template <int KB>
-__device__ __forceinline__ void tma_load_op(void* dst, const CUtensorMap* map, uint64_t* bar, int kstage, int row) {
-  if constexpr (KB == 1)
-    tma_load_2d(dst, map, bar, kstage * 64, row);
-  else
-    tma_load_3d(dst, map, bar, 0, row, kstage * KB);
-}
 
 // Output tile -> (M-block, N-block).  band == 0: M fastest.  band > 0: grouped raster -- bands of
 // `band` N-blocks, each swept over every M-block with the band's N fastest, so concurrent CTAs share
@@ -220,11 +191,11 @@ __device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, 
   nb = n0 + idx % w;
 }
 
-template <int BN, int KB>
+template <int BN, int AR>
 __global__ void __launch_bounds__(256, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, int M,
                         int N, int K, const Epilogue epi) {
-  using C = GemmCfg<BN, KB>;
+  using C = GemmCfg<BN, AR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -239,7 +210,7 @@ __global__ void __launch_bounds__(256, 1)
   const int m_tiles = (M + C::BM - 1) / C::BM;
   const int n_tiles = (N + BN - 1) / BN;
   const int num_tiles = m_tiles * n_tiles;
-  const int k_blocks = K / (C::BK * KB);  // stage-sized k-blocks
+  const int k_blocks = K / C::BK;
   // work item w: output tile w % num_tiles, k-split w / num_tiles (k-blocks [kb0, kb1))
   const int ks = epi.k_splits;
   const int num_work = num_tiles * ks;
@@ -288,12 +259,12 @@ __global__ void __launch_bounds__(256, 1)
           const int n0 = max(0, min(C::STAGES, kb1 - sp * kpb));
           for (int i = 0; i < n0; ++i) {
             mbar_arrive_expect_tx(&full[i], C::STAGE_BYTES);
-            tma_load_op<KB>(sB + i * C::B_BYTES, &tma_b, &full[i], sp * kpb + i, nb * BN);
+            tma_load_2d(sB + i * C::B_BYTES, &tma_b, &full[i], (sp * kpb + i) * C::BK, nb * BN);
           }
           pdl_wait();
           pdl_trigger();
           for (int i = 0; i < n0; ++i)
-            tma_load_op<KB>(sA + i * C::A_BYTES, &tma_a, &full[i], sp * kpb + i, mb * C::BM);
+            tma_load_2d(sA + i * C::A_BYTES, &tma_a, &full[i], (sp * kpb + i) * C::BK, mb * C::BM);
           issued = n0;
           waited = true;
           stage = n0 % C::STAGES;
@@ -302,12 +273,12 @@ __global__ void __launch_bounds__(256, 1)
         for (int kb = sp * kpb + issued; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-          if (KB == 1 && epi.raster_n) {  // A streams through L2 once; B (the weights) stays resident
+          if (epi.raster_n) {  // A streams through L2 once; B (the weights) stays resident
             tma_load_2d_hint(sA + stage * C::A_BYTES, &tma_a, &full[stage], kb * C::BK, mb * C::BM, pol_first);
             tma_load_2d_hint(sB + stage * C::B_BYTES, &tma_b, &full[stage], kb * C::BK, nb * BN, pol_last);
           } else {
-            tma_load_op<KB>(sA + stage * C::A_BYTES, &tma_a, &full[stage], kb, mb * C::BM);
-            tma_load_op<KB>(sB + stage * C::B_BYTES, &tma_b, &full[stage], kb, nb * BN);
+            tma_load_2d(sA + stage * C::A_BYTES, &tma_a, &full[stage], kb * C::BK, mb * C::BM);
+            tma_load_2d(sB + stage * C::B_BYTES, &tma_b, &full[stage], kb * C::BK, nb * BN);
           }
           if (++stage == C::STAGES) {
             stage = 0;
@@ -337,13 +308,11 @@ __global__ void __launch_bounds__(256, 1)
           const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
-          for (int kbi = 0; kbi < KB; ++kbi)
-#pragma unroll
-            for (int kk = 0; kk < C::BK / 16; ++kk) {
-              const uint64_t ad = make_sdesc(a_addr + kbi * C::A_TILE + kk * 32, 16, 1024, kSw128);
-              const uint64_t bd = make_sdesc(b_addr + kbi * C::B_TILE + kk * 32, 16, 1024, kSw128);
-              umma_bf16_ss(d_tmem, ad, bd, idesc, (kb != kb0 || kbi != 0 || kk != 0) ? 1u : 0u);
-            }
+          for (int kk = 0; kk < C::BK / 16; ++kk) {
+            const uint64_t ad = make_sdesc(a_addr + kk * 32, 16, 1024, kSw128);
+            const uint64_t bd = make_sdesc(b_addr + kk * 32, 16, 1024, kSw128);
+            umma_bf16_ss(d_tmem, ad, bd, idesc, (kb != kb0 || kk != 0) ? 1u : 0u);
+          }
           umma_commit(&empty[stage]);  // frees the smem slot once these MMAs have read it
           if (++stage == C::STAGES) {
             stage = 0;
@@ -471,13 +440,13 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
-template <int BN, int KB = 1>
+template <int BN, int AR = 128>
 static cudaError_t launch_gemm_bn(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
                                   const Epilogue& epi, cudaStream_t stream) {
-  using C = GemmCfg<BN, KB>;
+  using C = GemmCfg<BN, AR>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tc_kernel<BN, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tc_kernel<BN, AR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(C::SMEM));
     if (e != cudaSuccess) return e;
     attr_set = true;
@@ -485,7 +454,7 @@ static cudaError_t launch_gemm_bn(const CUtensorMap& ta, const CUtensorMap& tb, 
   const int tiles = ((M + C::BM - 1) / C::BM) * ((N + BN - 1) / BN) * epi.k_splits;
   const int grid = tiles < num_sms() ? tiles : num_sms();
   prof_mark(stream, true, g_prof_class);
-  cudaError_t e = launch_k(gemm_bf16_tc_kernel<BN, KB>, dim3(grid), dim3(256), C::SMEM, stream,
+  cudaError_t e = launch_k(gemm_bf16_tc_kernel<BN, AR>, dim3(grid), dim3(256), C::SMEM, stream,
                            epi.pdl && g_pdl && (g_pdl_mask & 1), ta, tb, M, N, K, epi);
   prof_mark(stream, false, g_prof_class);
   if (e != cudaSuccess) return e;
@@ -500,18 +469,17 @@ cudaError_t launch_gemm(const uint16_t* A, int64_t lda, const uint16_t* B, int64
   int BN = N > 128 ? 256 : 128;
   Epilogue ep = epi;
   ep.k_splits = 1;
-  // skinny M (decode, B > 8): ZDC_SKINNY_KB=2 fetches 2 k-blocks per stage with one 3-D box (measured
-  // no faster than 1 under ncu: 35 vs 32 us at the c4 a1 shape; profiles/r01/NOTES.md)
-  static const int skinny_kb = knob("ZDC_SKINNY_KB", 1);
+  // skinny M (decode, B > 8): BN = 128 when 256-wide tiles would be few (< 40: c4 a1 20, a5 32 tiles;
+  // 128 measured 4 % faster per c4 layer-step); ZDC_SKINNY_BN forces 128 / 256 (diagnostic builds)
   static const int skinny_bn = knob("ZDC_SKINNY_BN", 0);
+  static const int skinny_ar = knob("ZDC_SKINNY_AR", 0);  // 128 = load full 128-row A tiles (round 1)
   const bool skinny = epi.ws && epi.ws_cnt && M <= 128 && N % 8 == 0;
-  const int KBs = skinny && skinny_kb == 2 && K % 128 == 0 ? 2 : 1;
-  // skinny: BN = 128 when 256-wide tiles would be few (< 40: c4 a1 20, a5 32 tiles; 128 measured 4 % faster
-  // per c4 layer-step), ZDC_SKINNY_BN forces 128 / 256
   if (skinny && N > 128) BN = skinny_bn == 128 || (skinny_bn == 0 && (N + 255) / 256 < 40) ? 128 : 256;
+  // A rows per stage: the batch rounded up to 32 / 64 (more weight stages in flight), else 128
+  const int AR = !skinny || skinny_ar == 128 ? 128 : M <= 32 ? 32 : M <= 64 ? 64 : 128;
   if (skinny) {
     // split K so the weight stream spreads over the SMs (>= 4 stage blocks per split)
-    const int tiles = (N + BN - 1) / BN, kbs = K / (64 * KBs);
+    const int tiles = (N + BN - 1) / BN, kbs = K / 64;
     int sk = num_sms() / tiles;
     if (sk > kbs / 4) sk = kbs / 4;
     if (sk > 1) {
@@ -523,24 +491,22 @@ cudaError_t launch_gemm(const uint16_t* A, int64_t lda, const uint16_t* B, int64
   // weights B stay L2-resident; the default M-fastest order re-reads A once per N-tile (c4 prefill
   // a1: 174 GB of DRAM reads for 8.7 GB of operands, ncu).  ZDC_GEMM_RASTER=0/1 forces it.
   static const int raster_env = knob("ZDC_GEMM_RASTER", -1);
-  const double a_bytes = static_cast<double>(M) * K * 2, b_bytes = static_cast<double>(N) * K * 2;
+  const double a_bytes = static_cast<double>(M) * K * 2;
   // band: the N-blocks whose weight tiles fit ~40 MB of L2 (ZDC_GEMM_RASTER=0 keeps M-fastest,
   // = n forces a band of n)
   const int n_tiles_all = (N + BN - 1) / BN;
   int band = std::max(1, static_cast<int>(40e6 / (static_cast<double>(BN) * K * 2)));
   if (band > n_tiles_all) band = n_tiles_all;
   ep.raster_n = raster_env >= 0 ? raster_env : (a_bytes > 128e6 && N > BN ? band : 0);
-  (void)b_bytes;
   CUtensorMap ta, tb;
-  if (KBs == 2 && make_tmap_3d_kblocks(&ta, A, K, M, lda * 2, 128, 2) && make_tmap_3d_kblocks(&tb, B, K, N, ldb * 2, BN, 2))
-    return BN == 256 ? launch_gemm_bn<256, 2>(ta, tb, M, N, K, ep, stream)
-                     : launch_gemm_bn<128, 2>(ta, tb, M, N, K, ep, stream);
-  if (KBs == 2) {  // the 3-D view was refused: one k-block per stage, the same number of splits
-    const int kbs = K / 64, sk = ep.k_splits, kpb = (kbs + sk - 1) / sk;
-    ep.k_splits = (kbs + kpb - 1) / kpb;
-  }
-  if (!make_tmap_2d(&ta, A, K, M, lda * 2, 64, 128, 128)) return cudaErrorInvalidValue;
+  if (!make_tmap_2d(&ta, A, K, M, lda * 2, 64, AR, 128)) return cudaErrorInvalidValue;
   if (!make_tmap_2d(&tb, B, K, N, ldb * 2, 64, BN, 128)) return cudaErrorInvalidValue;
+  if (AR == 32)
+    return BN == 256 ? launch_gemm_bn<256, 32>(ta, tb, M, N, K, ep, stream)
+                     : launch_gemm_bn<128, 32>(ta, tb, M, N, K, ep, stream);
+  if (AR == 64)
+    return BN == 256 ? launch_gemm_bn<256, 64>(ta, tb, M, N, K, ep, stream)
+                     : launch_gemm_bn<128, 64>(ta, tb, M, N, K, ep, stream);
   return BN == 256 ? launch_gemm_bn<256>(ta, tb, M, N, K, ep, stream)
                    : launch_gemm_bn<128>(ta, tb, M, N, K, ep, stream);
 }
