@@ -18,6 +18,8 @@ Contents
   select_important  sort descending, top g^l fraction important
   OracleModel       prefill / decode over a compressed KV cache, with
                     zero-filled unimportant rows and layer groups     P:774-776 (DEL)
+  kmeans            K-means consolidation of calibration vectors      P:1157-1167 (§5.1 offline computation)
+  layer_groups      layers sharing the representative's classes       P:1455-1456 (repetition ratio > 95%)
 
 Readings of silent / ambiguous points are DESIGN.md §3 (c1..c19), cited inline.
 Every function here is pinned by tests/test_oracle_pins.py (P1-P13) except where a
@@ -104,7 +106,33 @@ def svd_right(A: np.ndarray):
     return s, canonical_signs(R)
 
 
-def fold_layer(dims, wq, wk, wv, wo, xc) -> Dict[str, np.ndarray]:
+def kmeans(X: np.ndarray, k: int, iters: int, row_block: int = 4096):
+    """P:1157-1167 (§5.1 "Offline rotation matrix computation"): "K-means is a common quantization
+    technique that consolidates vectors within each cluster by averaging them into a single vector."
+    Lloyd's algorithm as written (reading c21): centroid j starts at row floor(j n / k); each round
+    assigns every row to the nearest centroid by squared Euclidean distance (ties -> the lowest
+    centroid index) and replaces each centroid by the mean of its rows (an empty cluster keeps its
+    centroid); `iters` rounds.  k <= 0 or k >= n: no consolidation (the rows themselves).
+    Returns (centroids [k][dim], assignment of the last round [n])."""
+    X = np.asarray(X, dtype=np.float64)
+    n = X.shape[0]
+    if k <= 0 or k >= n:
+        return X.copy(), np.arange(n)
+    C = X[(np.arange(k) * n) // k].copy()
+    assign = np.zeros(n, dtype=np.int64)
+    for _ in range(iters):
+        for r0 in range(0, n, row_block):   # complete rows per block: identical to the unblocked argmin
+            xb = X[r0:r0 + row_block]
+            d2 = np.sum((xb[:, None, :] - C[None, :, :]) ** 2, axis=2)
+            assign[r0:r0 + row_block] = np.argmin(d2, axis=1)   # first minimum = lowest index
+        for j in range(k):
+            rows = X[assign == j]
+            if rows.shape[0]:
+                C[j] = rows.mean(axis=0)
+    return C, assign
+
+
+def fold_layer(dims, wq, wk, wv, wo, xc, k_clusters: int = 0, kmeans_iters: int = 0) -> Dict[str, np.ndarray]:
     """Offline fold of one layer (host, untimed).
 
     P:989-990 (§4.3): "since Q and K need the same R, we concatenate them into a
@@ -116,10 +144,17 @@ def fold_layer(dims, wq, wk, wv, wo, xc) -> Dict[str, np.ndarray]:
     P:1218-1219: W_V^h <- W_V^h R_h; [W_L^1, ...] <- [W_L^1 R^1, ...]; in Eq. 4's
     orientation (W_O^h is d_h x d) this is R_vl^T W_O^h (reading c1).
     Returns full-rank folded weights in the input shapes plus R and sigma per group.
+    k_clusters > 0: the Q, K and V vectors of the calibration rows are each
+    consolidated by kmeans() before stacking ("we conduct the K-means clustering on Q, K, and V,
+    respectively"); the W_L^h rows are not ("there is no need to use pruning and K-mean for W_L^h").
     """
+    def red(A):
+        return kmeans(A, k_clusters, kmeans_iters)[0] if k_clusters > 0 else A
+
     d, nh, nkv, dh = dims.d_model, dims.n_heads, dims.n_kv_heads, dims.d_head
     G = nh // nkv
-    if xc.shape[0] * (G + 1) < dh:
+    n_rows = min(xc.shape[0], k_clusters) if k_clusters > 0 else xc.shape[0]
+    if n_rows * (G + 1) < dh:
         raise ValueError("insufficient samples: n_calib*(G+1) < d_head")
     out = dict(r_qk=np.zeros((nkv, dh, dh)), r_vl=np.zeros((nkv, dh, dh)),
                sigma_qk=np.zeros((nkv, dh)), sigma_vl=np.zeros((nkv, dh)),
@@ -129,10 +164,10 @@ def fold_layer(dims, wq, wk, wv, wo, xc) -> Dict[str, np.ndarray]:
         heads = range(g * G, (g + 1) * G)
         cols_g = slice(g * dh, (g + 1) * dh)
         # QK pair: [Q^h for h in group; K^g] with Q^h = X_c W_Q^h (Eq. 1)
-        blocks = [xc @ wq[:, h * dh:(h + 1) * dh] for h in heads] + [xc @ wk[:, cols_g]]
+        blocks = [red(xc @ wq[:, h * dh:(h + 1) * dh]) for h in heads] + [red(xc @ wk[:, cols_g])]
         s_qk, R_qk = svd_right(np.vstack(blocks))
         # VW_L pair: [V^g; (W_O^h)^T for h in group]
-        blocks = [xc @ wv[:, cols_g]] + [wo[h * dh:(h + 1) * dh, :].T for h in heads]
+        blocks = [red(xc @ wv[:, cols_g])] + [wo[h * dh:(h + 1) * dh, :].T for h in heads]
         s_vl, R_vl = svd_right(np.vstack(blocks))
         out["r_qk"][g], out["r_vl"][g] = R_qk, R_vl
         out["sigma_qk"][g], out["sigma_vl"][g] = s_qk, s_vl
@@ -468,4 +503,27 @@ def sp_bytes_received_ulysses(P: int, B: int, S: int, n_h: int, n_kv: int, r_k: 
     cols1 = (n_h * r_k + n_kv * (r_k + r_v)) // P
     cols2 = n_h * r_v // P
     return (P - 1) * rows * (cols1 + cols2) * elem_bytes
+
+
+def layer_groups(classes: np.ndarray, threshold_bp: int = 9500) -> List[int]:
+    """"we offline identify layers that have the same important and unimportant token
+    sets (i.e., repetition ratio > 95%)"; the classification of a group's first layer is then
+    reused by the others.  Reading c22: consecutive layers; layer l joins the current
+    group when the fraction of (sequence, token) positions whose class equals the group
+    representative's exceeds threshold_bp / 10000 (strict, integer arithmetic), else it starts a
+    new group.  classes: bool [L][B][S] (every layer classified as its own representative).
+    Returns group_rep [L]."""
+    classes = np.asarray(classes, dtype=bool)
+    L = classes.shape[0]
+    total = int(classes[0].size)
+    rep = [0] * L
+    cur = 0
+    for l in range(1, L):
+        same = int(np.sum(classes[l] == classes[cur]))
+        if same * 10000 > threshold_bp * total:
+            rep[l] = cur
+        else:
+            cur = l
+            rep[l] = l
+    return rep
 

@@ -50,6 +50,14 @@ MUTANTS = [
      "self.length[l] = t + 1\n        self.K[l], self.V[l] = self.K[l][:, :, :-1], self.V[l][:, :, :-1]\n        O = np.zeros"),
     ("Ulysses bytes without all-to-all #2", "return (P - 1) * rows * (cols1 + cols2) * elem_bytes",
      "return (P - 1) * rows * cols1 * elem_bytes"),
+    ("k-means ties to the highest index", "assign[r0:r0 + row_block] = np.argmin(d2, axis=1)",
+     "assign[r0:r0 + row_block] = d2.shape[1] - 1 - np.argmin(d2[:, ::-1], axis=1)"),
+    ("k-means init from the first k rows", "C = X[(np.arange(k) * n) // k].copy()", "C = X[:k].copy()"),
+    ("k-means empty cluster reset to 0", "            if rows.shape[0]:\n                C[j] = rows.mean(axis=0)",
+     "            C[j] = rows.mean(axis=0) if rows.shape[0] else 0.0"),
+    ("layer groups compare to the previous layer", "same = int(np.sum(classes[l] == classes[cur]))",
+     "same = int(np.sum(classes[l] == classes[l - 1]))"),
+    ("layer groups >= threshold", "if same * 10000 > threshold_bp * total:", "if same * 10000 >= threshold_bp * total:"),
     ("SP bytes without (P-1)", "return (P - 1) * (S // P) * B * n_kv * (r_k + r_v) * elem_bytes",
      "return P * (S // P) * B * n_kv * (r_k + r_v) * elem_bytes"),
 ]

@@ -567,3 +567,66 @@ def test_P12_ulysses_bytes_by_element_tagging():
     assert abs(got / 1e9 - 0.235) < 0.0005
     # the all-gather of compressed K'/V' moves 0.940 GB there: P/2 = 4x more (MHA)
     assert O.sp_bytes_received(8, 1, 131072, 32, 64, 64) == 4 * got
+
+
+# ---------------------------------------------------------------- NEXT-3: K-means and layer groups
+def test_kmeans_golden():
+    """Hand-worked Lloyd rounds (golden/kmeans_examples.json, reading c21)."""
+    spec = json.load(open(os.path.join(GOLDEN, "kmeans_examples.json")))
+    for c in spec["cases"]:
+        C, a = O.kmeans(np.array(c["X"], dtype=float), c["k"], c["iters"])
+        assert np.array_equal(C, np.array(c["centroids"], dtype=float)), (c, C)
+        assert a.tolist() == c["assign"], (c, a)
+
+
+def test_kmeans_recovers_separated_clusters_and_objective_decreases():
+    """Blocks of rows around well-separated centres: the strided init picks one row per block and
+    one round gives the block means (computed here by reshape); the Lloyd objective never rises."""
+    rng = np.random.default_rng(8)
+    k, per, dim = 6, 40, 5
+    centres = rng.standard_normal((k, dim)) * 100.0
+    X = np.repeat(centres, per, axis=0) + rng.standard_normal((k * per, dim))
+    C, a = O.kmeans(X, k, 1)
+    assert np.allclose(C, X.reshape(k, per, dim).mean(axis=1), rtol=0, atol=1e-12)
+    assert a.tolist() == np.repeat(np.arange(k), per).tolist()
+    Y = rng.standard_normal((300, 4))
+    obj = []
+    for it in range(0, 7):
+        C, a = O.kmeans(Y, 9, it)
+        if it:
+            obj.append(float(np.sum((Y - C[a]) ** 2)))
+    assert all(obj[i + 1] <= obj[i] + 1e-12 for i in range(len(obj) - 1)), obj
+
+
+def test_kmeans_identity_and_fold_equivalence():
+    """k >= n (or 0) consolidates nothing, so the K-means fold equals the plain SVD fold."""
+    dims = Dims(1, 16, 2, 1, 8)
+    w = Z.layer_weights(dims, 1, 0)
+    xc = Z.calibration(dims, 1, 0, 40)
+    C, a = O.kmeans(xc, 40, 3)
+    assert np.array_equal(C, xc) and a.tolist() == list(range(40))
+    f0 = O.fold_layer(dims, w.wq, w.wk, w.wv, w.wo, xc)
+    f1 = O.fold_layer(dims, w.wq, w.wk, w.wv, w.wo, xc, k_clusters=40, kmeans_iters=5)
+    for key in ("r_qk", "r_vl", "wq_f", "wo_f"):
+        assert np.array_equal(f0[key], f1[key])
+    # with fewer clusters the QK stack is the centroids': its Gram equals the centroid Gram
+    f2 = O.fold_layer(dims, w.wq, w.wk, w.wv, w.wo, xc, k_clusters=10, kmeans_iters=4)
+    Aq = np.vstack([O.kmeans(xc @ w.wq[:, h * 8:(h + 1) * 8], 10, 4)[0] for h in range(2)] +
+                   [O.kmeans(xc @ w.wk, 10, 4)[0]])
+    ev = np.sort(np.linalg.eigvalsh(Aq.T @ Aq))[::-1]
+    assert np.allclose(f2["sigma_qk"][0] ** 2, np.maximum(ev, 0), rtol=1e-9, atol=1e-9 * ev[0])
+    assert np.max(np.abs(f2["r_qk"][0].T @ f2["r_qk"][0] - np.eye(8))) <= 1e-10
+
+
+def test_layer_groups_rule():
+    """P:1455-1456 repetition ratio > 95% (reading c22), on crafted classes: identical layers
+    join; a layer differing in exactly 5% of positions does NOT (strict >); 4.9% does."""
+    B, S = 2, 500
+    base = np.zeros((B, S), dtype=bool)
+    base[:, :250] = True
+    flip = lambda c, n: np.where(np.arange(B * S).reshape(B, S) < n, ~c, c)  # noqa: E731
+    cls = np.stack([base, base, flip(base, 49), flip(base, 50), flip(base, 50)])
+    # layer 3 differs from rep 0 in 50 of 1000 positions = 5.0% -> new group; layer 4 equals layer 3
+    assert O.layer_groups(cls, 9500) == [0, 0, 0, 3, 3]
+    assert O.layer_groups(cls, 10000) == [0, 1, 2, 3, 4]   # strict: no agreement exceeds 100 %
+    assert O.layer_groups(cls, 0) == [0, 0, 0, 0, 0]
