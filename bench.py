@@ -69,6 +69,7 @@ def parse():
     p.add_argument("--sp", action="store_true", help="also run the SP prefill at N = 1 (P = 1, no exchange)")
     p.add_argument("--no-sp", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-fold", action="store_true", help="skip the NEXT-3 GPU fold timing")
     p.add_argument("--no-uncompressed", action="store_true",
                    help="skip the r = d_h (R = I) baseline and the torch SDPA / matmul comparison")
     p.add_argument("--no-e2e", action="store_true")
@@ -685,6 +686,44 @@ def uncompressed_bench(args, zdc, torch, dev, stream, pre_ms_r, dec_ms_r, dec_by
     }
 
 
+# ------------------------------------------------------------------------------------ NEXT-3 fold
+def fold_bench(zdc, torch, dev, stream, n_calib=32768, k=2048, iters=5):
+    """NEXT-3: the offline fold of one c2-shaped layer on the GPU in fp64
+    (calibration capture -> K-means of every Q^h / K^g / V^g block -> Gram + Jacobi -> fold), with
+    n_calib calibration rows consolidated into k clusters by `iters` Lloyd rounds; plus the plain
+    (no K-means) GPU fold and the host TSQR + Jacobi fold at 4096 rows.  Timing-only random inputs."""
+    import zdc_synth as Z
+    dims = Z.dims_of(2, n_layers=1)
+    d, nh, nkv, dh = dims.d_model, dims.n_heads, dims.n_kv_heads, dims.d_head
+    g = torch.Generator(device=dev).manual_seed(31)
+    f64 = torch.float64
+    w = [torch.randn(d, nh * dh, device=dev, generator=g, dtype=f64) / math.sqrt(d),
+         torch.randn(d, nkv * dh, device=dev, generator=g, dtype=f64) / math.sqrt(d),
+         torch.randn(d, nkv * dh, device=dev, generator=g, dtype=f64) / math.sqrt(d),
+         torch.randn(nh * dh, d, device=dev, generator=g, dtype=f64) / math.sqrt(d)]
+    xc = torch.randn(n_calib, d, device=dev, generator=g, dtype=f64)
+    out = {"layer": "c2 (d 4096, 32 heads, d_h 128)"}
+    for name, rows, kk, it in (("kmeans", n_calib, k, iters), ("plain", 4096, 0, 0)):
+        zdc.fold_weights_gpu(dims, *w, xc[:rows], k_clusters=kk, kmeans_iters=it, return_device=True)  # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        zdc.fold_weights_gpu(dims, *w, xc[:rows], k_clusters=kk, kmeans_iters=it, return_device=True)
+        torch.cuda.synchronize()
+        out["gpu_%s" % name] = {"calib_rows": rows, "clusters": kk, "lloyd_rounds": it,
+                                "seconds_per_layer": round(time.perf_counter() - t0, 3)}
+    wh = [t.cpu().numpy() for t in w]
+    xh = xc[:4096].cpu().numpy()
+    t0 = time.perf_counter()
+    zdc.fold_weights(dims, *wh, xh)
+    out["host_plain"] = {"calib_rows": 4096, "seconds_per_layer": round(time.perf_counter() - t0, 3),
+                         "threads": os.cpu_count()}
+    out["gpu_kmeans"]["model_minutes_extrapolated"] = round(out["gpu_kmeans"]["seconds_per_layer"] * 32 / 60, 2)
+    out["paper"] = "rotation-matrix computation 7.8-282 min per model (P:1897-1901; A100 cluster, up to 1M clusters)"
+    del w, xc
+    torch.cuda.empty_cache()
+    return out
+
+
 # ------------------------------------------------------------------------------------ zdc arm
 def run_zdc(args):
     import torch
@@ -930,6 +969,15 @@ def run_zdc(args):
         except Exception as e:  # reported, never hides the main line
             unc = {"error": "%s: %s" % (type(e).__name__, e)}
 
+    # ---- NEXT-3: the offline fold on the GPU at calibration scale (N = 1)
+    fold = None
+    if world == 1 and not args.no_fold:
+        log("offline fold on the GPU (NEXT-3)")
+        try:
+            fold = fold_bench(zdc, torch, dev, stream)
+        except Exception as e:  # reported, never hides the main line
+            fold = {"error": "%s: %s" % (type(e).__name__, e)}
+
     # ---- CPU baseline (oracle as it stands), rank 0 at N=1 only
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -963,7 +1011,7 @@ def run_zdc(args):
                 "note": "whole decode layer-step inside the graph-replayed step: algorithmic bytes (packed "
                         "weights + K'/V' at the average context + x/y) / measured time per layer-step"},
             "clocks": clocks, "gpu_launches": kernels_per_step * args.steps,
-            "e2e": e2e, "cpu_baseline": cpu, "sp": sp, "other_configs": other, "baseline_uncompressed": unc,
+            "e2e": e2e, "cpu_baseline": cpu, "sp": sp, "other_configs": other, "baseline_uncompressed": unc, "offline_fold": fold,
         }
         print(json.dumps(out), flush=True)
     ctx.close()

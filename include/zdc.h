@@ -99,6 +99,34 @@ zdc_status zdc_fold_weights(const zdc_dims* dims,
                             double* r_qk, double* r_vl, double* sigma_qk, double* sigma_vl,
                             double* wq_f, double* wk_f, double* wv_f, double* wo_f);
 
+/* (1b) NEXT-3: the same fold on the GPU at the paper's calibration scale (§5.1:
+ * "we propose employing pruning and K-means clustering ... K-means ... consolidates vectors within
+ * each cluster by averaging them into a single vector ... we conduct the K-means clustering on Q,
+ * K, and V, respectively"; no K-means for W_L^h).  All pointers are DEVICE fp64, same
+ * shapes as zdc_fold_weights; `workspace` is caller-owned device memory of at least
+ * zdc_fold_gpu_workspace() bytes.  k_clusters <= 0 or >= n_calib: no consolidation (the plain fold
+ * of P:989-990); else kmeans_iters Lloyd rounds per Q^h / K^g / V^g block (reading c21: centroid j
+ * starts at row floor(j n / k), nearest by squared distance, ties -> lowest index, empty clusters
+ * keep their centroid).  R comes from a Jacobi eigen-decomposition of each stack's Gram matrix
+ * (eigenvectors = right singular vectors; sigma = sqrt(eigenvalue); canonical signs, reading c5).
+ * d_head must be even and <= 128 (ZDC_ERR_UNSUPPORTED).  Asynchronous on `stream`. */
+int64_t zdc_fold_gpu_workspace(const zdc_dims* dims, int64_t n_calib, int32_t k_clusters);
+zdc_status zdc_fold_weights_gpu(const zdc_dims* dims, const double* wq, const double* wk, const double* wv,
+                                const double* wo, const double* calib_x, int64_t n_calib, int32_t k_clusters,
+                                int32_t kmeans_iters, double* r_qk, double* r_vl, double* sigma_qk,
+                                double* sigma_vl, double* wq_f, double* wk_f, double* wv_f, double* wo_f,
+                                void* workspace, int64_t workspace_bytes, void* stream);
+
+/* NEXT-3 planner step (layers whose important / unimportant token sets repeat with
+ * ratio > 95% share one representative).  classes: host uint8 [n_layers][positions] (nonzero =
+ * important; every layer classified as its own representative, e.g. by zdc_cache_export after a
+ * calibration prefill); positions = B * S.  Consecutive layers: layer l joins the current group when
+ * the fraction of positions whose class equals the representative's exceeds threshold_bp / 10000
+ * (strict, exact integer arithmetic; reading c22), else it starts a new group.  Writes group_rep
+ * [n_layers] (a valid zdc_plan.group_rep). */
+zdc_status zdc_layer_groups(const uint8_t* classes, int32_t n_layers, int64_t positions, int32_t threshold_bp,
+                            int32_t* group_rep);
+
 /* ------------------------------------------------------------------------------------
  * Context: host metadata only.  Device memory is caller-owned: query the three sizes,
  * allocate (any allocator; 256-byte aligned), bind.  zdc_ctx_bind zeroes the regions;

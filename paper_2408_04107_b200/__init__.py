@@ -31,6 +31,7 @@ EXPORTED_SYMBOLS = ["zdc_last_error", "zdc_version", "zdc_fold_weights", "zdc_ct
                     "zdc_prefill", "zdc_decode", "zdc_comm_unique_id", "zdc_comm_init",
                     "zdc_sp_set_exchange_hook", "zdc_sp_prefill", "zdc_sp_positions",
                     "zdc_sp_prefill_ulysses", "zdc_sp_set_alltoall_hook",
+                    "zdc_fold_gpu_workspace", "zdc_fold_weights_gpu", "zdc_layer_groups",
                     "zdc_cache_export", "zdc_cache_length", "zdc_cache_sync", "zdc_scores_export", "zdc_cache_reset", "zdc_last_lse",
                     "zdc_gemm_bf16", "zdc_gemv_bf16", "zdc_prefill_attention_bf16",
                     "zdc_decode_attention_workspace", "zdc_decode_attention_bf16",
@@ -88,6 +89,9 @@ def lib():
             "zdc_last_error": ([], ctypes.c_char_p), "zdc_version": ([], ctypes.c_char_p),
             "zdc_fold_weights": ([ctypes.POINTER(Dims), dp, dp, dp, dp, dp, I64, dp, dp, dp, dp, dp, dp, dp, dp], I32),
             "zdc_ctx_create": ([ctypes.POINTER(Dims), ctypes.POINTER(Plan), I32, I32, ctypes.POINTER(P)], I32),
+            "zdc_fold_gpu_workspace": ([ctypes.POINTER(Dims), I64, I32], I64),
+            "zdc_layer_groups": ([P, I32, I64, I32, ctypes.POINTER(I32)], I32),
+            "zdc_fold_weights_gpu": ([ctypes.POINTER(Dims)] + [P] * 5 + [I64, I32, I32] + [P] * 8 + [P, I64, P], I32),
             "zdc_ctx_sizes": ([P, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)], I32),
             "zdc_ctx_bind": ([P, P, P, P], I32), "zdc_ctx_destroy": ([P], None),
             "zdc_load_folded": ([P, I32, dp, dp, dp, dp, P], I32),
@@ -223,6 +227,46 @@ def fold_weights(dims, wq, wk, wv, wo, xc):
                                 _dptr(out["wv_f"]), _dptr(out["wo_f"]))
     _check(st, "zdc_fold_weights")
     return out
+
+
+def fold_weights_gpu(dims, wq, wk, wv, wo, xc, k_clusters: int = 0, kmeans_iters: int = 0, stream=None,
+                     return_device: bool = False):
+    """zdc_fold_weights_gpu (NEXT-3): the fold on the GPU in fp64, with optional K-means
+    consolidation of the calibration Q / K / V vectors.  Host numpy (or device fp64 torch) inputs;
+    returns a dict like fold_weights (numpy, or device tensors with return_device=True)."""
+    import torch
+    dev = torch.device("cuda", torch.cuda.current_device())
+    t = lambda a: (a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))  # noqa: E731
+                   ).to(device=dev, dtype=torch.float64).contiguous()
+    wq, wk, wv, wo, xc = t(wq), t(wk), t(wv), t(wo), t(xc)
+    nkv, dh = dims.n_kv_heads, dims.d_head
+    out = dict(r_qk=torch.empty(nkv, dh, dh, dtype=torch.float64, device=dev),
+               r_vl=torch.empty(nkv, dh, dh, dtype=torch.float64, device=dev),
+               sigma_qk=torch.empty(nkv, dh, dtype=torch.float64, device=dev),
+               sigma_vl=torch.empty(nkv, dh, dtype=torch.float64, device=dev),
+               wq_f=torch.empty_like(wq), wk_f=torch.empty_like(wk), wv_f=torch.empty_like(wv), wo_f=torch.empty_like(wo))
+    D = make_dims(dims)
+    nbytes = int(lib().zdc_fold_gpu_workspace(ctypes.byref(D), xc.shape[0], int(k_clusters)))
+    ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=dev)
+    p = lambda x: ctypes.c_void_p(x.data_ptr())  # noqa: E731
+    _check(lib().zdc_fold_weights_gpu(ctypes.byref(D), p(wq), p(wk), p(wv), p(wo), p(xc), xc.shape[0], int(k_clusters),
+                                      int(kmeans_iters), p(out["r_qk"]), p(out["r_vl"]), p(out["sigma_qk"]),
+                                      p(out["sigma_vl"]), p(out["wq_f"]), p(out["wk_f"]), p(out["wv_f"]), p(out["wo_f"]),
+                                      p(ws), nbytes, ctypes.c_void_p(_stream(stream))), "zdc_fold_weights_gpu")
+    if return_device:
+        return out
+    torch.cuda.synchronize()
+    return {k: v.cpu().numpy() for k, v in out.items()}
+
+
+def layer_groups(classes, threshold_bp: int = 9500):
+    """zdc_layer_groups: classes bool/uint8 [L][B][S] -> group_rep list."""
+    c = np.ascontiguousarray(np.asarray(classes).astype(np.uint8))
+    L = c.shape[0]
+    out = (ctypes.c_int32 * L)()
+    _check(lib().zdc_layer_groups(ctypes.c_void_p(c.ctypes.data), L, int(c.size // L), int(threshold_bp), out),
+           "zdc_layer_groups")
+    return list(out)
 
 
 def sp_positions(S_total: int, world: int, rank: int, layout: int) -> np.ndarray:

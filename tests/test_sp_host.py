@@ -64,3 +64,22 @@ def test_gloo_world2_partition_and_bytes(layout):
             assert works[0] == works[1]
         else:
             assert works[0] < works[1]
+
+
+def test_layer_groups_library_equals_oracle():
+    """zdc_layer_groups (host C, NEXT-3 planner) is bit-exact with the oracle's layer_groups
+    (reading c22) on random and near-threshold class sets."""
+    import numpy as np
+    import oracle as O
+    import paper_2408_04107_b200 as zdc
+    rng = np.random.default_rng(12)
+    for trial in range(20):
+        L, B, S = 6, 2, int(rng.integers(50, 400))
+        base = rng.random((B, S)) < 0.5
+        cls = []
+        for l in range(L):
+            flip = rng.random((B, S)) < float(rng.choice([0.0, 0.02, 0.049, 0.05, 0.051, 0.2]))
+            cls.append(base ^ flip)
+        cls = np.stack(cls)
+        for thr in (9500, 9000, 9950, 0, 10000):
+            assert zdc.layer_groups(cls, thr) == O.layer_groups(cls, thr), (trial, thr)
