@@ -85,3 +85,37 @@ def test_gpu_fold_errors():
     with pytest.raises(zdc.ZdcError):   # 8 clusters x (G+1) < d_head
         zdc.fold_weights_gpu(dims, w.wq, w.wk, w.wv, w.wo, Z.calibration(dims, 1, 0, 512), k_clusters=8,
                              kmeans_iters=2)
+
+
+def test_layer_groups_from_gpu_classes():
+    """NEXT-3 planner on classes the GPU computed: every layer its own representative (g = 0.5),
+    layers 0 and 1 share weights (so, with the same input, identical token sets), layers 2 and 3 are
+    independent.  zdc_layer_groups on the exported classes gives [0, 0, 2, 3], the same
+    as the oracle's rule on the oracle's own classes."""
+    import paper_2408_04107_b200 as zdc
+    from zdc_synth import plan_split
+    from zdc_testlib import fold_stack
+    dims = Dims(4, 256, 4, 4, 64)
+    _, folded = fold_stack(dims, 1, n_calib=256)
+    folded[1] = folded[0]
+    plan = plan_split(4, 32, 16, [[0], [1], [2], [3]], [5000] * 4)
+    B, S = 2, 200
+    x = Z.prompt(dims, 1, B, S, seed=52)
+    ctx = zdc.Context(dims, plan, B, S)
+    for l, f in enumerate(folded):
+        g = f["lib"]
+        ctx.load_folded(l, g["wq_f"], g["wk_f"], g["wv_f"], g["wo_f"])
+    xd = to_dev_bf16(x)
+    y = torch.empty_like(xd)
+    for l in range(4):
+        ctx.prefill(xd, y, l, l + 1)
+    torch.cuda.synchronize()
+    cls = np.stack([ctx.cache_export(l, B)[2] for l in range(4)])
+    assert zdc.layer_groups(cls, 9500) == O.layer_groups(cls, 9500) == [0, 0, 2, 3]
+    m = O.OracleModel(dims, plan, folded, faithful=True)
+    for l in range(4):
+        m.prefill_layer(l, x)
+    ocls = np.stack([m.classes[l] for l in range(4)])
+    assert O.layer_groups(ocls, 9500) == [0, 0, 2, 3]
+    assert np.mean(ocls == cls) >= 0.98
+    ctx.close()
