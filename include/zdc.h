@@ -196,11 +196,14 @@ zdc_status zdc_decode(zdc_ctx* ctx, int32_t l0, int32_t l1, const uint16_t* x, u
  * Per layer: a1 on local tokens -> all-gather of K'/V' over NCCL (the only data moved;
  * bytes = (P-1)/P * B S N_kv (r_k + r_v) * 2) -> a3 for local queries against all keys at
  * or before their global position -> a5 on local rows.  The result rows equal the
- * zdc_prefill rows of the same tokens.  Token split under SP is not supported
- * (ZDC_ERR_UNSUPPORTED).  zdc_comm_init takes a 128-byte ncclUniqueId.  Each rank keeps the
+ * zdc_prefill rows of the same tokens.  Token split under SP (NEXT-2): a representative
+ * layer's importance scores of the local rows are all-gathered (B S/P f32 per rank) and every rank
+ * runs the same top-g selection over the whole sequence (identical classes and tau on every rank,
+ * equal to zdc_prefill's); unimportant rows are truncated to r^u in the gather buffer (the
+ * representative after classifying, the other layers of its group before their exchange).  zdc_comm_init takes a 128-byte ncclUniqueId.  Each rank keeps the
  * gathered compressed K'/V' of the whole sequence in its cache, in the gather layout
- * [P][K|V][B][N_kv][S/P][r]; zdc_decode / zdc_cache_export on such a layer return
- * ZDC_ERR_UNSUPPORTED (SP decode is NEXT-2).  Chunks (S/P, or S/(2P) for zigzag) must be
+ * [P][K|V][B][N_kv][S/P][r]; zdc_decode on such a layer returns ZDC_ERR_UNSUPPORTED, and
+ * zdc_cache_export exports only its classes and tau (k = v = NULL).  Chunks (S/P, or S/(2P) for zigzag) must be
  * multiples of 128 when P > 1.
  *   stats (optional, host): bytes exchanged per rank and the exchange time on the device.
  * ---------------------------------------------------------------------------------- */

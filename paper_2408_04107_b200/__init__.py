@@ -406,6 +406,16 @@ class Context:
                                       ctypes.c_void_p(_stream(stream))), "zdc_cache_export")
         return k, v, imp.astype(bool), tau
 
+    def classes_export(self, layer: int, B: int, stream=None):
+        """(is_important bool [B][len], tau [B]) of a layer's group, also for SP layers."""
+        length = self.cache_length(layer)
+        imp = np.zeros((B, length), dtype=np.uint8)
+        tau = np.zeros(B, dtype=np.float32)
+        ptr = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+        _check(lib().zdc_cache_export(self.h, layer, None, None, ptr(imp), ptr(tau), ctypes.c_void_p(_stream(stream))),
+               "zdc_cache_export")
+        return imp.astype(bool), tau
+
     def scores_export(self, layer: int, B: int, stream=None) -> np.ndarray:
         """GPU importance scores (f32) of every cached token of a representative layer."""
         length = self.cache_length(layer)

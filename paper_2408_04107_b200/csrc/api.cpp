@@ -877,8 +877,32 @@ zdc_status zdc_cache_export(const zdc_ctx* c, int32_t layer, float* k, float* v,
   if (!c) return fail(ZDC_ERR_INVALID_ARG, "zdc_cache_export: null ctx");
   if (!c->cache) return fail(ZDC_ERR_STATE, "zdc_cache_export: ctx not bound");
   if (layer < 0 || layer >= c->dims.n_layers) return fail(ZDC_ERR_SHAPE, "zdc_cache_export: layer %d", layer);
-  if (c->sp_layer[layer]) return fail(ZDC_ERR_UNSUPPORTED, "zdc_cache_export: layer %d holds an SP gather buffer", layer);
   const LayerInfo& L = c->layers[layer];
+  if (c->sp_layer[layer]) {
+    // an SP layer keeps a gather buffer (all-gather) or only its head groups (Ulysses): the rows
+    // are not exported; the classes and tau of a split group are (global positions)
+    if (k || v) return fail(ZDC_ERR_UNSUPPORTED, "zdc_cache_export: layer %d holds an SP-sharded cache (k, v)", layer);
+    ZDC_CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    const int B = c->batch, len = c->len[layer];
+    if (is_imp) {
+      if (!L.split) {
+        std::memset(is_imp, 1, static_cast<size_t>(B) * len);
+      } else {
+        for (int b = 0; b < B; ++b)
+          ZDC_CUDA_TRY(cudaMemcpy(is_imp + static_cast<int64_t>(b) * len,
+                                  c->cache + c->layers[L.rep].cls_off + static_cast<int64_t>(b) * c->max_seq, len,
+                                  cudaMemcpyDeviceToHost));
+      }
+    }
+    if (tau) {
+      if (L.split)
+        ZDC_CUDA_TRY(cudaMemcpy(tau, c->cache + c->layers[L.rep].tau_off, static_cast<size_t>(B) * 4,
+                                cudaMemcpyDeviceToHost));
+      else
+        for (int b = 0; b < B; ++b) tau[b] = INFINITY;
+    }
+    return ZDC_OK;
+  }
   const int B = c->batch, len = c->len[layer], Nkv = c->dims.n_kv_heads, S_cap = c->max_seq;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   ZDC_CUDA_TRY(cudaStreamSynchronize(st));

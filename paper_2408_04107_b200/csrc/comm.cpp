@@ -183,6 +183,20 @@ zdc_status zdc_sp_positions(int32_t S_total, int32_t world, int32_t rank, int32_
   return ZDC_OK;
 }
 
+// in-place all-gather of P equal slots of buf (slot q = rank q's chunk)
+static zdc_status sp_allgather(zdc_ctx* c, uint8_t* buf, int64_t chunk_bytes, cudaStream_t s) {
+  const int p = c->comm->rank;
+  if (c->comm->hook) {
+    c->comm->hook(c->comm->hook_user, buf, chunk_bytes, p, c->comm->world, s);
+    return ZDC_OK;
+  }
+  if (!c->comm->comm) return fail(ZDC_ERR_STATE, "zdc_sp_prefill: no NCCL communicator and no exchange hook");
+  ncclResult_t r = nccl_api()->AllGather(buf + p * chunk_bytes, buf, static_cast<size_t>(chunk_bytes), ncclUint8,
+                                         c->comm->comm, s);
+  if (r != ncclSuccess) return fail(ZDC_ERR_NCCL, "ncclAllGather: %s", nccl_api()->GetErrorString(r));
+  return ZDC_OK;
+}
+
 zdc_status zdc_sp_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, uint16_t* y, int32_t B,
                           int32_t S_total, int32_t layout, zdc_sp_stats* stats, void* stream) {
   if (!c || !x || !y) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_prefill: null argument");
@@ -205,7 +219,10 @@ zdc_status zdc_sp_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x,
     return fail(ZDC_ERR_CAPACITY, "zdc_sp_prefill: B=%d S_total=%d exceeds max_batch=%d max_seq=%d", B, S_total,
                 c->max_batch, c->max_seq);
   for (int l = l0; l < l1; ++l) {
-    if (c->layers[l].split) return fail(ZDC_ERR_UNSUPPORTED, "zdc_sp_prefill: token split under SP is NEXT-2 (layer %d)", l);
+    const LayerInfo& L = c->layers[l];
+    // a layer reusing classes needs its representative classified by an SP prefill of this prompt
+    if (L.split && L.rep != l && L.rep < l0 && c->sp_layer[L.rep] != 1)
+      return fail(ZDC_ERR_STATE, "zdc_sp_prefill: layer %d: representative %d has not classified this prompt", l, L.rep);
     if (c->len[l] != 0) return fail(ZDC_ERR_STATE, "zdc_sp_prefill: layer %d cache is not empty", l);
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -215,6 +232,14 @@ zdc_status zdc_sp_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x,
   float exch_ms = 0.f;
   int64_t bytes_recv = 0, bytes_recv_unc = 0;
   cudaEvent_t t_begin = nullptr, t_end = nullptr;
+  std::vector<cudaEvent_t> ev;  // exchange brackets, read after the loop (no per-layer host sync)
+  auto mark = [&]() -> cudaError_t {
+    cudaEvent_t e;
+    cudaError_t r = cudaEventCreate(&e);
+    if (r == cudaSuccess) r = cudaEventRecord(e, s);
+    ev.push_back(e);
+    return r;
+  };
   if (stats) {
     ZDC_CUDA_TRY(cudaEventCreate(&t_begin));
     ZDC_CUDA_TRY(cudaEventCreate(&t_end));
@@ -222,6 +247,9 @@ zdc_status zdc_sp_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x,
   }
   for (int l = l0; l < l1; ++l) {
     const LayerInfo& L = c->layers[l];
+    const LayerInfo& R = c->layers[L.rep];
+    const bool split_rep = L.split && L.rep == l, split_other = L.split && L.rep != l;
+    const uint8_t* rep_cls = c->cache + R.cls_off;  // [B][max_seq] classes of the group (global positions)
     const uint16_t* xin = l == l0 ? x : y;
     uint16_t* gbuf = reinterpret_cast<uint16_t*>(c->cache + L.k_off);  // [P][K|V][B][Nkv][n_local][r]
     const int64_t slot_rows = static_cast<int64_t>(B) * Nkv * n_local;
@@ -246,24 +274,17 @@ zdc_status zdc_sp_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x,
     q.pos0 = 0;
     g_prof_class = kProfGemmQkv;
     ZDC_CUDA_TRY(launch_gemm(xin, d, reinterpret_cast<const uint16_t*>(c->w + L.w_qkv), d, M, L.n_qkv, d, e1, s));
+    // a layer that reuses its representative's classes: unimportant rows of this rank's slot lose
+    // dims >= r^u BEFORE the exchange and the attention (P:774-776 DEL; reading c13)
+    if (split_other)
+      ZDC_CUDA_TRY(launch_sp_truncate(gbuf, p, p + 1, P, layout, S_total, B, Nkv, n_local, L.rk_p, L.rku, rep_cls,
+                                      c->max_seq, s));
     // a6: in-place all-gather of the compressed K'/V' slots
     const int64_t chunk_bytes = chunk_elems * 2;
     if (P > 1) {
-      if (stats) ZDC_CUDA_TRY(cudaEventRecord(c->comm->e0, s));
-      if (c->comm->hook) {
-        c->comm->hook(c->comm->hook_user, gbuf, chunk_bytes, p, P, s);
-      } else {
-        ncclResult_t r = nccl_api()->AllGather(gbuf + p * chunk_elems, gbuf, static_cast<size_t>(chunk_bytes), ncclUint8,
-                                               c->comm->comm, s);
-        if (r != ncclSuccess) return fail(ZDC_ERR_NCCL, "ncclAllGather: %s", nccl_api()->GetErrorString(r));
-      }
-      if (stats) {
-        ZDC_CUDA_TRY(cudaEventRecord(c->comm->e1, s));
-        ZDC_CUDA_TRY(cudaEventSynchronize(c->comm->e1));
-        float ms = 0.f;
-        ZDC_CUDA_TRY(cudaEventElapsedTime(&ms, c->comm->e0, c->comm->e1));
-        exch_ms += ms;
-      }
+      if (stats) ZDC_CUDA_TRY(mark());
+      if (zdc_status st = sp_allgather(c, reinterpret_cast<uint8_t*>(gbuf), chunk_bytes, s)) return st;
+      if (stats) ZDC_CUDA_TRY(mark());
       bytes_recv += (P - 1) * chunk_bytes;
       bytes_recv_unc += (P - 1) * 2 * slot_rows * c->dims.d_head * 2;
     }
@@ -298,6 +319,28 @@ zdc_status zdc_sp_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x,
       a.q_pos0 = sp_position(S_total, P, p, layout, a.q_row0);
       ZDC_CUDA_TRY(launch_prefill_attention(a, s));
     }
+    if (split_rep) {
+      // a4 under SP (NEXT-2): scores of the local rows -> all-gather -> the same global top-g
+      // selection on every rank (identical inputs, deterministic select) -> truncate the stored rows
+      float* slots = reinterpret_cast<float*>(c->scratch + c->s_sp);  // [P][B][n_local]
+      const int64_t sc_chunk = static_cast<int64_t>(B) * n_local * 4;
+      ZDC_CUDA_TRY(launch_sp_importance(reinterpret_cast<const float*>(c->scratch + c->s_lse), n_local, Nh, B,
+                                        c->importance_mode, S_total, P, p, layout,
+                                        slots + static_cast<int64_t>(p) * B * n_local, s));
+      if (P > 1) {
+        if (stats) ZDC_CUDA_TRY(mark());
+        if (zdc_status st = sp_allgather(c, reinterpret_cast<uint8_t*>(slots), sc_chunk, s)) return st;
+        if (stats) ZDC_CUDA_TRY(mark());
+        bytes_recv += (P - 1) * sc_chunk;
+        bytes_recv_unc += (P - 1) * sc_chunk;
+      }
+      float* scores = reinterpret_cast<float*>(c->cache + L.score_off);
+      ZDC_CUDA_TRY(launch_sp_scores_global(slots, P, B, n_local, S_total, layout, scores, c->max_seq, s));
+      ZDC_CUDA_TRY(launch_select(scores, c->max_seq, S_total, L.g_bp, B, c->cache + L.cls_off,
+                                 reinterpret_cast<float*>(c->cache + L.tau_off), s));
+      ZDC_CUDA_TRY(launch_sp_truncate(gbuf, 0, P, P, layout, S_total, B, Nkv, n_local, L.rk_p, L.rku,
+                                      c->cache + L.cls_off, c->max_seq, s));
+    }
     // a5
     Epilogue e5;
     e5.mode = 0;
@@ -320,6 +363,12 @@ zdc_status zdc_sp_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x,
     ZDC_CUDA_TRY(cudaEventElapsedTime(&tot, t_begin, t_end));
     cudaEventDestroy(t_begin);
     cudaEventDestroy(t_end);
+    for (size_t i = 0; i + 1 < ev.size(); i += 2) {
+      float ms = 0.f;
+      ZDC_CUDA_TRY(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+      exch_ms += ms;
+    }
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
     stats->bytes_recv = bytes_recv;
     stats->bytes_sent = bytes_recv;  // all-gather: each slot goes to the P-1 peers
     stats->bytes_recv_uncompressed = bytes_recv_unc;

@@ -58,6 +58,14 @@ struct Epilogue {
 };
 
 #ifdef __CUDACC__
+// SP layouts: global position of local row t of rank q (0 contiguous, 1 zigzag: chunks q, 2P-1-q)
+__device__ __forceinline__ int sp_global_pos(int S, int P, int q, int layout, int t) {
+  const int n = S / P;
+  if (layout == 0) return q * n + t;
+  const int c = S / (2 * P);
+  return t < c ? q * c + t : (2 * P - 1 - q) * c + (t - c);
+}
+
 // Decode length advance (one thread, after every reader of the old length): saturates at len_cap;
 // a step that found the cache full sets the overflow flag instead (zdc_cache_sync reports it).
 __device__ __forceinline__ void advance_len(const Epilogue& e) {
@@ -108,6 +116,19 @@ struct PrefillAttnArgs {
   int64_t kv_rows_total = 0;  // rows of the K/V tensor maps (0 = B * Nkv * S_cap)
 };
 cudaError_t launch_prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream);
+
+// ---- SP x token split (sp_split.cu, NEXT-2): the global top-g selection across ranks
+// scores of this rank's local query rows (global positions for the mean-mode adjustment) into its
+// slot out[B][n_local]; lse [B][Nh][n_local]
+cudaError_t launch_sp_importance(const float* lse, int n_local, int Nh, int B, int mode, int S, int P, int p,
+                                 int layout, float* out, cudaStream_t s);
+// gathered score slots [P][B][n_local] -> scores [B][ld] in global position order
+cudaError_t launch_sp_scores_global(const float* slots, int P, int B, int n_local, int S, int layout, float* scores,
+                                    int64_t ld, cudaStream_t s);
+// zero dims [r_u, w) of the rows of unimportant tokens in gather-buffer slots [q0, q1) of
+// [P][K|V][B][Nkv][n_local][w] (class of (b, position) at cls[b ld + position])
+cudaError_t launch_sp_truncate(uint16_t* gbuf, int q0, int q1, int P, int layout, int S, int B, int Nkv, int n_local,
+                               int w, int r_u, const uint8_t* cls, int64_t ld_cls, cudaStream_t s);
 
 // ---- Ulysses SP re-layouts (sp_ulysses.cu).  Global position of local row t of rank q:
 // layout 0 contiguous (q n + t), 1 zigzag (chunks q and 2P-1-q of 2P).

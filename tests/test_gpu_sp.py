@@ -25,7 +25,16 @@ def _cudart():
     raise OSError("libcudart not found")
 
 
-DIMS = {"mha": (2, 256, 4, 2, 64, 32), "gqa4": (2, 256, 8, 4, 64, 32)}
+DIMS = {"mha": (2, 256, 4, 2, 64, 32), "gqa4": (2, 256, 8, 4, 64, 32), "split": (2, 256, 4, 2, 64, 32),
+        "split_mean": (2, 256, 4, 2, 64, 32)}
+
+
+def _plan(shape):
+    import zdc_synth as Z
+    r = DIMS[shape][5]
+    if shape.startswith("split"):   # both layers one group, layer 0 the representative, g = 0.45
+        return Z.plan_split(2, r, 16, [[0, 1]], [4500], importance_mode=1 if shape == "split_mean" else 0)
+    return Z.plan_uniform(2, r)
 
 
 def _worker(rank, world, port, layout, S, B, out_q, dataflow="allgather", shape="mha"):
@@ -39,7 +48,7 @@ def _worker(rank, world, port, layout, S, B, out_q, dataflow="allgather", shape=
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     dims = Z.Dims(*DIMS[shape][:5])
-    plan = Z.plan_uniform(2, DIMS[shape][5])
+    plan = _plan(shape)
     _, folded = fold_stack(dims, 1, n_calib=256)
     ctx = zdc.Context(dims, plan, B, S)
     for l, f in enumerate(folded):
@@ -75,13 +84,17 @@ def _worker(rank, world, port, layout, S, B, out_q, dataflow="allgather", shape=
     yl = torch.empty_like(xl)
     stats = ctx.sp_prefill(xl, yl, S_total=S, layout=layout, stats=True, dataflow=dataflow)
     torch.cuda.synchronize()
-    out_q.put((rank, pos, yl.float().cpu().numpy(), stats))
+    extra = None
+    if shape.startswith("split"):
+        extra = ctx.classes_export(0, B) + (ctx.scores_export(0, B),)
+    out_q.put((rank, pos, yl.float().cpu().numpy(), stats, extra))
     dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("world,layout,dataflow,shape", [
     (2, 0, "allgather", "mha"), (2, 1, "allgather", "mha"), (4, 1, "allgather", "mha"),
-    (2, 0, "ulysses", "mha"), (2, 1, "ulysses", "mha"), (4, 1, "ulysses", "gqa4")])
+    (2, 0, "ulysses", "mha"), (2, 1, "ulysses", "mha"), (4, 1, "ulysses", "gqa4"),
+    (2, 1, "allgather", "split"), (4, 1, "allgather", "split_mean"), (2, 0, "allgather", "split_mean")])
 def test_sp_prefill_equals_single_gpu_rows(world, layout, dataflow, shape):
     import multiprocessing as pymp
     import oracle as O
@@ -104,19 +117,36 @@ def test_sp_prefill_equals_single_gpu_rows(world, layout, dataflow, shape):
     # single-process reference through zdc_prefill
     dims = Z.Dims(*DIMS[shape][:5])
     r = DIMS[shape][5]
-    plan = Z.plan_uniform(2, r)
+    plan = _plan(shape)
     _, folded = fold_stack(dims, 1, n_calib=256)
     x = Z.prompt(dims, 1, B, S, seed=41)
     ctx = make_context(dims, plan, folded, B, S)
     xd = to_dev_bf16(x)
     y = torch.empty_like(xd)
-    ctx.prefill(xd, y)
+    ctx.prefill(xd, y, 0, 1)
+    y0 = torch.empty_like(xd)
+    if shape.startswith("split"):   # the SP run chains layer 0 -> 1: the single run does the same
+        ctx.prefill(y, y0, 1, 2)
+        y, y0 = y0, y
+    else:
+        ctx.prefill(y, y0, 1, 2)
+        y, y0 = y0, y
     torch.cuda.synchronize()
     y_single = y.float().cpu().numpy()
+    if shape.startswith("split"):
+        cls_single, tau_single = ctx.classes_export(0, B)
+        sc_single = ctx.scores_export(0, B)
     want = O.OracleModel(dims, plan, folded, faithful=True).prefill(x)
     covered = []
-    for rank, pos, yl, stats in res:
+    for rank, pos, yl, stats, extra in res:
         assert np.array_equal(yl, y_single[:, pos]), rank      # bit-identical rows
+        if extra is not None:   # NEXT-2: the global top-g selection equals the single-GPU one
+            cls_sp, tau_sp, sc_sp = extra
+            assert np.array_equal(sc_sp, sc_single), rank
+            assert np.array_equal(cls_sp, cls_single) and np.array_equal(tau_sp, tau_single), rank
+            for b in range(B):
+                c_o, t_o, _ = O.select_important(sc_sp[b], plan.g_bp[0])
+                assert c_o.tolist() == cls_sp[b].tolist()
         assert normwise(yl, want[:, pos]) <= 2e-2
         covered += pos.tolist()
         nh, nkv, dh = dims.n_heads, dims.n_kv_heads, dims.d_head
@@ -124,6 +154,9 @@ def test_sp_prefill_equals_single_gpu_rows(world, layout, dataflow, shape):
             # bytes received per rank and layer: (P-1)/P * B * S * N_kv * (r_k + r_v) * 2, two layers
             want_b = O.sp_bytes_received(world, B, S, nkv, r, r)
             want_u = O.sp_bytes_received(world, B, S, nkv, dh, dh)
+            if extra is not None:   # + the representative's scores: (P-1) * B * S/P f32, once
+                want_b += (world - 1) * B * (S // world) * 4 / 2
+                want_u += (world - 1) * B * (S // world) * 4 / 2
         else:
             # both all-to-alls (compressed Q'/K'/V' of this rank's heads, then O' back)
             want_b = O.sp_bytes_received_ulysses(world, B, S, nh, nkv, r, r)
