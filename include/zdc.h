@@ -247,6 +247,18 @@ zdc_status zdc_sp_prefill_ulysses(zdc_ctx* ctx, int32_t l0, int32_t l1, const ui
 typedef void (*zdc_alltoall_fn)(void* user, const void* send, void* recv, int64_t chunk_bytes, int32_t rank,
                                 int32_t world, void* stream);
 zdc_status zdc_sp_set_alltoall_hook(zdc_ctx* ctx, zdc_alltoall_fn fn, void* user, int32_t rank, int32_t world);
+/* (4c) NEXT-2: decode over the sequence-sharded compressed cache an all-gather zdc_sp_prefill left
+ * (non-split layers).  One token per sequence on EVERY rank (same x on every rank, replicated a1/a5):
+ * decode token j (j = 0, 1, ... after the prompt) is appended by rank j mod P only, into that rank's
+ * tail of S/P rows per (sequence, KV head) after the gather buffer (needs max_seq >= S + S/P;
+ * ZDC_ERR_CAPACITY past S/P decode tokens per rank).  Each rank attends over ITS keys only (its
+ * prompt slot + its decode rows, the split-K kernel with two pools) -> {O'_p, LSE_p}; the ranks
+ * all-gather these partials (B N_h (r_v + 1) f32 each) and every rank merges them by LSE (the
+ * softmax of P:254-260 over the union of the key sets), then a5.  y rows equal zdc_decode's up to
+ * the bf16 rounding of the partial O'_p.  Host-driven (no caller graph capture); B must equal the
+ * SP prefill's batch. */
+zdc_status zdc_sp_decode(zdc_ctx* ctx, int32_t l0, int32_t l1, const uint16_t* x, uint16_t* y, int32_t B,
+                         void* stream);
 /* Host helper: the global token positions rank `rank` holds (n = S_total / world). */
 zdc_status zdc_sp_positions(int32_t S_total, int32_t world, int32_t rank, int32_t layout,
                             int32_t* positions);

@@ -31,7 +31,7 @@ EXPORTED_SYMBOLS = ["zdc_last_error", "zdc_version", "zdc_fold_weights", "zdc_ct
                     "zdc_prefill", "zdc_decode", "zdc_comm_unique_id", "zdc_comm_init",
                     "zdc_sp_set_exchange_hook", "zdc_sp_prefill", "zdc_sp_positions",
                     "zdc_sp_prefill_ulysses", "zdc_sp_set_alltoall_hook",
-                    "zdc_fold_gpu_workspace", "zdc_fold_weights_gpu", "zdc_layer_groups",
+                    "zdc_fold_gpu_workspace", "zdc_fold_weights_gpu", "zdc_layer_groups", "zdc_sp_decode",
                     "zdc_cache_export", "zdc_cache_length", "zdc_cache_sync", "zdc_scores_export", "zdc_cache_reset", "zdc_last_lse",
                     "zdc_gemm_bf16", "zdc_gemv_bf16", "zdc_prefill_attention_bf16",
                     "zdc_decode_attention_workspace", "zdc_decode_attention_bf16",
@@ -104,6 +104,7 @@ def lib():
             "zdc_sp_prefill": ([P, I32, I32, P, P, I32, I32, I32, ctypes.POINTER(SpStats), P], I32),
             "zdc_sp_prefill_ulysses": ([P, I32, I32, P, P, I32, I32, I32, ctypes.POINTER(SpStats), P], I32),
             "zdc_sp_set_alltoall_hook": ([P, ALLTOALL_FN, P, I32, I32], I32),
+            "zdc_sp_decode": ([P, I32, I32, P, P, I32, P], I32),
             "zdc_sp_positions": ([I32, I32, I32, I32, ctypes.POINTER(I32)], I32),
             "zdc_cache_export": ([P, I32, P, P, P, P, P], I32),
             "zdc_cache_length": ([P, I32, ctypes.POINTER(I32)], I32),
@@ -458,6 +459,12 @@ class Context:
                     "bytes_recv_uncompressed": st.bytes_recv_uncompressed, "exchange_ms": st.exchange_ms,
                     "total_ms": st.total_ms}
         return None
+
+    def sp_decode(self, x, y, l0: int = 0, l1: Optional[int] = None, stream=None):
+        """zdc_sp_decode: one token per sequence over the sequence-sharded cache of an SP prefill."""
+        l1 = self.dims.n_layers if l1 is None else l1
+        _check(lib().zdc_sp_decode(self.h, l0, l1, _tptr(x, "bf16"), _tptr(y, "bf16"), x.shape[0],
+                                   ctypes.c_void_p(_stream(stream))), "zdc_sp_decode")
 
     def reset(self, stream=None):
         _check(lib().zdc_cache_reset(self.h, ctypes.c_void_p(_stream(stream))), "zdc_cache_reset")

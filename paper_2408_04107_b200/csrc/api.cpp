@@ -121,6 +121,7 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
   c->layers.resize(d.n_layers);
   c->len.assign(d.n_layers, 0);
   c->sp_layer.assign(d.n_layers, 0);
+  c->sp_prompt.assign(d.n_layers, 0);
   int64_t woff = 0, coff = 0;
   int max_nq = 0, max_ko = 0, max_rv = 0, max_split_w = 0, max_nqkv = 0;
   bool any_split = false;
@@ -296,6 +297,7 @@ zdc_status zdc_ctx_bind(zdc_ctx* c, void* w, void* cache, void* scratch) {
   }
   c->len.assign(c->dims.n_layers, 0);
   c->sp_layer.assign(c->dims.n_layers, 0);
+  c->sp_prompt.assign(c->dims.n_layers, 0);
   c->batch = 0;
   return ZDC_OK;
 }
@@ -861,6 +863,7 @@ zdc_status zdc_cache_reset(zdc_ctx* c, void* stream) {
                                static_cast<cudaStream_t>(stream)));
   c->len.assign(c->dims.n_layers, 0);
   c->sp_layer.assign(c->dims.n_layers, 0);
+  c->sp_prompt.assign(c->dims.n_layers, 0);
   c->batch = 0;
   return ZDC_OK;
 }

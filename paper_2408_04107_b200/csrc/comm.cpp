@@ -352,6 +352,7 @@ zdc_status zdc_sp_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x,
     g_prof_class = kProfOther;
     c->len[l] = S_total;
     c->sp_layer[l] = 1;
+    c->sp_prompt[l] = S_total;
     c->last_layer = l;
     c->last_T = n_local;
   }
@@ -552,6 +553,131 @@ zdc_status zdc_sp_prefill_ulysses(zdc_ctx* c, int32_t l0, int32_t l1, const uint
     stats->bytes_recv_uncompressed = bytes_recv_unc;
     stats->exchange_ms = exch_ms;
     stats->total_ms = tot;
+  }
+  return ZDC_OK;
+}
+
+zdc_status zdc_sp_decode(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, uint16_t* y, int32_t B, void* stream) {
+  if (!c || !x || !y) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_decode: null argument");
+  if (x == y) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_decode: x and y alias");
+  if (!c->w || !c->comm) return fail(ZDC_ERR_STATE, "zdc_sp_decode: ctx not bound / no communicator");
+  if (l0 < 0 || l1 > c->dims.n_layers || l0 >= l1) return fail(ZDC_ERR_SHAPE, "zdc_sp_decode: layer range [%d, %d)", l0, l1);
+  if (B != c->batch) return fail(ZDC_ERR_SHAPE, "zdc_sp_decode: B=%d but the SP prefill had B=%d", B, c->batch);
+  const int P = c->comm->world, p = c->comm->rank;
+  const int d = c->dims.d_model, Nh = c->dims.n_heads, Nkv = c->dims.n_kv_heads;
+  for (int l = l0; l < l1; ++l) {
+    const LayerInfo& L = c->layers[l];
+    if (c->sp_layer[l] != 1)
+      return fail(ZDC_ERR_STATE, "zdc_sp_decode: layer %d was not prefilled by zdc_sp_prefill (all-gather)", l);
+    if (L.split) return fail(ZDC_ERR_UNSUPPORTED, "zdc_sp_decode: layer %d has a token split", l);
+    const int S = c->sp_prompt[l], n_local = S / P, j = c->len[l] - S;
+    // this rank's decode tail has n_local rows per (sequence, KV head), after the gather buffer
+    if (j / P + 1 > n_local || S + n_local > c->max_seq)
+      return fail(ZDC_ERR_CAPACITY, "zdc_sp_decode: layer %d: decode token %d exceeds the sharded tail (%d rows per rank, "
+                  "max_seq >= S + S/P needed)", l, j, n_local);
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  g_launches = 0;
+  uint8_t* sp = c->scratch + c->s_sp;
+  for (int l = l0; l < l1; ++l) {
+    const LayerInfo& L = c->layers[l];
+    const uint16_t* xin = l == l0 ? x : y;
+    const int S = c->sp_prompt[l], n_local = S / P, j = c->len[l] - S;
+    const int owner = j % P, own_before = (j + P - 1 - p) / P;  // decode tokens this rank held before
+    const int64_t slot_rows = static_cast<int64_t>(B) * Nkv * n_local;
+    uint16_t* gbuf = reinterpret_cast<uint16_t*>(c->cache + L.k_off);
+    uint16_t* tail_k = gbuf + 2 * static_cast<int64_t>(P) * slot_rows * L.rk_p;  // [B][Nkv][n_local][r]
+    uint16_t* tail_v = tail_k + slot_rows * L.rk_p;
+    // scratch: per-sequence pool counts, the new K'/V' rows, the exchanged partials
+    int* n0 = reinterpret_cast<int*>(sp);
+    int* n1 = n0 + B;
+    uint16_t* knew = reinterpret_cast<uint16_t*>(sp + 4096);
+    uint16_t* vnew = knew + static_cast<int64_t>(B) * Nkv * L.rk_p;
+    float* parts = reinterpret_cast<float*>(sp + 4096 + 4 * static_cast<int64_t>(B) * Nkv * L.rk_p + 4096);
+    // a1 (replicated: every rank has the weights): Q' to staging, the new K'/V' rows to knew/vnew
+    Epilogue e1;
+    e1.mode = 1;
+    QkvDest& q = e1.qkv;
+    q.q = reinterpret_cast<uint16_t*>(c->scratch + c->s_q);
+    q.ldq = L.nq;
+    q.nq = L.nq;
+    q.nk = L.nk;
+    q.k = knew;
+    q.v = vnew;
+    q.rk = L.rk_p;
+    q.rv = L.rv_p;
+    q.S = 1;
+    q.kg = L.rk_p;
+    q.kb = static_cast<int64_t>(Nkv) * L.rk_p;
+    q.vg = L.rv_p;
+    q.vb = static_cast<int64_t>(Nkv) * L.rv_p;
+    q.pos0 = 0;
+    const uint16_t* wqkv = reinterpret_cast<const uint16_t*>(c->w + L.w_qkv);
+    if (gemv_supported(B, d))
+      ZDC_CUDA_TRY(launch_gemv(wqkv, xin, d, B, L.n_qkv, d, e1, s));
+    else
+      ZDC_CUDA_TRY(launch_gemm(xin, d, wqkv, d, B, L.n_qkv, d, e1, s));
+    // a2: the owner appends the new token to its tail (decode token j -> rank j mod P)
+    const int own_now = own_before + (owner == p ? 1 : 0);
+    if (owner == p) {
+      ZDC_CUDA_TRY(cudaMemcpy2DAsync(tail_k + static_cast<int64_t>(own_before) * L.rk_p, n_local * L.rk_p * 2, knew,
+                                     L.rk_p * 2, L.rk_p * 2, static_cast<size_t>(B) * Nkv, cudaMemcpyDeviceToDevice, s));
+      ZDC_CUDA_TRY(cudaMemcpy2DAsync(tail_v + static_cast<int64_t>(own_before) * L.rv_p, n_local * L.rv_p * 2, vnew,
+                                     L.rv_p * 2, L.rv_p * 2, static_cast<size_t>(B) * Nkv, cudaMemcpyDeviceToDevice, s));
+    }
+    std::vector<int> hcnt(2 * B);
+    for (int b = 0; b < B; ++b) {
+      hcnt[b] = n_local;
+      hcnt[B + b] = own_now;
+    }
+    ZDC_CUDA_TRY(cudaMemcpyAsync(n0, hcnt.data(), 2 * B * sizeof(int), cudaMemcpyHostToDevice, s));
+    // a3 over this rank's keys: pool 0 = its prompt slot, pool 1 = the decode rows it owns
+    DecodeAttnArgs a;
+    a.q = reinterpret_cast<const uint16_t*>(c->scratch + c->s_q);
+    a.ldq = L.nq;
+    a.k = gbuf + static_cast<int64_t>(p) * 2 * slot_rows * L.rk_p;
+    a.v = a.k + slot_rows * L.rk_p;
+    a.rk = L.rk_p;
+    a.rv = L.rv_p;
+    a.k1 = tail_k;
+    a.v1 = tail_v;
+    a.rk1 = L.rk_p;
+    a.rv1 = L.rv_p;
+    a.S_cap = n_local;
+    a.len = n_local;
+    a.n0_ptr = n0;
+    a.n1_ptr = n1;
+    a.o = reinterpret_cast<uint16_t*>(c->scratch + c->s_o);
+    a.ldo = L.ko_p;
+    a.lse = reinterpret_cast<float*>(c->scratch + c->s_lse);
+    a.part = reinterpret_cast<float*>(c->scratch + c->s_part);
+    a.counters = reinterpret_cast<int*>(c->scratch + c->s_cnt);
+    a.B = B;
+    a.Nh = Nh;
+    a.Nkv = Nkv;
+    a.scale = 1.0f / std::sqrt(static_cast<float>(c->dims.d_head));
+    a.splits = decode_splits(B, Nkv, n_local);
+    ZDC_CUDA_TRY(launch_decode_attention(a, s));
+    // exchange {O'_p, LSE_p} and merge over the ranks (the LSE merge of P:254-260's softmax)
+    const int64_t chunk = static_cast<int64_t>(B) * Nh * (L.rv_p + 1) * 4;
+    ZDC_CUDA_TRY(launch_sp_decode_pack(a.o, L.ko_p, a.lse, B, Nh, L.rv_p,
+                                       parts + static_cast<int64_t>(p) * B * Nh * (L.rv_p + 1), s));
+    if (P > 1)
+      if (zdc_status st = sp_allgather(c, reinterpret_cast<uint8_t*>(parts), chunk, s)) return st;
+    ZDC_CUDA_TRY(launch_sp_decode_merge(parts, P, B, Nh, L.rv_p, a.o, L.ko_p, a.lse, s));
+    // a5 (replicated)
+    Epilogue e5;
+    e5.mode = 0;
+    e5.d = y;
+    e5.ldd = d;
+    const uint16_t* wo = reinterpret_cast<const uint16_t*>(c->w + L.w_o);
+    if (gemv_supported(B, L.ko_p))
+      ZDC_CUDA_TRY(launch_gemv(wo, a.o, L.ko_p, B, d, L.ko_p, e5, s));
+    else
+      ZDC_CUDA_TRY(launch_gemm(a.o, L.ko_p, wo, L.ko_p, B, d, L.ko_p, e5, s));
+    c->len[l] += 1;
+    c->last_layer = l;
+    c->last_T = 1;
   }
   return ZDC_OK;
 }

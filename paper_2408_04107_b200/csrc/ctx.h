@@ -56,6 +56,7 @@ struct zdc_ctx {
   uint8_t* scratch = nullptr;
   std::vector<int> len;  // per-layer cache length
   std::vector<int> sp_layer;  // 1 = the layer's cache holds an SP gather buffer (not position-ordered)
+  std::vector<int> sp_prompt;  // SP prefill length of each such layer (zdc_sp_decode counts tokens after it)
   int batch = 0;
   int last_layer = -1, last_T = 0;
   zdc::CommState* comm = nullptr;

@@ -130,6 +130,13 @@ cudaError_t launch_sp_scores_global(const float* slots, int P, int B, int n_loca
 cudaError_t launch_sp_truncate(uint16_t* gbuf, int q0, int q1, int P, int layout, int S, int B, int Nkv, int n_local,
                                int w, int r_u, const uint8_t* cls, int64_t ld_cls, cudaStream_t s);
 
+// SP decode partial merge: {O'_p bf16 [B][ldo], LSE_p [B][Nh]} -> f32 slot [B][Nh][rv+1]; slots
+// [P][...] -> O' (bf16) and LSE merged over the ranks
+cudaError_t launch_sp_decode_pack(const uint16_t* o, int64_t ldo, const float* lse, int B, int Nh, int rv, float* slot,
+                                  cudaStream_t s);
+cudaError_t launch_sp_decode_merge(const float* slots, int P, int B, int Nh, int rv, uint16_t* o, int64_t ldo,
+                                   float* lse, cudaStream_t s);
+
 // ---- Ulysses SP re-layouts (sp_ulysses.cu).  Global position of local row t of rank q:
 // layout 0 contiguous (q n + t), 1 zigzag (chunks q and 2P-1-q of 2P).
 // recv[src][B][n_local][cols] (this rank's heads, from every rank) -> Q' [B*S][hq] and the K'/V'

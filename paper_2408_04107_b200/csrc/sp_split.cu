@@ -56,6 +56,45 @@ __global__ void sp_truncate_kernel(uint16_t* __restrict__ gbuf, int q0, int q1, 
   }
 }
 
+// ---- SP decode (NEXT-2): this rank's attention over ITS keys (its prompt slot + the decode tokens
+// it owns) gives O'_p (bf16, normalised over those keys) and LSE_p; the ranks all-gather
+// {O'_p, LSE_p} and merge them like the key splits of one GPU: O' = sum_p w_p O'_p / sum_p w_p,
+// w_p = exp(LSE_p - max_p LSE_p), LSE = max + log sum_p w_p.
+__global__ void sp_decode_pack_kernel(const uint16_t* __restrict__ o, int64_t ldo, const float* __restrict__ lse, int B,
+                                      int Nh, int rv, float* __restrict__ slot) {
+  const int64_t total = static_cast<int64_t>(B) * Nh * (rv + 1);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % (rv + 1));
+    const int64_t bh = i / (rv + 1);
+    const int b = static_cast<int>(bh / Nh), h = static_cast<int>(bh % Nh);
+    slot[i] = c < rv ? __uint_as_float(static_cast<uint32_t>(o[b * ldo + h * rv + c]) << 16) : lse[bh];
+  }
+}
+
+__global__ void sp_decode_merge_kernel(const float* __restrict__ slots, int P, int B, int Nh, int rv,
+                                       uint16_t* __restrict__ o, int64_t ldo, float* __restrict__ lse) {
+  const int64_t per = static_cast<int64_t>(B) * Nh * (rv + 1);
+  const int64_t total = static_cast<int64_t>(B) * Nh * rv;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % rv);
+    const int64_t bh = i / rv;
+    float M = -INFINITY;
+    for (int q = 0; q < P; ++q) M = fmaxf(M, slots[q * per + bh * (rv + 1) + rv]);
+    float W = 0.f, O = 0.f;
+    for (int q = 0; q < P; ++q) {
+      const float* e = slots + q * per + bh * (rv + 1);
+      const float w = e[rv] == -INFINITY ? 0.f : expf(e[rv] - M);
+      W += w;
+      O = fmaf(w, e[c], O);
+    }
+    const int b = static_cast<int>(bh / Nh), h = static_cast<int>(bh % Nh);
+    o[b * ldo + h * rv + c] = f32_to_bf16_bits(O / W);
+    if (c == 0 && lse) lse[bh] = M + logf(W);
+  }
+}
+
 static int sp_grid(int64_t n) {
   const int64_t g = (n + 255) / 256;
   const int cap = 8 * num_sms();
@@ -82,6 +121,20 @@ cudaError_t launch_sp_truncate(uint16_t* gbuf, int q0, int q1, int P, int layout
                                int w, int r_u, const uint8_t* cls, int64_t ld_cls, cudaStream_t s) {
   const int64_t rows = static_cast<int64_t>(q1 - q0) * 2 * B * Nkv * n_local;
   sp_truncate_kernel<<<sp_grid(rows), 256, 0, s>>>(gbuf, q0, q1, P, layout, S, B, Nkv, n_local, w, r_u, cls, ld_cls);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sp_decode_pack(const uint16_t* o, int64_t ldo, const float* lse, int B, int Nh, int rv, float* slot,
+                                  cudaStream_t s) {
+  sp_decode_pack_kernel<<<sp_grid(static_cast<int64_t>(B) * Nh * (rv + 1)), 256, 0, s>>>(o, ldo, lse, B, Nh, rv, slot);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sp_decode_merge(const float* slots, int P, int B, int Nh, int rv, uint16_t* o, int64_t ldo,
+                                   float* lse, cudaStream_t s) {
+  sp_decode_merge_kernel<<<sp_grid(static_cast<int64_t>(B) * Nh * rv), 256, 0, s>>>(slots, P, B, Nh, rv, o, ldo, lse);
   ++g_launches;
   return cudaGetLastError();
 }

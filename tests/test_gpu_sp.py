@@ -37,7 +37,7 @@ def _plan(shape):
     return Z.plan_uniform(2, r)
 
 
-def _worker(rank, world, port, layout, S, B, out_q, dataflow="allgather", shape="mha"):
+def _worker(rank, world, port, layout, S, B, out_q, dataflow="allgather", shape="mha", T=0):
     import torch.distributed as dist
     import oracle as O  # noqa: F401
     import paper_2408_04107_b200 as zdc
@@ -50,10 +50,10 @@ def _worker(rank, world, port, layout, S, B, out_q, dataflow="allgather", shape=
     dims = Z.Dims(*DIMS[shape][:5])
     plan = _plan(shape)
     _, folded = fold_stack(dims, 1, n_calib=256)
-    ctx = zdc.Context(dims, plan, B, S)
+    ctx = zdc.Context(dims, plan, B, S + (S if T else 0))
     for l, f in enumerate(folded):
         load_lib_fold(ctx, l, f)
-    x = Z.prompt(dims, 1, B, S, seed=41)
+    x = Z.prompt(dims, 1, B, S + T, seed=41)
     pos = zdc.sp_positions(S, world, rank, layout)
     cudart = _cudart()
     cudart.cudaMemcpy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
@@ -87,6 +87,14 @@ def _worker(rank, world, port, layout, S, B, out_q, dataflow="allgather", shape=
     extra = None
     if shape.startswith("split"):
         extra = ctx.classes_export(0, B) + (ctx.scores_export(0, B),)
+    if T:   # NEXT-2: decode over the sequence-sharded cache (partials merged by LSE across ranks)
+        ys = []
+        for t in range(T):
+            xt = to_dev_bf16(np.ascontiguousarray(x[:, S + t]))
+            yt = torch.empty_like(xt)
+            ctx.sp_decode(xt, yt)
+            ys.append(yt.float().cpu().numpy())
+        extra = np.stack(ys, axis=1)
     out_q.put((rank, pos, yl.float().cpu().numpy(), stats, extra))
     dist.destroy_process_group()
 
@@ -195,3 +203,36 @@ def test_sp_prefill_nccl_world1():
         outs.append(from_dev(y))
         ctx.close()
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
+@pytest.mark.parametrize("world,layout", [(2, 1), (4, 0)])
+def test_sp_decode_over_sharded_cache(world, layout):
+    """NEXT-2: after an all-gather SP prefill, zdc_sp_decode appends decode token j on rank j mod P
+    only and merges the ranks' partial attention by LSE; every rank's y equals the oracle's rows
+    (P7) within the north-star tolerance, and all ranks agree."""
+    import multiprocessing as pymp
+    import oracle as O
+    import zdc_synth as Z
+    from zdc_testlib import fold_stack, normwise
+    B, T = 2, 7
+    S = 256 * world * (2 if layout else 1)
+    ctx_mp = pymp.get_context("spawn")
+    q = ctx_mp.Queue()
+    port = 29700 + world * 10 + layout + os.getpid() % 500
+    procs = [ctx_mp.Process(target=_worker, args=(r, world, port, layout, S, B, q, "allgather", "mha", T))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    dims = Z.Dims(*DIMS["mha"][:5])
+    plan = _plan("mha")
+    _, folded = fold_stack(dims, 1, n_calib=256)
+    x = Z.prompt(dims, 1, B, S + T, seed=41)
+    want = O.OracleModel(dims, plan, folded, faithful=True).prefill(x)[:, S:]
+    ys = [r[4] for r in res]
+    for yd in ys:
+        assert normwise(yd, want) <= 2e-2
+        assert np.array_equal(yd, ys[0])     # every rank computes the same merged rows
