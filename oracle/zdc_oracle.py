@@ -19,6 +19,7 @@ Contents
   OracleModel       prefill / decode over a compressed KV cache, with
                     zero-filled unimportant rows and layer groups     P:774-776 (DEL)
   kmeans            K-means consolidation of calibration vectors      P:1157-1167 (§5.1 offline computation)
+  e4m3 / quantize_rows  FP8 (E4M3) compressed KV cache, GEAR-ZDC      P:1642 (DEL), P:1606 (§6 compared methods)
   layer_groups      layers sharing the representative's classes       P:1455-1456 (repetition ratio > 95%)
 
 Readings of silent / ambiguous points are DESIGN.md §3 (c1..c19), cited inline.
@@ -50,6 +51,52 @@ def bf16(a: np.ndarray) -> np.ndarray:
     lsb = (bits >> 16) & 1
     bits = (bits + 0x7FFF + lsb) & 0xFFFF0000
     return bits.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+# --------------------------------------------------------------------------------------
+# FP8 E4M3 (the oracle's own; OCP 8-bit "e4m3fn": bias 7, 3 mantissa bits, no infinities,
+# largest finite 448, smallest subnormal 2^-9) for the quantized compressed cache of NEXT-4
+# --------------------------------------------------------------------------------------
+def _e4m3_table():
+    vals, codes = [], []
+    for code in range(0x7F):          # 0x7F is NaN; non-negative codes only
+        e, m = code >> 3, code & 7
+        v = (m / 8.0) * 2.0 ** -6 if e == 0 else (1.0 + m / 8.0) * 2.0 ** (e - 7)
+        vals.append(v)
+        codes.append(code)
+    return np.array(vals), np.array(codes)
+
+
+_E4M3_VALS, _E4M3_CODES = _e4m3_table()
+
+
+def e4m3(a) -> np.ndarray:
+    """Round to the nearest E4M3 value, ties to the even code (round-to-nearest-even), magnitudes
+    above 448 saturate to 448 (reading c23: the GPU converts with RNE + satfinite).  Returns the
+    E4M3 value as fp64 (the sign is kept, so -0 stays -0)."""
+    a = np.asarray(a, dtype=np.float64)
+    mag = np.minimum(np.abs(a), 448.0)
+    idx = np.searchsorted(_E4M3_VALS, mag)              # first table value >= mag
+    hi = np.minimum(idx, len(_E4M3_VALS) - 1)
+    lo = np.maximum(idx - 1, 0)
+    dlo = mag - _E4M3_VALS[lo]
+    dhi = _E4M3_VALS[hi] - mag
+    pick_hi = (dhi < dlo) | ((dhi == dlo) & (_E4M3_CODES[hi] % 2 == 0))
+    out = np.where(pick_hi, _E4M3_VALS[hi], _E4M3_VALS[lo])
+    return np.copysign(out, a)
+
+
+def quantize_rows(x) -> np.ndarray:
+    """GEAR-ZDC's quantized compressed cache (P:1642 DEL: "quantizes each matrix element of the
+    compressed data after ZDC compression and dequantizes them before ZDC decompression"), with the
+    reading c23 scheme: per cached row (token, KV head) of r values, in FP32 as the GPU computes it,
+    scale = max|x| / 448 (1 for an all-zero row), code = E4M3(x / scale), stored value = code * scale.
+    x [..., r] -> the dequantized values (fp64 holding FP32 results)."""
+    x32 = np.asarray(x, dtype=np.float64).astype(np.float32)
+    amax = np.max(np.abs(x32), axis=-1, keepdims=True)
+    scale = np.where(amax > 0, amax / np.float32(448.0), np.float32(1.0)).astype(np.float32)
+    codes = e4m3((x32 / scale).astype(np.float64))
+    return (codes.astype(np.float32) * scale).astype(np.float64)
 
 
 # --------------------------------------------------------------------------------------
@@ -306,6 +353,10 @@ class OracleModel:
     def _rnd(self, a):
         return bf16(a) if self.faithful else a
 
+    def _store(self, a):
+        """What the cache keeps of K'/V' rows: FP8 codes x per-row scale when plan.kv_fp8 (NEXT-4)."""
+        return quantize_rows(a) if getattr(self.plan, "kv_fp8", 0) else a
+
     def _split(self, l):
         return self.plan.g_bp[l] < 10000
 
@@ -391,7 +442,7 @@ class OracleModel:
                 cls[b], tau[b], _ = select_important(sc[b], plan.g_bp[l])
             self.classes[l], self.tau[l], self.scores[l] = cls, tau, sc
             K, V = self._truncate_rows(l, K, V, ~cls)
-        self.K[l], self.V[l] = K, V
+        self.K[l], self.V[l] = self._store(K), self._store(V)   # the prompt attended at full precision
         self.length[l] = S
         return self._output(l, O)
 
@@ -438,8 +489,8 @@ class OracleModel:
             if self.classes[rep].shape[1] <= t:
                 raise ValueError("layer %d: representative %d has not classified position %d" % (l, rep, t))
             K, V = self._truncate_rows(l, K, V, ~self.classes[rep][:, t:t + 1])
-        self.K[l] = np.concatenate([self.K[l], K], axis=2)
-        self.V[l] = np.concatenate([self.V[l], V], axis=2)
+        self.K[l] = np.concatenate([self.K[l], self._store(K)], axis=2)   # quantized on append (NEXT-4)
+        self.V[l] = np.concatenate([self.V[l], self._store(V)], axis=2)
         self.length[l] = t + 1
         O = np.zeros((B, dims.n_heads, 1, V.shape[3]))
         lse = np.zeros((B, dims.n_heads, 1))

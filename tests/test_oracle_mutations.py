@@ -58,6 +58,13 @@ MUTANTS = [
     ("layer groups compare to the previous layer", "same = int(np.sum(classes[l] == classes[cur]))",
      "same = int(np.sum(classes[l] == classes[l - 1]))"),
     ("layer groups >= threshold", "if same * 10000 > threshold_bp * total:", "if same * 10000 >= threshold_bp * total:"),
+    ("e4m3 ties away from zero", "pick_hi = (dhi < dlo) | ((dhi == dlo) & (_E4M3_CODES[hi] % 2 == 0))",
+     "pick_hi = (dhi <= dlo)"),
+    ("e4m3 subnormals at 2^-7", "v = (m / 8.0) * 2.0 ** -6 if e == 0", "v = (m / 8.0) * 2.0 ** -7 if e == 0"),
+    ("fp8 scale over 240", "scale = np.where(amax > 0, amax / np.float32(448.0), np.float32(1.0)).astype(np.float32)",
+     "scale = np.where(amax > 0, amax / np.float32(240.0), np.float32(1.0)).astype(np.float32)"),
+    ("fp8 cache not quantized on append", "self.K[l] = np.concatenate([self.K[l], self._store(K)], axis=2)",
+     "self.K[l] = np.concatenate([self.K[l], K], axis=2)"),
     ("SP bytes without (P-1)", "return (P - 1) * (S // P) * B * n_kv * (r_k + r_v) * elem_bytes",
      "return P * (S // P) * B * n_kv * (r_k + r_v) * elem_bytes"),
 ]

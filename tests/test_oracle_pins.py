@@ -630,3 +630,52 @@ def test_layer_groups_rule():
     assert O.layer_groups(cls, 9500) == [0, 0, 0, 3, 3]
     assert O.layer_groups(cls, 10000) == [0, 1, 2, 3, 4]   # strict: no agreement exceeds 100 %
     assert O.layer_groups(cls, 0) == [0, 0, 0, 0, 0]
+
+
+# ---------------------------------------------------------------- NEXT-4: FP8 compressed cache
+def test_e4m3_golden():
+    spec = json.load(open(os.path.join(GOLDEN, "e4m3_examples.json")))
+    for c in spec["cases"]:
+        got = float(O.e4m3(np.array([c["x"]]))[0])
+        assert got == c["value"], (c, got)
+        assert float(O.e4m3(np.array([-c["x"]]))[0]) == -c["value"]
+
+
+def test_quantize_rows_bounds():
+    """Reading c23: per-row absmax scale.  The row maximum is kept to FP32 rounding, rows of E4M3
+    multiples of a power of two round-trip exactly, an all-zero row stays zero, and every element
+    is within half an E4M3 ulp of its row-scaled value (2^-4 relative in the normal range,
+    2^-10 x scale in the subnormal range)."""
+    rng = np.random.default_rng(21)
+    x = rng.standard_normal((64, 48)) * np.exp(rng.uniform(-8, 8, size=(64, 1)))
+    q = O.quantize_rows(x)
+    x32 = x.astype(np.float32).astype(np.float64)
+    amax = np.max(np.abs(x32), axis=1, keepdims=True)
+    scale = amax / 448.0
+    assert np.allclose(np.max(np.abs(q), axis=1, keepdims=True), amax, rtol=1e-6, atol=0)
+    normal = np.abs(x32) >= scale * 2.0 ** -6
+    err = np.abs(q - x32)
+    assert np.all(err[normal] <= np.abs(x32)[normal] * 2.0 ** -4 * (1 + 1e-6))
+    assert np.all(err[~normal] <= (scale * 2.0 ** -10 * (1 + 1e-6) + 0 * err)[~normal])
+    assert np.array_equal(O.quantize_rows(np.zeros((3, 16))), np.zeros((3, 16)))
+    exact = np.array([[448.0, -1.0, 0.5, 18.0, 0.001953125, 0.0]]) * 2.0 ** -5
+    assert np.array_equal(O.quantize_rows(exact), exact)
+
+
+def test_fp8_cache_model_semantics():
+    """NEXT-4: with kv_fp8 the prompt still attends at full precision (prefill rows unchanged);
+    the cache keeps quantize_rows of K'/V'; decode attends the quantized cache (itself included)."""
+    dims = Dims(1, 32, 4, 2, 16)
+    _, folded = _fold_all(dims, 1, n_calib=128)
+    plan = plan_uniform(1, 12)
+    plan8 = plan_uniform(1, 12)
+    plan8.kv_fp8 = 1
+    x = Z.prompt(dims, 1, 2, 20)
+    m, m8 = O.OracleModel(dims, plan, folded), O.OracleModel(dims, plan8, folded)
+    y, y8 = m.prefill(x[:, :16]), m8.prefill(x[:, :16])
+    assert np.array_equal(y, y8)
+    assert np.array_equal(m8.K[0], O.quantize_rows(m.K[0])) and np.array_equal(m8.V[0], O.quantize_rows(m.V[0]))
+    for t in range(16, 20):
+        yd, yd8 = m.decode(x[:, t]), m8.decode(x[:, t])
+        assert 0 < _rel(yd8, yd) < 0.1
+    assert np.array_equal(m8.K[0][:, :, 16:], O.quantize_rows(m.K[0][:, :, 16:]))

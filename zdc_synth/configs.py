@@ -33,6 +33,7 @@ class Plan:
     g_bp: List[int]          # important fraction in basis points; 10000 = no token split
     group_rep: List[int]     # representative layer of each layer's group
     importance_mode: int = 0  # 0 = raw sum_h sum_k exp(s); 1 = per-key mean
+    kv_fp8: int = 0           # 1 = FP8 E4M3 compressed cache with a per-row scale (NEXT-4, GEAR-ZDC)
 
     @property
     def n_layers(self) -> int:
