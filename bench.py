@@ -70,6 +70,7 @@ def parse():
     p.add_argument("--no-sp", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-fold", action="store_true", help="skip the NEXT-3 GPU fold timing")
+    p.add_argument("--no-fp8", action="store_true", help="skip the NEXT-4 FP8 cache decode timing")
     p.add_argument("--no-uncompressed", action="store_true",
                    help="skip the r = d_h (R = I) baseline and the torch SDPA / matmul comparison")
     p.add_argument("--no-e2e", action="store_true")
@@ -686,6 +687,74 @@ def uncompressed_bench(args, zdc, torch, dev, stream, pre_ms_r, dec_ms_r, dec_by
     }
 
 
+# ------------------------------------------------------------------------------------ NEXT-4 FP8 cache
+def _decode_step_us(zdc, torch, dev, stream, dims, plan, B, S, T=32):
+    """Per-layer decode layer-step time (us) of `dims.n_layers` layers called one by one (same x),
+    each step one CUDA graph, after a prefill of S tokens; timing-only weights."""
+    L, d, nh, nkv, dh = dims.n_layers, dims.d_model, dims.n_heads, dims.n_kv_heads, dims.d_head
+    ctx = zdc.Context(dims, plan, B, S + T + 4)
+    g = torch.Generator(device=dev).manual_seed(77)
+    for l in range(L):
+        ctx.load_folded_device(l, *_timing_weights(torch, dev, g, d, nh, nkv, dh))
+    x = torch.randn(B, S, d, device=dev, generator=g).to(torch.bfloat16)
+    y = torch.empty_like(x)
+    for l in range(L):
+        ctx.prefill(x, y, l, l + 1)
+    xb = torch.randn(B, d, device=dev, generator=g).to(torch.bfloat16)
+    yb = torch.empty_like(xb)
+    for l in range(L):
+        ctx.decode(xb, yb, l, l + 1)
+    gs = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gs, stream=stream):
+        for l in range(L):
+            ctx.decode(xb, yb, l, l + 1)
+    gs.replay()
+    torch.cuda.synchronize()
+    time.sleep(0.2)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(T - 2):
+        gs.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ctx.close()
+    return e0.elapsed_time(e1) * 1e3 / ((T - 2) * L)
+
+
+def fp8_bench(zdc, torch, dev, stream):
+    """NEXT-4 (GEAR-ZDC, P:1642 DEL): decode layer-step with the FP8 E4M3 compressed cache (r codes +
+    f32 scale + 12 pad bytes per row) against the bf16 cache, at the c2 shape (B = 1, ctx 2048+) and
+    at a c3-like uniform shape (B = 32, 40 heads, r = 96, ctx 1024+).  The FP8 cache runs the
+    separate-kernel decode path (split-K FP8 attention); bf16 is shown on that path and, at B = 1,
+    on the fused layer-step kernel the headline uses."""
+    import zdc_synth as Z
+    out = {}
+    shapes = {"c2_B1": (Z.Dims(4, 4096, 32, 32, 128), 64, 1, 2048), "c3_uniform_B32": (Z.Dims(4, 5120, 40, 40, 128), 96, 32, 1024)}
+    peaks = load_peaks()
+    for name, (dims, r, B, S) in shapes.items():
+        rec = {"rank": r, "batch": B, "prompt": S}
+        wbytes = sum(decode_layer_bytes(dims.d_model, dims.n_heads, dims.n_kv_heads, r, B, 0).values())
+        ctx_avg = S + 16
+        for label, fp8, mode in (("bf16_fused", 0, "auto"), ("bf16_separate", 0, "separate"), ("fp8", 1, "separate")):
+            if label == "bf16_fused" and B > 8:
+                continue
+            plan = Z.plan_uniform(dims.n_layers, r)
+            plan.kv_fp8 = fp8
+            old = zdc.decode_mode(mode)
+            try:
+                us = _decode_step_us(zdc, torch, dev, stream, dims, plan, B, S)
+            finally:
+                zdc.decode_mode(old)
+            row = (r + 16) if fp8 else 2 * r
+            kv = B * dims.n_kv_heads * ctx_avg * 2 * row
+            rec[label] = {"us_per_layer_step": round(us, 2), "kv_bytes": kv, "bytes_per_layer_step": wbytes + kv,
+                          "achieved_gbs": round((wbytes + kv) / (us / 1e6) / 1e9, 1),
+                          "frac": round((wbytes + kv) / (us / 1e6) / 1e9 / peaks["hbm"], 4)}
+        out[name] = rec
+    torch.cuda.empty_cache()
+    return out
+
+
 # ------------------------------------------------------------------------------------ NEXT-3 fold
 def fold_bench(zdc, torch, dev, stream, n_calib=32768, k=2048, iters=5):
     """NEXT-3: the offline fold of one c2-shaped layer on the GPU in fp64
@@ -978,6 +1047,15 @@ def run_zdc(args):
         except Exception as e:  # reported, never hides the main line
             fold = {"error": "%s: %s" % (type(e).__name__, e)}
 
+    # ---- NEXT-4: FP8 compressed cache decode (N = 1)
+    fp8 = None
+    if world == 1 and not args.no_fp8:
+        log("FP8 cache decode (NEXT-4)")
+        try:
+            fp8 = fp8_bench(zdc, torch, dev, stream)
+        except Exception as e:  # reported, never hides the main line
+            fp8 = {"error": "%s: %s" % (type(e).__name__, e)}
+
     # ---- CPU baseline (oracle as it stands), rank 0 at N=1 only
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -1011,7 +1089,7 @@ def run_zdc(args):
                 "note": "whole decode layer-step inside the graph-replayed step: algorithmic bytes (packed "
                         "weights + K'/V' at the average context + x/y) / measured time per layer-step"},
             "clocks": clocks, "gpu_launches": kernels_per_step * args.steps,
-            "e2e": e2e, "cpu_baseline": cpu, "sp": sp, "other_configs": other, "baseline_uncompressed": unc, "offline_fold": fold,
+            "e2e": e2e, "cpu_baseline": cpu, "sp": sp, "other_configs": other, "baseline_uncompressed": unc, "offline_fold": fold, "kv_fp8": fp8,
         }
         print(json.dumps(out), flush=True)
     ctx.close()

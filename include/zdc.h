@@ -68,6 +68,14 @@ typedef struct {
   const int32_t *g_bp;
   const int32_t *group_rep;
   int32_t importance_mode;
+  /* NEXT-4 (GEAR-ZDC, P:1642 DEL: "quantizes each matrix element of the compressed data after ZDC
+   * compression and dequantizes them before ZDC decompression"): 1 = the compressed K'/V' cache is
+   * stored as FP8 E4M3 codes with one f32 scale per row (token, KV head), reading c23 (scale =
+   * max|x| / 448, RNE + satfinite); the prompt attends at full precision, decode attends the
+   * quantized cache (its own new row included).  Uniform-rank plans with padded ranks in
+   * {32, 64, 96, 128} only (else ZDC_ERR_UNSUPPORTED).  Row layout: r codes, the f32 scale,
+   * 12 pad bytes (r + 16 bytes vs 2 r for bf16).  0 = bf16 cache. */
+  int32_t kv_fp8;
 } zdc_plan;
 
 /* ------------------------------------------------------------------------------------

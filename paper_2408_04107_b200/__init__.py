@@ -54,7 +54,7 @@ class Plan(ctypes.Structure):
     _fields_ = [("r_qk_imp", ctypes.POINTER(ctypes.c_int32)), ("r_qk_unimp", ctypes.POINTER(ctypes.c_int32)),
                 ("r_vl_imp", ctypes.POINTER(ctypes.c_int32)), ("r_vl_unimp", ctypes.POINTER(ctypes.c_int32)),
                 ("g_bp", ctypes.POINTER(ctypes.c_int32)), ("group_rep", ctypes.POINTER(ctypes.c_int32)),
-                ("importance_mode", ctypes.c_int32)]
+                ("importance_mode", ctypes.c_int32), ("kv_fp8", ctypes.c_int32)]
 
 
 class SpStats(ctypes.Structure):
@@ -335,7 +335,8 @@ class Context:
         self.dims, self.plan = dims, plan
         self._keep = [_i32arr(plan.r_qk_imp), _i32arr(plan.r_qk_unimp), _i32arr(plan.r_vl_imp),
                       _i32arr(plan.r_vl_unimp), _i32arr(plan.g_bp), _i32arr(plan.group_rep)]
-        P = Plan(*[ctypes.cast(a, ctypes.POINTER(ctypes.c_int32)) for a in self._keep], int(plan.importance_mode))
+        P = Plan(*[ctypes.cast(a, ctypes.POINTER(ctypes.c_int32)) for a in self._keep], int(plan.importance_mode),
+                 int(getattr(plan, "kv_fp8", 0)))
         D = make_dims(dims)
         h = ctypes.c_void_p()
         _check(lib().zdc_ctx_create(ctypes.byref(D), ctypes.byref(P), max_batch, max_seq, ctypes.byref(h)),

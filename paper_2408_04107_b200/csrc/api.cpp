@@ -111,6 +111,8 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
     return fail(ZDC_ERR_INVALID_ARG, "zdc_ctx_create: null plan array");
   if (plan->importance_mode != 0 && plan->importance_mode != 1)
     return fail(ZDC_ERR_INVALID_ARG, "zdc_ctx_create: importance_mode %d", plan->importance_mode);
+  if (plan->kv_fp8 != 0 && plan->kv_fp8 != 1)
+    return fail(ZDC_ERR_INVALID_ARG, "zdc_ctx_create: kv_fp8 %d", plan->kv_fp8);
 
   zdc_ctx* c = new zdc_ctx();
   c->dims = d;
@@ -118,6 +120,7 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
   c->max_batch = max_batch;
   c->max_seq = max_seq;
   c->importance_mode = plan->importance_mode;
+  c->kv_fp8 = plan->kv_fp8;
   c->layers.resize(d.n_layers);
   c->len.assign(d.n_layers, 0);
   c->sp_layer.assign(d.n_layers, 0);
@@ -180,10 +183,21 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
       }
     }
     const int64_t kv_rows = static_cast<int64_t>(max_batch) * d.n_kv_heads * max_seq;
+    if (c->kv_fp8) {
+      const bool w_ok = L.rk_p == 32 || L.rk_p == 64 || L.rk_p == 96 || L.rk_p == 128;
+      if (L.split || !w_ok || L.rk_p != L.rv_p) {
+        delete c;
+        return fail(ZDC_ERR_UNSUPPORTED, "zdc_ctx_create: kv_fp8 needs uniform-rank layers with padded ranks in "
+                    "{32, 64, 96, 128} (layer %d: split %d, rank %d)", l, L.split ? 1 : 0, L.rk_p);
+      }
+    }
+    // bf16 rows of r, or FP8 rows of r codes + f32 scale + 12 pad bytes (NEXT-4)
+    const int64_t krow = c->kv_fp8 ? L.rk_p + 16 : L.rk_p * 2, vrow = c->kv_fp8 ? L.rv_p + 16 : L.rv_p * 2;
     L.k_off = coff;
-    coff = align_up(coff + kv_rows * L.rk_p * 2, 256);
+    coff = align_up(coff + kv_rows * krow, 256);
     L.v_off = coff;
-    coff = align_up(coff + kv_rows * L.rv_p * 2, 256);
+    coff = align_up(coff + kv_rows * vrow, 256);
+    if (c->kv_fp8 && L.rk_p > max_split_w) max_split_w = L.rk_p;
     if (L.split) {
       L.ku_off = coff;
       coff = align_up(coff + kv_rows * L.rku_p * 2, 256);
@@ -243,7 +257,7 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
   s = align_up(s + rows * max_nqkv * 2, 256);
   c->s_ybuf = s;  // cluster decode: y accumulator [8][d] f32 then 16 arrival counters, zero between launches
   s = align_up(s + static_cast<int64_t>(8) * d.d_model * 4 + 16 * 4, 256);
-  if (any_split) {  // staged K'/V' of a split layer before packing, compaction indices, new-row staging
+  if (any_split || c->kv_fp8) {  // staged K'/V' (split: before packing; FP8: before quantizing), indices, new rows
     const int64_t kv_rows = static_cast<int64_t>(max_batch) * d.n_kv_heads * max_seq;
     c->s_ks = s;
     s = align_up(s + kv_rows * max_split_w * 2, 256);
@@ -449,7 +463,7 @@ zdc_status zdc_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, ui
     e1.qkv = qkv_dest(c, L, S, 0, nullptr);
     uint16_t* ks = reinterpret_cast<uint16_t*>(c->scratch + c->s_ks);
     uint16_t* vs = reinterpret_cast<uint16_t*>(c->scratch + c->s_vs);
-    if (L.split) {
+    if (L.split || c->kv_fp8) {  // staged: class-aware packing (split) / quantization (FP8, NEXT-4)
       e1.qkv.k = ks;
       e1.qkv.v = vs;
     }
@@ -469,8 +483,8 @@ zdc_status zdc_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, ui
     PrefillAttnArgs a;
     a.q = reinterpret_cast<const uint16_t*>(c->scratch + c->s_q);
     a.ldq = L.nq;
-    a.k = L.split ? ks : reinterpret_cast<const uint16_t*>(c->cache + L.k_off);
-    a.v = L.split ? vs : reinterpret_cast<const uint16_t*>(c->cache + L.v_off);
+    a.k = L.split || c->kv_fp8 ? ks : reinterpret_cast<const uint16_t*>(c->cache + L.k_off);
+    a.v = L.split || c->kv_fp8 ? vs : reinterpret_cast<const uint16_t*>(c->cache + L.v_off);
     a.S_cap = c->max_seq;
     a.o = reinterpret_cast<uint16_t*>(c->scratch + c->s_o);
     a.ldo = L.ko_p;
@@ -486,6 +500,11 @@ zdc_status zdc_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, ui
     a.q_row0 = 0;
     a.n_q = S;
     ZDC_CUDA_TRY(launch_prefill_attention(a, s));
+    if (c->kv_fp8) {  // NEXT-4: the prompt attended at full precision; the cache keeps FP8 rows
+      g_prof_class = kProfOther;
+      ZDC_CUDA_TRY(launch_quantize_kv(ks, c->max_seq, c->cache + L.k_off, c->max_seq, B * Nkv, 0, S, L.rk_p, nullptr, s));
+      ZDC_CUDA_TRY(launch_quantize_kv(vs, c->max_seq, c->cache + L.v_off, c->max_seq, B * Nkv, 0, S, L.rv_p, nullptr, s));
+    }
     if (L.split) {
       g_prof_class = kProfOther;
       if (is_rep) {
@@ -552,7 +571,7 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
     e1.qkv.pos_cap = c->max_seq;
     uint16_t* knew = reinterpret_cast<uint16_t*>(c->scratch + c->s_new);
     uint16_t* vnew = knew + static_cast<int64_t>(B) * Nkv * L.rk_p;
-    if (L.split) {  // stage the new row; the class-aware append places it below
+    if (L.split || c->kv_fp8) {  // stage the new row; the class-aware / quantizing append places it below
       e1.qkv.k = knew;
       e1.qkv.v = vnew;
       e1.qkv.pos_ptr = nullptr;
@@ -565,7 +584,7 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
     const uint16_t* wqkv = reinterpret_cast<const uint16_t*>(c->w + L.w_qkv);
     const uint16_t* wo = reinterpret_cast<const uint16_t*>(c->w + L.w_o);
     const int mode = g_decode_mode;
-    const bool fused_on = mode != 3 && knob("ZDC_DEC_FUSED", 1) != 0;
+    const bool fused_on = mode != 3 && knob("ZDC_DEC_FUSED", 1) != 0 && !c->kv_fp8;
     if (fused_on && mode != 1 && !L.split && L.w_od >= 0 && L.w_qd >= 0) {
       // the cluster layer-step: one cluster per KV group, no grid barrier (decode_cluster.cuh)
       const int C = decode_cluster_size(B, L.rk_p, c->G, Nkv, d);
@@ -662,6 +681,11 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
     }
     const LayerInfo& R = c->layers[L.rep];
     const bool is_rep = L.rep == l;
+    if (c->kv_fp8) {  // NEXT-4: quantize the new row into the FP8 cache at position *len_dev
+      g_prof_class = kProfOther;
+      ZDC_CUDA_TRY(launch_quantize_kv(knew, 1, c->cache + L.k_off, c->max_seq, B * Nkv, 0, 1, L.rk_p, len_dev, s));
+      ZDC_CUDA_TRY(launch_quantize_kv(vnew, 1, c->cache + L.v_off, c->max_seq, B * Nkv, 0, 1, L.rv_p, len_dev, s));
+    }
     if (L.split) {
       g_prof_class = kProfOther;
       ZDC_CUDA_TRY(launch_append(knew, vnew, L.rk_p, Nkv, reinterpret_cast<uint16_t*>(c->cache + L.k_off),
@@ -726,7 +750,13 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
     }
     static const bool attn_tc_on = knob("ZDC_DEC_ATTN_TC", 1) != 0;
     cudaError_t ea = cudaErrorNotSupported;
-    if (attn_tc_on && !L.split && decode_attention_tc_supported(L.rk_p, L.rv_p, c->G)) {
+    if (c->kv_fp8) {
+      a.kv_fp8 = 1;
+      a.splits = decode2_splits(B, Nkv, c->max_seq, L.rk_p, c->G);
+      ea = launch_decode2_f8(a, s);
+      if (ea != cudaSuccess) return fail(ZDC_ERR_CUDA, "decode attention (FP8 cache) layer %d: %s", l, cudaGetErrorString(ea));
+    }
+    if (attn_tc_on && !L.split && !c->kv_fp8 && decode_attention_tc_supported(L.rk_p, L.rv_p, c->G)) {
       // grouped-query heads: the tensor-core kernel (decode_attn_tc.cu)
       DecodeAttnArgs at = a;
       at.splits = decode_tc_splits(B, Nkv, c->max_seq);
@@ -918,6 +948,34 @@ zdc_status zdc_cache_export(const zdc_ctx* c, int32_t layer, float* k, float* v,
     h.resize(n);
     return cudaMemcpy(h.data(), c->cache + off, n * 4, cudaMemcpyDeviceToHost);
   };
+  if (c->kv_fp8) {  // NEXT-4: rows of r E4M3 codes + f32 scale + 12 pad bytes -> code * scale
+    const int64_t rb = L.rk_p + 16;
+    std::vector<uint8_t> k8(rows * rb), v8(rows * rb);
+    ZDC_CUDA_TRY(cudaMemcpy(k8.data(), c->cache + L.k_off, k8.size(), cudaMemcpyDeviceToHost));
+    ZDC_CUDA_TRY(cudaMemcpy(v8.data(), c->cache + L.v_off, v8.size(), cudaMemcpyDeviceToHost));
+    auto e4m3 = [](uint8_t code) {
+      const int e = (code >> 3) & 15, m = code & 7;
+      const float mag = e == 0 ? std::ldexp(m / 8.0f, -6) : std::ldexp(1.0f + m / 8.0f, e - 7);
+      return (code & 0x80) ? -mag : mag;
+    };
+    for (int b = 0; b < B; ++b)
+      for (int t = 0; t < len; ++t)
+        for (int g = 0; g < Nkv; ++g) {
+          const int64_t row = (static_cast<int64_t>(b) * Nkv + g) * S_cap + t;
+          const int64_t o = (static_cast<int64_t>(b) * len + t) * Nkv + g;
+          float ks, vs;
+          std::memcpy(&ks, &k8[row * rb + L.rk_p], 4);
+          std::memcpy(&vs, &v8[row * rb + L.rk_p], 4);
+          for (int e2 = 0; e2 < L.rk; ++e2) {
+            if (k) k[o * L.rk + e2] = e4m3(k8[row * rb + e2]) * ks;
+            if (v) v[o * L.rv + e2] = e4m3(v8[row * rb + e2]) * vs;
+          }
+        }
+    if (is_imp) std::memset(is_imp, 1, static_cast<size_t>(B) * len);
+    if (tau)
+      for (int b = 0; b < B; ++b) tau[b] = INFINITY;
+    return ZDC_OK;
+  }
   std::vector<uint16_t> ki, vi, ku, vu;
   std::vector<int> posi, posu, ni, nu;
   ZDC_CUDA_TRY(fetch16(L.k_off, rows * L.rk_p, ki));

@@ -202,6 +202,7 @@ zdc_status zdc_sp_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x,
   if (!c || !x || !y) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_prefill: null argument");
   if (x == y) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_prefill: x and y alias");
   if (!c->w) return fail(ZDC_ERR_STATE, "zdc_sp_prefill: ctx not bound");
+  if (c->kv_fp8) return fail(ZDC_ERR_UNSUPPORTED, "zdc_sp_prefill: the FP8 cache (kv_fp8) is single-GPU");
   if (!c->comm) return fail(ZDC_ERR_STATE, "zdc_sp_prefill: zdc_comm_init not called");
   if (l0 < 0 || l1 > c->dims.n_layers || l0 >= l1)
     return fail(ZDC_ERR_SHAPE, "zdc_sp_prefill: layer range [%d, %d)", l0, l1);
@@ -406,6 +407,7 @@ zdc_status zdc_sp_prefill_ulysses(zdc_ctx* c, int32_t l0, int32_t l1, const uint
   if (!c || !x || !y) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_prefill_ulysses: null argument");
   if (x == y) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_prefill_ulysses: x and y alias");
   if (!c->w) return fail(ZDC_ERR_STATE, "zdc_sp_prefill_ulysses: ctx not bound");
+  if (c->kv_fp8) return fail(ZDC_ERR_UNSUPPORTED, "zdc_sp_prefill_ulysses: the FP8 cache (kv_fp8) is single-GPU");
   if (!c->comm) return fail(ZDC_ERR_STATE, "zdc_sp_prefill_ulysses: zdc_comm_init / an all-to-all hook not set");
   if (l0 < 0 || l1 > c->dims.n_layers || l0 >= l1)
     return fail(ZDC_ERR_SHAPE, "zdc_sp_prefill_ulysses: layer range [%d, %d)", l0, l1);

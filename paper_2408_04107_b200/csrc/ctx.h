@@ -39,6 +39,7 @@ struct zdc_ctx {
   int G = 1;
   int max_batch = 0, max_seq = 0;
   int importance_mode = 0;
+  int kv_fp8 = 0;  // FP8 E4M3 compressed cache (NEXT-4): rows of r codes + f32 scale + 12 pad bytes
   std::vector<zdc::LayerInfo> layers;
   int64_t weight_bytes = 0, cache_bytes = 0, scratch_bytes = 0;
   int64_t s_q = 0, s_o = 0, s_lse = 0, s_part = 0;  // scratch offsets

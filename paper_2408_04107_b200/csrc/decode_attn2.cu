@@ -11,6 +11,8 @@
 //   * the 8 warp partials merge in shared memory, the CTA writes one partial, and the last CTA of
 //     the (sequence, KV head) LSE-merges the splits (O' bf16 + LSE f32).
 // Same arguments and partial layout as v1 (decode.cu), so both pools of the token split work.
+#include <cuda_fp8.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -283,6 +285,270 @@ __global__ void __launch_bounds__(kNW * 32)
     if (c == 0 && a.lse) a.lse[b * a.Nh + g * G + gi] = (M + log2f(L)) / kLog2eD;
   }
   if (threadIdx.x == 0) a.counters[b * a.Nkv + g] = 0;
+}
+
+// ---- NEXT-4: the same kernel over an FP8 E4M3 cache (GEAR-ZDC, reading c23).  A cached row is
+// r codes, its f32 scale and 12 pad bytes (RB = r + 16 bytes, 16-byte aligned for the bulk
+// copies); scores use the codes, scaled once per row: s = (q . code_k) * scale_k; PV folds the
+// row's V scale into the rounded probability: o += (bf16(p) * scale_v) * code_v.
+// Static shared memory of one FP8 CTA.
+template <int G, int RMAX>
+struct DA2Smem {
+  __align__(16) float qsf[G][RMAX];
+  float wm[kNW][G], wl[kNW][G];
+  float wo[kNW][G][RMAX];
+  uint64_t bars[kNW][4];  // one mbarrier per ring stage of each warp (NST <= 4)
+  int s_last;
+};
+
+template <int RK>
+struct DA2F8 {
+  static constexpr int TR = 32, RB = RK + 16;
+  static constexpr int CPL = RK / 32;
+  static constexpr uint32_t KT = TR * RB, VT = TR * RB, STAGE = KT + VT;
+  static constexpr int NST = 2;  // 4 stages (and one wave of this kernel's own occupancy) measured slower
+  static constexpr uint32_t WARP_BYTES = NST * STAGE;
+};
+
+__device__ __forceinline__ float e4m3_to_f32(uint32_t code) {
+  const __half_raw h = __nv_cvt_fp8_to_halfraw(static_cast<__nv_fp8_storage_t>(code), __NV_E4M3);
+  return __half2float(__half(h));
+}
+// two E4M3 codes (low 16 bits of w) -> two floats (one packed conversion)
+__device__ __forceinline__ float2 e4m3x2_to_f32x2(uint32_t w) {
+  const __half2_raw h = __nv_cvt_fp8x2_to_halfraw2(static_cast<__nv_fp8x2_storage_t>(w & 0xFFFFu), __NV_E4M3);
+  return __half22float2(__half2(h));
+}
+
+template <int RK, int G>
+__global__ void __launch_bounds__(kNW * 32)
+    decode_attn2_f8_kernel(const DecodeAttnArgs a, const uint8_t* __restrict__ kp, const uint8_t* __restrict__ vp) {
+  using C = DA2F8<RK>;
+  extern __shared__ __align__(128) uint8_t dsm[];
+  __shared__ DA2Smem<G, RK> sh;
+  const int split = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row0 = (static_cast<int64_t>(b) * a.Nkv + g) * a.S_cap;
+  const float scl = a.scale * kLog2eD;
+  uint8_t* ring = dsm + warp * C::WARP_BYTES;
+  uint64_t* wbar = sh.bars[warp];
+  static_assert(C::NST <= 4, "one mbarrier per stage");
+  if (lane == 0) {
+    for (int i = 0; i < C::NST; ++i) mbar_init(&wbar[i], 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  pdl_trigger();
+  pdl_wait();
+  const int len = a.len_ptr ? min(*a.len_ptr + 1, a.S_cap) : a.len;
+  const int chunk = (len + a.splits - 1) / a.splits;
+  const int c0 = split * chunk, c1 = min(len, c0 + chunk);
+  const int per = (max(0, c1 - c0) + kNW - 1) / kNW;
+  const int w0 = c0 + warp * per, w1 = max(w0, min(c1, w0 + per));
+  const int ntile = (w1 - w0 + C::TR - 1) / C::TR;
+  auto issue = [&](int t, int stage) {
+    const int r0 = w0 + t * C::TR;
+    const uint32_t nr = static_cast<uint32_t>(min(C::TR, w1 - r0));
+    mbar_arrive_expect_tx(&wbar[stage], nr * 2u * C::RB);
+    bulk_g2s(ring + stage * C::STAGE, kp + (row0 + r0) * C::RB, nr * C::RB, &wbar[stage]);
+    bulk_g2s(ring + stage * C::STAGE + C::KT, vp + (row0 + r0) * C::RB, nr * C::RB, &wbar[stage]);
+  };
+  if (lane == 0)
+    for (int t = 0; t < min(ntile, C::NST); ++t) issue(t, t);
+  for (int i = threadIdx.x; i < G * (RK / 8); i += kNW * 32) {
+    const int gi = i / (RK / 8), u = i - gi * (RK / 8);
+    float f[8];
+    bf16x8_f32(*reinterpret_cast<const uint4*>(a.q + b * a.ldq + (g * G + gi) * a.rk + u * 8), f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) sh.qsf[gi][u * 8 + e] = f[e];
+  }
+  __syncthreads();
+  float m[G], l[G], o[G][C::CPL];
+#pragma unroll
+  for (int gi = 0; gi < G; ++gi) {
+    m[gi] = -INFINITY;
+    l[gi] = 0.f;
+#pragma unroll
+    for (int c = 0; c < C::CPL; ++c) o[gi][c] = 0.f;
+  }
+  for (int t = 0; t < ntile; ++t) {
+    const int stage = t % C::NST;
+    mbar_wait(&wbar[stage], (t / C::NST) & 1);
+    const uint8_t* Kt = ring + stage * C::STAGE;
+    const uint8_t* Vt = Kt + C::KT;
+    const int nr = min(C::TR, w1 - (w0 + t * C::TR));
+    const bool valid = lane < nr;
+    float s[G];
+#pragma unroll
+    for (int gi = 0; gi < G; ++gi) s[gi] = 0.f;
+    if (valid) {
+      const uint8_t* kr = Kt + lane * C::RB;
+#pragma unroll
+      for (int k = 0; k < RK / 16; ++k) {
+        int kc = k + (lane % (RK / 16));
+        if (kc >= RK / 16) kc -= RK / 16;
+        const uint4 u = *reinterpret_cast<const uint4*>(kr + kc * 16);
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int wi = 0; wi < 4; ++wi) {
+#pragma unroll
+          for (int e = 0; e < 4; e += 2) {
+            const float2 kf = e4m3x2_to_f32x2(w[wi] >> (8 * e));
+#pragma unroll
+            for (int gi = 0; gi < G; ++gi) {
+              s[gi] = fmaf(sh.qsf[gi][kc * 16 + wi * 4 + e], kf.x, s[gi]);
+              s[gi] = fmaf(sh.qsf[gi][kc * 16 + wi * 4 + e + 1], kf.y, s[gi]);
+            }
+          }
+        }
+      }
+      const float ksc = *reinterpret_cast<const float*>(kr + RK);
+#pragma unroll
+      for (int gi = 0; gi < G; ++gi) s[gi] *= ksc;
+    }
+    float pb[G];
+#pragma unroll
+    for (int gi = 0; gi < G; ++gi) {
+      const float x = valid ? s[gi] * scl : -INFINITY;
+      float tm = x;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, off));
+      const float mn = fmaxf(m[gi], tm);
+      const float alpha = exp2f(m[gi] - mn);
+      const float p = valid ? exp2f(x - mn) : 0.f;
+      float ps = p;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
+      l[gi] = l[gi] * alpha + ps;
+      m[gi] = mn;
+#pragma unroll
+      for (int c = 0; c < C::CPL; ++c) o[gi][c] *= alpha;
+      pb[gi] = __bfloat162float(__float2bfloat16_rn(p));  // P rounded before PV
+    }
+    // o += (P * scale_v) code_v: lane owns columns lane*CPL .. +CPL-1 (scale_v folded per row)
+    const float vsc_l = valid ? *reinterpret_cast<const float*>(Vt + lane * C::RB + RK) : 0.f;
+#pragma unroll
+    for (int gi = 0; gi < G; ++gi) pb[gi] *= vsc_l;
+    for (int j = 0; j < nr; ++j) {
+      float vf[C::CPL];
+      if constexpr (C::CPL == 2) {
+        const float2 f = e4m3x2_to_f32x2(*reinterpret_cast<const uint16_t*>(Vt + j * C::RB + lane * 2));
+        vf[0] = f.x;
+        vf[1] = f.y;
+      } else if constexpr (C::CPL == 4) {
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(Vt + j * C::RB + lane * 4);
+        const float2 f0 = e4m3x2_to_f32x2(w), f1 = e4m3x2_to_f32x2(w >> 16);
+        vf[0] = f0.x;
+        vf[1] = f0.y;
+        vf[2] = f1.x;
+        vf[3] = f1.y;
+      } else {
+#pragma unroll
+        for (int c = 0; c < C::CPL; ++c) vf[c] = e4m3_to_f32(Vt[j * C::RB + lane * C::CPL + c]);
+      }
+#pragma unroll
+      for (int gi = 0; gi < G; ++gi) {
+        const float pj = __shfl_sync(0xffffffffu, pb[gi], j);
+#pragma unroll
+        for (int c = 0; c < C::CPL; ++c) o[gi][c] = fmaf(pj, vf[c], o[gi][c]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && t + C::NST < ntile) issue(t + C::NST, stage);
+  }
+  // warp partials -> the CTA's partial -> the last CTA of (b, g) merges the splits (as above)
+#pragma unroll
+  for (int gi = 0; gi < G; ++gi) {
+    if (lane == 0) {
+      sh.wm[warp][gi] = m[gi];
+      sh.wl[warp][gi] = l[gi];
+    }
+#pragma unroll
+    for (int c = 0; c < C::CPL; ++c) sh.wo[warp][gi][lane * C::CPL + c] = o[gi][c];
+  }
+  __syncthreads();
+  const int nslots = a.splits;
+  for (int i = threadIdx.x; i < G * RK; i += kNW * 32) {
+    const int gi = i / RK, c = i - gi * RK;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kNW; ++w) M = fmaxf(M, sh.wm[w][gi]);
+    float L = 0.f, O = 0.f;
+#pragma unroll
+    for (int w = 0; w < kNW; ++w) {
+      const float f = sh.wm[w][gi] == -INFINITY ? 0.f : exp2f(sh.wm[w][gi] - M);
+      L += f * sh.wl[w][gi];
+      O += f * sh.wo[w][gi][c];
+    }
+    float* dst = a.part + ((static_cast<int64_t>(b) * a.Nh + g * G + gi) * nslots + split) * (RK + 2);
+    dst[c] = O;
+    if (c == 0) {
+      dst[RK] = M;
+      dst[RK + 1] = L;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) sh.s_last = atomicAdd(&a.counters[b * a.Nkv + g], 1) == nslots - 1;
+  __syncthreads();
+  if (!sh.s_last) return;
+  __threadfence();
+  for (int i = threadIdx.x; i < G * RK; i += kNW * 32) {
+    const int gi = i / RK, c = i - gi * RK;
+    const float* hp = a.part + ((static_cast<int64_t>(b) * a.Nh + g * G + gi) * nslots) * (RK + 2);
+    float M = -INFINITY;
+    for (int s2 = 0; s2 < nslots; ++s2) M = fmaxf(M, __ldcg(hp + s2 * (RK + 2) + RK));
+    float L = 0.f, O = 0.f;
+    for (int s2 = 0; s2 < nslots; ++s2) {
+      const float ms = __ldcg(hp + s2 * (RK + 2) + RK);
+      const float f = ms == -INFINITY ? 0.f : exp2f(ms - M);
+      L = fmaf(f, __ldcg(hp + s2 * (RK + 2) + RK + 1), L);
+      O = fmaf(f, __ldcg(hp + s2 * (RK + 2) + c), O);
+    }
+    __nv_bfloat16 ob = __float2bfloat16_rn(O / L);
+    a.o[b * a.ldo + (g * G + gi) * RK + c] = *reinterpret_cast<uint16_t*>(&ob);
+    if (c == 0 && a.lse) a.lse[b * a.Nh + g * G + gi] = (M + log2f(L)) / kLog2eD;
+  }
+  if (threadIdx.x == 0) a.counters[b * a.Nkv + g] = 0;
+}
+
+template <int RK, int G>
+static cudaError_t launch2_f8_t(const DecodeAttnArgs& a, cudaStream_t stream) {
+  using C = DA2F8<RK>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(decode_attn2_f8_kernel<RK, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kNW * C::WARP_BYTES));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  DecodeAttnArgs b = a;  // split count: the caller's (decode2_splits, the bf16 kernel's wave)
+  dim3 grid(b.splits, b.Nkv, b.B);
+  return launch_k(decode_attn2_f8_kernel<RK, G>, grid, dim3(kNW * 32), static_cast<size_t>(kNW * C::WARP_BYTES), stream,
+                  g_pdl && (g_pdl_mask & 2), b, reinterpret_cast<const uint8_t*>(b.k),
+                  reinterpret_cast<const uint8_t*>(b.v));
+}
+
+template <int G>
+static cudaError_t launch2_f8_g(const DecodeAttnArgs& a, cudaStream_t s) {
+  switch (a.rk) {
+    case 32: return launch2_f8_t<32, G>(a, s);
+    case 64: return launch2_f8_t<64, G>(a, s);
+    case 96: return launch2_f8_t<96, G>(a, s);
+    case 128: return launch2_f8_t<128, G>(a, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+cudaError_t launch_decode2_f8(const DecodeAttnArgs& a, cudaStream_t s) {
+  if (a.k1 || a.rk != a.rv || !a.counters || a.splits > 128) return cudaErrorInvalidValue;
+  switch (a.Nh / a.Nkv) {
+    case 1: return launch2_f8_g<1>(a, s);
+    case 2: return launch2_f8_g<2>(a, s);
+    case 4: return launch2_f8_g<4>(a, s);
+    case 8: return launch2_f8_g<8>(a, s);
+    default: return cudaErrorNotSupported;
+  }
 }
 
 template <int RK, int G>

@@ -171,6 +171,7 @@ struct DecodeAttnArgs {
   int S_cap = 0;
   int len = 0;                   // upper bound on any pool's rows (fixes the split count)
   const int* len_ptr = nullptr;  // uniform cache: pool-0 rows = *len_ptr + 1
+  int kv_fp8 = 0;                // FP8 cache rows (NEXT-4): launch_decode_attention -> launch_decode2_f8
   const int* n0_ptr = nullptr;   // token split: per-sequence rows of pool 0 / pool 1 [B]
   const int* n1_ptr = nullptr;
   uint16_t* o = nullptr;  // O' [B][ldo]
@@ -196,6 +197,13 @@ cudaError_t launch_decode_attention_tc(const DecodeAttnArgs& a, cudaStream_t str
 cudaError_t launch_decode2_partial(const DecodeAttnArgs& a, int width, const uint16_t* kp, const uint16_t* vp,
                                    int pool, int slot0, int nslots, cudaStream_t s);
 int decode2_splits(int B, int Nkv, int len, int width, int G);
+// NEXT-4: decode attention over the FP8 cache (decode_attn2.cu; uniform rank, one pool)
+cudaError_t launch_decode2_f8(const DecodeAttnArgs& a, cudaStream_t s);
+// NEXT-4 (kv_quant.cu): bf16 rows -> FP8 E4M3 rows (r codes, f32 scale, 12 pad bytes), reading c23.
+// Rows (bg, t) for bg < n_bg, t in [t0, t0 + T): src at (bg * src_bg + t) * w elements (bf16), dst
+// at (bg * S_cap + pos) * (w + 16) bytes with pos = (pos_ptr ? min(*pos_ptr, S_cap - 1) : 0) + t.
+cudaError_t launch_quantize_kv(const uint16_t* src, int64_t src_bg, uint8_t* dst, int S_cap, int n_bg, int t0, int T,
+                               int w, const int* pos_ptr, cudaStream_t s);
 int decode_splits(int B, int Nkv, int len);
 
 // ---- the fused decode layer-step (decode_fused.cuh): a1 + a2 + a3 + a5 of a run of consecutive
