@@ -226,8 +226,8 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
     if (L.n_qkv > max_nqkv) max_nqkv = L.n_qkv;
     if (L.rv_p > max_rv) max_rv = L.rv_p;
   }
-  c->len_dev_off = coff;  // [n_layers] device lengths + the decode overflow flag
-  coff = align_up(coff + static_cast<int64_t>(d.n_layers + 1) * 4, 256);
+  c->len_dev_off = coff;  // [n_layers] device lengths, the decode overflow flag, the NaN-score flag
+  coff = align_up(coff + static_cast<int64_t>(d.n_layers + 2) * 4, 256);
   c->weight_bytes = woff;
   c->cache_bytes = coff;
   const int64_t rows = static_cast<int64_t>(max_batch) * max_seq;
@@ -436,6 +436,10 @@ zdc_status zdc_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, ui
   zdc_status st = check_run(c, l0, l1, x, y, "zdc_prefill");
   if (st != ZDC_OK) return st;
   if (B <= 0 || S <= 0) return fail(ZDC_ERR_SHAPE, "zdc_prefill: B=%d S=%d", B, S);
+  {
+    const long long nb = 2LL * B * S * c->dims.d_model;
+    if (ranges_overlap(x, nb, y, nb)) return fail(ZDC_ERR_INVALID_ARG, "zdc_prefill: x and y overlap");
+  }
   if (B > c->max_batch || S > c->max_seq)
     return fail(ZDC_ERR_CAPACITY, "zdc_prefill: B=%d S=%d exceeds max_batch=%d max_seq=%d", B, S, c->max_batch,
                 c->max_seq);
@@ -514,7 +518,7 @@ zdc_status zdc_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, ui
                                        importance ? importance + static_cast<int64_t>(l) * B * c->max_seq : nullptr,
                                        c->max_seq, nullptr, s));
         ZDC_CUDA_TRY(launch_select(scores, c->max_seq, S, L.g_bp, B, reinterpret_cast<uint8_t*>(c->cache + L.cls_off),
-                                   reinterpret_cast<float*>(c->cache + L.tau_off), s));
+                                   reinterpret_cast<float*>(c->cache + L.tau_off), s, c->len_dev() + c->dims.n_layers + 1));
       }
       // a2 (split): stable class-aware compaction of the staged rows into pool_I / pool_U
       int* didx = reinterpret_cast<int*>(c->scratch + c->s_didx);
@@ -803,6 +807,8 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
 
 zdc_status zdc_decode(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, uint16_t* y, int32_t B, void* stream) {
   zdc_status st = check_run(c, l0, l1, x, y, "zdc_decode");
+  if (st == ZDC_OK && B > 0 && ranges_overlap(x, 2LL * B * c->dims.d_model, y, 2LL * B * c->dims.d_model))
+    return fail(ZDC_ERR_INVALID_ARG, "zdc_decode: x and y overlap");
   if (st != ZDC_OK) return st;
   if (B <= 0 || B > c->max_batch) return fail(ZDC_ERR_CAPACITY, "zdc_decode: B=%d (max_batch %d)", B, c->max_batch);
   if (c->batch != 0 && B != c->batch) return fail(ZDC_ERR_SHAPE, "zdc_decode: B=%d but cache batch is %d", B, c->batch);
@@ -874,10 +880,13 @@ zdc_status zdc_cache_sync(zdc_ctx* c, void* stream) {
   if (!c) return fail(ZDC_ERR_INVALID_ARG, "zdc_cache_sync: null ctx");
   if (!c->cache) return fail(ZDC_ERR_STATE, "zdc_cache_sync: ctx not bound");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  std::vector<int> h(c->dims.n_layers + 1);
+  std::vector<int> h(c->dims.n_layers + 2);
   ZDC_CUDA_TRY(cudaMemcpyAsync(h.data(), c->len_dev(), h.size() * 4, cudaMemcpyDeviceToHost, s));
   ZDC_CUDA_TRY(cudaStreamSynchronize(s));
   for (int l = 0; l < c->dims.n_layers; ++l) c->len[l] = h[l];
+  if (h[c->dims.n_layers + 1])
+    return fail(ZDC_ERR_INVALID_ARG, "zdc_cache_sync: a representative layer produced a NaN importance score "
+                "(non-finite activations); its classes are invalid (zdc_cache_reset clears)");
   if (h[c->dims.n_layers])
     return fail(ZDC_ERR_CAPACITY, "zdc_cache_sync: decode steps replayed past max_seq = %d (each step uses one "
                 "row; the overflowing steps rewrote the last row and their outputs are invalid; zdc_cache_reset clears)",
@@ -889,7 +898,7 @@ zdc_status zdc_cache_reset(zdc_ctx* c, void* stream) {
   if (!c) return fail(ZDC_ERR_INVALID_ARG, "zdc_cache_reset: null ctx");
   if (!c->cache) return fail(ZDC_ERR_STATE, "zdc_cache_reset: ctx not bound");
   // Only the lengths are reset: no kernel ever reads a cache row at or beyond its layer's length.
-  ZDC_CUDA_TRY(cudaMemsetAsync(c->len_dev(), 0, static_cast<size_t>(c->dims.n_layers + 1) * 4,
+  ZDC_CUDA_TRY(cudaMemsetAsync(c->len_dev(), 0, static_cast<size_t>(c->dims.n_layers + 2) * 4,
                                static_cast<cudaStream_t>(stream)));
   c->len.assign(c->dims.n_layers, 0);
   c->sp_layer.assign(c->dims.n_layers, 0);

@@ -9,6 +9,12 @@
 namespace zdc {
 void set_error(const char* fmt, ...);
 zdc_status fail(zdc_status s, const char* fmt, ...);
+// byte ranges [a, a + na) and [b, b + nb) overlap (the x / y alias check of every entry point)
+inline bool ranges_overlap(const void* a, long long na, const void* b, long long nb) {
+  const char* pa = static_cast<const char*>(a);
+  const char* pb = static_cast<const char*>(b);
+  return pa < pb + nb && pb < pa + na;
+}
 }  // namespace zdc
 
 #define ZDC_CUDA_TRY(expr)                                                                   \

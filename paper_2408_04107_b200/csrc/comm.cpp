@@ -19,6 +19,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -200,7 +201,9 @@ static zdc_status sp_allgather(zdc_ctx* c, uint8_t* buf, int64_t chunk_bytes, cu
 zdc_status zdc_sp_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, uint16_t* y, int32_t B,
                           int32_t S_total, int32_t layout, zdc_sp_stats* stats, void* stream) {
   if (!c || !x || !y) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_prefill: null argument");
-  if (x == y) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_prefill: x and y alias");
+  if (x == y || (B > 0 && S_total > 0 && ranges_overlap(x, 2LL * B * (S_total / std::max(1, c->comm ? c->comm->world : 1)) * c->dims.d_model,
+                                                      y, 2LL * B * (S_total / std::max(1, c->comm ? c->comm->world : 1)) * c->dims.d_model)))
+    return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_prefill: x and y overlap");
   if (!c->w) return fail(ZDC_ERR_STATE, "zdc_sp_prefill: ctx not bound");
   if (c->kv_fp8) return fail(ZDC_ERR_UNSUPPORTED, "zdc_sp_prefill: the FP8 cache (kv_fp8) is single-GPU");
   if (!c->comm) return fail(ZDC_ERR_STATE, "zdc_sp_prefill: zdc_comm_init not called");
@@ -338,7 +341,7 @@ zdc_status zdc_sp_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x,
       float* scores = reinterpret_cast<float*>(c->cache + L.score_off);
       ZDC_CUDA_TRY(launch_sp_scores_global(slots, P, B, n_local, S_total, layout, scores, c->max_seq, s));
       ZDC_CUDA_TRY(launch_select(scores, c->max_seq, S_total, L.g_bp, B, c->cache + L.cls_off,
-                                 reinterpret_cast<float*>(c->cache + L.tau_off), s));
+                                 reinterpret_cast<float*>(c->cache + L.tau_off), s, c->len_dev() + c->dims.n_layers + 1));
       ZDC_CUDA_TRY(launch_sp_truncate(gbuf, 0, P, P, layout, S_total, B, Nkv, n_local, L.rk_p, L.rku,
                                       c->cache + L.cls_off, c->max_seq, s));
     }
@@ -405,7 +408,9 @@ static zdc_status sp_alltoall(zdc_ctx* c, const uint8_t* send, uint8_t* recv, in
 zdc_status zdc_sp_prefill_ulysses(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, uint16_t* y, int32_t B,
                                   int32_t S_total, int32_t layout, zdc_sp_stats* stats, void* stream) {
   if (!c || !x || !y) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_prefill_ulysses: null argument");
-  if (x == y) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_prefill_ulysses: x and y alias");
+  if (x == y || (B > 0 && S_total > 0 && ranges_overlap(x, 2LL * B * (S_total / std::max(1, c->comm ? c->comm->world : 1)) * c->dims.d_model,
+                                                      y, 2LL * B * (S_total / std::max(1, c->comm ? c->comm->world : 1)) * c->dims.d_model)))
+    return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_prefill_ulysses: x and y overlap");
   if (!c->w) return fail(ZDC_ERR_STATE, "zdc_sp_prefill_ulysses: ctx not bound");
   if (c->kv_fp8) return fail(ZDC_ERR_UNSUPPORTED, "zdc_sp_prefill_ulysses: the FP8 cache (kv_fp8) is single-GPU");
   if (!c->comm) return fail(ZDC_ERR_STATE, "zdc_sp_prefill_ulysses: zdc_comm_init / an all-to-all hook not set");
@@ -561,7 +566,8 @@ zdc_status zdc_sp_prefill_ulysses(zdc_ctx* c, int32_t l0, int32_t l1, const uint
 
 zdc_status zdc_sp_decode(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, uint16_t* y, int32_t B, void* stream) {
   if (!c || !x || !y) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_decode: null argument");
-  if (x == y) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_decode: x and y alias");
+  if (x == y || (B > 0 && ranges_overlap(x, 2LL * B * c->dims.d_model, y, 2LL * B * c->dims.d_model)))
+    return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_decode: x and y overlap");
   if (!c->w || !c->comm) return fail(ZDC_ERR_STATE, "zdc_sp_decode: ctx not bound / no communicator");
   if (l0 < 0 || l1 > c->dims.n_layers || l0 >= l1) return fail(ZDC_ERR_SHAPE, "zdc_sp_decode: layer range [%d, %d)", l0, l1);
   if (B != c->batch) return fail(ZDC_ERR_SHAPE, "zdc_sp_decode: B=%d but the SP prefill had B=%d", B, c->batch);

@@ -698,6 +698,16 @@ inline cudaError_t launch_fused_t(DecFusedArgs a, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  // the grid barriers need every CTA resident at once: one per SM (num_sms() CTAs).  Checked once
+  // per shared-memory size with the occupancy API; otherwise the caller runs the separate kernels.
+  static size_t checked_smem = 0;
+  if (checked_smem != smem) {
+    int per_sm = 0;
+    cudaError_t eo = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_fused_kernel<NB, RK, G>, kNC + 32, smem);
+    if (eo != cudaSuccess) return eo;
+    if (per_sm < 1) return cudaErrorNotSupported;
+    checked_smem = smem;
+  }
   prof_mark(stream, true, g_prof_class);
   cudaError_t e = launch_k(decode_fused_kernel<NB, RK, G>, dim3(num_sms()), dim3(kNC + 32), smem, stream, g_pdl, a);
   prof_mark(stream, false, g_prof_class);

@@ -295,7 +295,7 @@ cudaError_t launch_pack_weights_bf16(const uint16_t* wq, const uint16_t* wk, con
 cudaError_t launch_importance(const float* lse, int T, int Nh, int B, int t0, int mode, float* scores, int64_t ld,
                               float* out_copy, int64_t ld_copy, const int* pos_ptr, cudaStream_t s);
 cudaError_t launch_select(const float* scores, int64_t ld, int S, int g_bp, int B, uint8_t* cls, float* tau,
-                          cudaStream_t s);
+                          cudaStream_t s, int* nan_flag = nullptr);
 cudaError_t launch_truncate(uint16_t* kv, int width, int r_u, int B, int Nkv, int S, int S_cap, const uint8_t* cls,
                             int64_t ld_cls, cudaStream_t s);
 cudaError_t launch_rank(const uint8_t* cls, int64_t ld_cls, int S, int B, int* didx, int64_t ld_didx, int* pos_i,

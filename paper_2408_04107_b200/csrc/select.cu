@@ -48,9 +48,14 @@ __device__ __forceinline__ uint64_t order_key(float score, int t) {
 
 // One CTA of 1024 threads per sequence.  Important = the k largest keys.
 __global__ void __launch_bounds__(1024) select_kernel(const float* __restrict__ scores, int64_t ld, int S, int g_bp,
-                                                      uint8_t* __restrict__ cls, float* __restrict__ tau) {
+                                                      uint8_t* __restrict__ cls, float* __restrict__ tau,
+                                                      int* __restrict__ nan_flag) {
   const int b = blockIdx.x;
   const float* sc = scores + b * ld;
+  // a NaN score has no place in the order (the oracle raises, reading c11): flag it for the host
+  if (nan_flag)
+    for (int t = threadIdx.x; t < S; t += blockDim.x)
+      if (isnan(sc[t])) *nan_flag = 1;
   const int k = static_cast<int>((static_cast<int64_t>(g_bp) * S + 9999) / 10000);
   __shared__ uint32_t hist[256];
   __shared__ uint64_t s_prefix;
@@ -304,8 +309,8 @@ cudaError_t launch_importance(const float* lse, int T, int Nh, int B, int t0, in
 }
 
 cudaError_t launch_select(const float* scores, int64_t ld, int S, int g_bp, int B, uint8_t* cls, float* tau,
-                          cudaStream_t s) {
-  select_kernel<<<B, 1024, 0, s>>>(scores, ld, S, g_bp, cls, tau);
+                          cudaStream_t s, int* nan_flag) {
+  select_kernel<<<B, 1024, 0, s>>>(scores, ld, S, g_bp, cls, tau, nan_flag);
   ++g_launches;
   return cudaGetLastError();
 }

@@ -144,3 +144,31 @@ def test_split_c3_shape_slice():
         yd = _decode(ctx, Z.decode_input(dims, 3, B, t))
         wd = m.decode(Z.decode_input(dims, 3, B, t))
         assert normwise(yd, wd) <= TOL
+
+
+def test_nan_importance_is_reported_and_overlap_rejected():
+    """A NaN importance score (non-finite activations) is flagged by the selector and reported by
+    zdc_cache_sync (the oracle's selector raises on NaN, reading c11); x / y ranges that overlap
+    without being equal are rejected (ADVICE / VERDICT r1 hygiene)."""
+    import paper_2408_04107_b200 as zdc
+    dims = Dims(1, 64, 2, 2, 32)
+    plan = plan_split(1, 16, 8, [[0]], [5000])
+    _, folded = fold_stack(dims, 1, n_calib=256)
+    ctx = make_context(dims, plan, folded, 1, 64)
+    x = Z.prompt(dims, 1, 1, 32, seed=71)
+    x[0, 5, :] = np.nan
+    xd = to_dev_bf16(x)
+    y = torch.empty_like(xd)
+    ctx.prefill(xd, y)
+    torch.cuda.synchronize()
+    with pytest.raises(zdc.ZdcError) as e:
+        ctx.cache_sync()
+    assert e.value.status == -1
+    ctx.reset()
+    ctx.cache_sync()
+    buf = torch.zeros(2 * 32 * 64, dtype=torch.bfloat16, device="cuda")
+    xa = buf[: 32 * 64].view(1, 32, 64)
+    ya = buf[16 * 64: 48 * 64].view(1, 32, 64)   # overlaps xa by 16 rows
+    with pytest.raises(zdc.ZdcError):
+        ctx.prefill(xa, ya)
+    ctx.close()
