@@ -348,7 +348,7 @@ def sp_bench(args, zdc, torch, dist, rank, world, dev, stream, dataflow="allgath
     y = torch.empty_like(x)
     for _ in range(2):  # warm-up (NCCL connection set-up, kernel attributes)
         ctx.reset()
-        ctx.sp_prefill(x, y, S_tot, layout=1, stream=stream, dataflow=dataflow)
+        ctx.sp_prefill(x, y, S_tot, layout=2 if dataflow == "allgather" else 1, stream=stream, dataflow=dataflow)
     torch.cuda.synchronize()
     reps = max(1, args.steps)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -359,13 +359,13 @@ def sp_bench(args, zdc, torch, dist, rank, world, dev, stream, dataflow="allgath
         ctx.reset()
         torch.cuda.synchronize()
         e0.record(stream)
-        ctx.sp_prefill(x, y, S_tot, layout=1, stream=stream, dataflow=dataflow)
+        ctx.sp_prefill(x, y, S_tot, layout=2 if dataflow == "allgather" else 1, stream=stream, dataflow=dataflow)
         e1.record(stream)
         torch.cuda.synchronize()
         ms += e0.elapsed_time(e1)
     ms /= reps
     ctx.reset()
-    st = ctx.sp_prefill(x, y, S_tot, layout=1, stats=True, stream=stream, dataflow=dataflow)
+    st = ctx.sp_prefill(x, y, S_tot, layout=2 if dataflow == "allgather" else 1, stats=True, stream=stream, dataflow=dataflow)
     torch.cuda.synchronize()
     tt = torch.tensor([ms, st["exchange_ms"], -st["exchange_ms"]], device=dev)
     if world > 1:
@@ -374,7 +374,7 @@ def sp_bench(args, zdc, torch, dist, rank, world, dev, stream, dataflow="allgath
     per_layer_recv = st["bytes_recv"] / Lsp
     ctx.close()
     out = {"workload": "c5_sp_llama2_7b", "dataflow": dataflow, "S_total": S_tot, "layers": Lsp, "P": world,
-           "layout": "zigzag",
+           "layout": "zigzag, exchange overlapped on a comm stream (layout 2)" if dataflow == "allgather" else "zigzag",
            "rank": r, "ms": ms, "sp_prefill_tok_s": S_tot / (ms / 1e3),
            "bytes_recv_per_gpu_per_layer": per_layer_recv,
            "bytes_recv_uncompressed_per_gpu_per_layer": st["bytes_recv_uncompressed"] / Lsp,

@@ -200,7 +200,13 @@ zdc_status zdc_decode(zdc_ctx* ctx, int32_t l0, int32_t l1, const uint16_t* x, u
  * the exchange here is an all-gather of compressed K'/V', reading c17).  Rank p of P
  * holds S_total/P tokens of every sequence:
  *   layout 0 = contiguous (rank p holds [p S/P, (p+1) S/P)),
- *   layout 1 = zigzag (2P chunks of S/(2P); rank p holds chunks p and 2P-1-p).
+ *   layout 1 = zigzag (2P chunks of S/(2P); rank p holds chunks p and 2P-1-p),
+ *   layout 2 = zigzag with the exchange overlapped: the gather buffer is half-major
+ *     [2][P][K|V][B][N_kv][S/(2P)][r]; a1 runs per local chunk and each half (every rank's early /
+ *     late chunk) is all-gathered on a library-owned comm stream as soon as it exists -- half 0
+ *     overlaps the late chunk's a1, half 1 overlaps the early chunk's attention (which needs keys
+ *     of half 0 only); the compute stream waits on events.  Same result rows as layout 1 (bit for
+ *     bit); not combinable with a token split or zdc_sp_decode (ZDC_ERR_UNSUPPORTED).
  * Per layer: a1 on local tokens -> all-gather of K'/V' over NCCL (the only data moved;
  * bytes = (P-1)/P * B S N_kv (r_k + r_v) * 2) -> a3 for local queries against all keys at
  * or before their global position -> a5 on local rows.  The result rows equal the

@@ -75,6 +75,10 @@ __global__ void __launch_bounds__(352, 1)
     const int pos = j * C::BN;
     if (a.kv_mode == 0) return (b * a.Nkv + g) * a.S_cap + pos;
     const int qq = pos / a.sp_chunk, rr = pos - qq * a.sp_chunk;  // SP gather buffer
+    if (a.kv_mode == 2) {  // zigzag, half-major buffer [half][owner][K|V][B][Nkv][chunk][r] (overlapped exchange)
+      const int h = qq < a.sp_P ? 0 : 1, ow = h == 0 ? qq : 2 * a.sp_P - 1 - qq;
+      return (((h * a.sp_P + ow) * 2 * a.B + b) * a.Nkv + g) * a.sp_chunk + rr;
+    }
     int owner, local;
     if (!a.sp_zigzag) {
       owner = qq;

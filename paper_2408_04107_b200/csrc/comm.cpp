@@ -83,10 +83,28 @@ struct CommState {
   zdc_alltoall_fn a2a_hook = nullptr;
   void* a2a_user = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
+  // overlapped exchange (layout 2): a dedicated comm stream and its handoff events
+  cudaStream_t cs = nullptr;
+  cudaEvent_t e_a1[2] = {nullptr, nullptr}, e_ag[2] = {nullptr, nullptr};
 };
+
+static cudaError_t comm_stream(CommState* cm) {
+  if (cm->cs) return cudaSuccess;
+  cudaError_t e = cudaStreamCreateWithFlags(&cm->cs, cudaStreamNonBlocking);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&cm->e_a1[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cm->e_ag[i], cudaEventDisableTiming);
+  }
+  return e;
+}
 
 void comm_destroy(zdc_ctx* c) {
   if (!c->comm) return;
+  if (c->comm->cs) cudaStreamDestroy(c->comm->cs);
+  for (int i = 0; i < 2; ++i) {
+    if (c->comm->e_a1[i]) cudaEventDestroy(c->comm->e_a1[i]);
+    if (c->comm->e_ag[i]) cudaEventDestroy(c->comm->e_ag[i]);
+  }
   if (c->comm->comm && nccl_api()->ok) nccl_api()->CommDestroy(c->comm->comm);
   if (c->comm->e0) cudaEventDestroy(c->comm->e0);
   if (c->comm->e1) cudaEventDestroy(c->comm->e1);
@@ -94,7 +112,7 @@ void comm_destroy(zdc_ctx* c) {
   c->comm = nullptr;
 }
 
-// global position of local token t on rank p (layout 0 contiguous, 1 zigzag)
+// global position of local token t on rank p (layout 0 contiguous, 1 zigzag, 2 zigzag overlapped)
 static inline int sp_position(int S, int P, int p, int layout, int t) {
   const int n = S / P;
   if (layout == 0) return p * n + t;
@@ -174,11 +192,11 @@ zdc_status zdc_sp_set_alltoall_hook(zdc_ctx* c, zdc_alltoall_fn fn, void* user, 
 
 zdc_status zdc_sp_positions(int32_t S_total, int32_t world, int32_t rank, int32_t layout, int32_t* positions) {
   if (!positions) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_positions: null output");
-  if (world < 1 || rank < 0 || rank >= world || (layout != 0 && layout != 1))
+  if (world < 1 || rank < 0 || rank >= world || layout < 0 || layout > 2)
     return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_positions: rank %d world %d layout %d", rank, world, layout);
-  if (S_total <= 0 || S_total % (layout == 1 ? 2 * world : world) != 0)
+  if (S_total <= 0 || S_total % (layout >= 1 ? 2 * world : world) != 0)
     return fail(ZDC_ERR_SHAPE, "zdc_sp_positions: S_total %d not divisible by %d", S_total,
-                layout == 1 ? 2 * world : world);
+                layout >= 1 ? 2 * world : world);
   const int n = S_total / world;
   for (int t = 0; t < n; ++t) positions[t] = sp_position(S_total, world, rank, layout, t);
   return ZDC_OK;
@@ -210,11 +228,11 @@ zdc_status zdc_sp_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x,
   if (l0 < 0 || l1 > c->dims.n_layers || l0 >= l1)
     return fail(ZDC_ERR_SHAPE, "zdc_sp_prefill: layer range [%d, %d)", l0, l1);
   const int P = c->comm->world, p = c->comm->rank;
-  if (layout != 0 && layout != 1) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_prefill: layout %d", layout);
-  const int parts = layout == 1 ? 2 * P : P;
+  if (layout < 0 || layout > 2) return fail(ZDC_ERR_INVALID_ARG, "zdc_sp_prefill: layout %d", layout);
+  const int parts = layout >= 1 ? 2 * P : P;
   if (B <= 0 || S_total <= 0 || S_total % parts != 0)
     return fail(ZDC_ERR_SHAPE, "zdc_sp_prefill: S_total %d not divisible by %d (%s layout)", S_total, parts,
-                layout == 1 ? "zigzag" : "contiguous");
+                layout >= 1 ? "zigzag" : "contiguous");
   const int n_local = S_total / P;
   const int chunk = S_total / parts;
   if (P > 1 && chunk % 128 != 0)
@@ -222,8 +240,11 @@ zdc_status zdc_sp_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x,
   if (B > c->max_batch || S_total > c->max_seq)
     return fail(ZDC_ERR_CAPACITY, "zdc_sp_prefill: B=%d S_total=%d exceeds max_batch=%d max_seq=%d", B, S_total,
                 c->max_batch, c->max_seq);
+  const bool overlap = layout == 2 && P > 1;  // half-major gather buffer, exchange on the comm stream
   for (int l = l0; l < l1; ++l) {
     const LayerInfo& L = c->layers[l];
+    if (layout == 2 && L.split)
+      return fail(ZDC_ERR_UNSUPPORTED, "zdc_sp_prefill: layout 2 (overlapped exchange) with a token split (layer %d)", l);
     // a layer reusing classes needs its representative classified by an SP prefill of this prompt
     if (L.split && L.rep != l && L.rep < l0 && c->sp_layer[L.rep] != 1)
       return fail(ZDC_ERR_STATE, "zdc_sp_prefill: layer %d: representative %d has not classified this prompt", l, L.rep);
@@ -277,6 +298,96 @@ zdc_status zdc_sp_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x,
     q.vb = q.vg * Nkv;
     q.pos0 = 0;
     g_prof_class = kProfGemmQkv;
+    if (overlap) {
+      // layout 2: the gather buffer is half-major [2][P][K|V][B][Nkv][chunk][r]; the a1 rows of each
+      // local chunk (half h) go to block (h, p), and each half is all-gathered on the comm stream as
+      // soon as its rows exist: half 0 (the first P chunks, every key of the local early chunk's
+      // queries) overlaps the second half's a1; half 1 overlaps the early chunk's attention
+      ZDC_CUDA_TRY(comm_stream(c->comm));
+      const int64_t bnc = static_cast<int64_t>(B) * Nkv * chunk;
+      const int64_t half_elems = static_cast<int64_t>(P) * 2 * bnc * L.rk_p;
+      const int64_t hchunk_bytes = 2 * bnc * L.rk_p * 2;
+      for (int h = 0; h < 2; ++h) {
+        for (int b = 0; b < B; ++b) {
+          Epilogue eh = e1;
+          QkvDest& qh = eh.qkv;
+          qh.q = q.q + (static_cast<int64_t>(b) * n_local + h * chunk) * L.nq;
+          qh.k = gbuf + h * half_elems + p * 2 * bnc * L.rk_p + static_cast<int64_t>(b) * Nkv * chunk * L.rk_p;
+          qh.v = qh.k + bnc * L.rk_p;
+          qh.S = chunk;
+          qh.kg = static_cast<int64_t>(chunk) * L.rk_p;
+          qh.kb = qh.kg * Nkv;
+          qh.vg = static_cast<int64_t>(chunk) * L.rv_p;
+          qh.vb = qh.vg * Nkv;
+          ZDC_CUDA_TRY(launch_gemm(xin + (static_cast<int64_t>(b) * n_local + h * chunk) * d, d,
+                                   reinterpret_cast<const uint16_t*>(c->w + L.w_qkv), d, chunk, L.n_qkv, d, eh, s));
+        }
+        ZDC_CUDA_TRY(cudaEventRecord(c->comm->e_a1[h], s));
+        ZDC_CUDA_TRY(cudaStreamWaitEvent(c->comm->cs, c->comm->e_a1[h], 0));
+        if (stats) {
+          cudaEvent_t e;
+          ZDC_CUDA_TRY(cudaEventCreate(&e));
+          ZDC_CUDA_TRY(cudaEventRecord(e, c->comm->cs));
+          ev.push_back(e);
+        }
+        if (zdc_status st = sp_allgather(c, reinterpret_cast<uint8_t*>(gbuf + h * half_elems), hchunk_bytes, c->comm->cs))
+          return st;
+        if (stats) {
+          cudaEvent_t e;
+          ZDC_CUDA_TRY(cudaEventCreate(&e));
+          ZDC_CUDA_TRY(cudaEventRecord(e, c->comm->cs));
+          ev.push_back(e);
+        }
+        ZDC_CUDA_TRY(cudaEventRecord(c->comm->e_ag[h], c->comm->cs));
+      }
+      g_prof_class = kProfOther;
+      bytes_recv += (P - 1) * 2 * hchunk_bytes;
+      bytes_recv_unc += (P - 1) * 2 * slot_rows * c->dims.d_head * 2;
+      for (int sg = 0; sg < 2; ++sg) {  // the early chunk needs half 0 only; the late chunk both
+        ZDC_CUDA_TRY(cudaStreamWaitEvent(s, c->comm->e_ag[sg], 0));
+        PrefillAttnArgs a;
+        a.q = reinterpret_cast<const uint16_t*>(c->scratch + c->s_q);
+        a.ldq = L.nq;
+        a.k = gbuf;
+        a.v = gbuf;
+        a.kv_mode = 2;
+        a.sp_P = P;
+        a.sp_n_local = n_local;
+        a.sp_chunk = chunk;
+        a.sp_zigzag = 1;
+        a.v_row_off = bnc;
+        a.kv_rows_total = static_cast<int64_t>(P) * 2 * slot_rows;
+        a.S_cap = n_local;
+        a.o = reinterpret_cast<uint16_t*>(c->scratch + c->s_o);
+        a.ldo = L.ko_p;
+        a.lse = reinterpret_cast<float*>(c->scratch + c->s_lse);
+        a.B = B;
+        a.S = n_local;
+        a.Nh = Nh;
+        a.Nkv = Nkv;
+        a.rk = L.rk_p;
+        a.rv = L.rv_p;
+        a.scale = 1.0f / std::sqrt(static_cast<float>(c->dims.d_head));
+        a.q_row0 = sg * chunk;
+        a.n_q = chunk;
+        a.q_pos0 = sp_position(S_total, P, p, 1, a.q_row0);
+        ZDC_CUDA_TRY(launch_prefill_attention(a, s));
+      }
+      Epilogue e5o;
+      e5o.mode = 0;
+      e5o.d = y;
+      e5o.ldd = d;
+      g_prof_class = kProfGemmO;
+      ZDC_CUDA_TRY(launch_gemm(reinterpret_cast<const uint16_t*>(c->scratch + c->s_o), L.ko_p,
+                               reinterpret_cast<const uint16_t*>(c->w + L.w_o), L.ko_p, M, d, L.ko_p, e5o, s));
+      g_prof_class = kProfOther;
+      c->len[l] = S_total;
+      c->sp_layer[l] = 3;
+      c->sp_prompt[l] = S_total;
+      c->last_layer = l;
+      c->last_T = n_local;
+      continue;
+    }
     ZDC_CUDA_TRY(launch_gemm(xin, d, reinterpret_cast<const uint16_t*>(c->w + L.w_qkv), d, M, L.n_qkv, d, e1, s));
     // a layer that reuses its representative's classes: unimportant rows of this rank's slot lose
     // dims >= r^u BEFORE the exchange and the attention (P:774-776 DEL; reading c13)

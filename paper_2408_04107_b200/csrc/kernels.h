@@ -109,7 +109,8 @@ struct PrefillAttnArgs {
   int q_row0;          // first row of this chunk inside the Q'/O' matrices
   int n_q;             // number of query rows of this launch (per sequence)
   // key addressing: kv_mode 0 = position-ordered rows (above); 1 = SP gather buffer
-  // [P][K|V][B][Nkv][sp_n_local][r]: key position -> (owner rank, local row) by the layout
+  // [P][K|V][B][Nkv][sp_n_local][r]: key position -> (owner rank, local row) by the layout;
+  // 2 = zigzag half-major gather buffer [2][P][K|V][B][Nkv][sp_chunk][r] (overlapped exchange)
   int kv_mode = 0;
   int sp_P = 1, sp_n_local = 0, sp_chunk = 0, sp_zigzag = 0;
   int64_t v_row_off = 0;      // V row = K row + v_row_off (kv_mode 1: both maps share the base)

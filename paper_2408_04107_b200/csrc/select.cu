@@ -212,6 +212,8 @@ __global__ void append_kernel(const uint16_t* __restrict__ knew, const uint16_t*
                               int* __restrict__ n_u, int* __restrict__ pos_i, int* __restrict__ pos_u, int64_t ld_pos,
                               const int* __restrict__ len_ptr, const uint8_t* __restrict__ rep_cls, int64_t ld_cls,
                               int is_rep) {
+  pdl_wait();     // knew / vnew come from the a1 projection (a programmatic launch waits for it)
+  pdl_trigger();  // the attention may start its prologue
   const int b = blockIdx.x;
   const int t = *len_ptr;
   if (t >= S_cap) return;  // cache full (graph replays past max_seq): the a5 length advance flags it
@@ -257,6 +259,8 @@ __global__ void classify_kernel(const float* __restrict__ lse, int Nh, int mode,
                                 uint16_t* __restrict__ vi, uint16_t* __restrict__ ku, uint16_t* __restrict__ vu,
                                 int wu, int r_u, int S_cap, int* __restrict__ n_i, int* __restrict__ n_u,
                                 int* __restrict__ pos_i, int* __restrict__ pos_u, const int* __restrict__ len_ptr) {
+  pdl_wait();     // the LSE of the attention
+  pdl_trigger();
   const int b = blockIdx.x;
   const int t = *len_ptr;
   if (t >= S_cap) return;  // cache full: nothing was appended
@@ -340,20 +344,20 @@ cudaError_t launch_append(const uint16_t* knew, const uint16_t* vnew, int w, int
                           uint16_t* ku, uint16_t* vu, int wu, int r_u, int S_cap, int* n_i, int* n_u, int* pos_i,
                           int* pos_u, int64_t ld_pos, const int* len_ptr, const uint8_t* rep_cls, int64_t ld_cls,
                           int is_rep, int B, cudaStream_t s) {
-  append_kernel<<<B, 256, 0, s>>>(knew, vnew, w, Nkv, ki, vi, ku, vu, wu, r_u, S_cap, n_i, n_u, pos_i, pos_u, ld_pos,
-                                  len_ptr, rep_cls, ld_cls, is_rep);
+  cudaError_t e = launch_k(append_kernel, dim3(B), dim3(256), 0, s, g_pdl, knew, vnew, w, Nkv, ki, vi, ku, vu, wu, r_u,
+                           S_cap, n_i, n_u, pos_i, pos_u, ld_pos, len_ptr, rep_cls, ld_cls, is_rep);
   ++g_launches;
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_classify(const float* lse, int Nh, int mode, const float* tau, float* scores, uint8_t* cls,
                             int64_t ld, float* out_copy, int64_t ld_copy, int w, int Nkv, uint16_t* ki, uint16_t* vi,
                             uint16_t* ku, uint16_t* vu, int wu, int r_u, int S_cap, int* n_i, int* n_u, int* pos_i,
                             int* pos_u, const int* len_ptr, int B, cudaStream_t s) {
-  classify_kernel<<<B, 256, 0, s>>>(lse, Nh, mode, tau, scores, cls, ld, out_copy, ld_copy, w, Nkv, ki, vi, ku, vu, wu,
-                                    r_u, S_cap, n_i, n_u, pos_i, pos_u, len_ptr);
+  cudaError_t e = launch_k(classify_kernel, dim3(B), dim3(256), 0, s, g_pdl, lse, Nh, mode, tau, scores, cls, ld,
+                           out_copy, ld_copy, w, Nkv, ki, vi, ku, vu, wu, r_u, S_cap, n_i, n_u, pos_i, pos_u, len_ptr);
   ++g_launches;
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace zdc

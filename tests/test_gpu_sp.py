@@ -102,7 +102,8 @@ def _worker(rank, world, port, layout, S, B, out_q, dataflow="allgather", shape=
 @pytest.mark.parametrize("world,layout,dataflow,shape", [
     (2, 0, "allgather", "mha"), (2, 1, "allgather", "mha"), (4, 1, "allgather", "mha"),
     (2, 0, "ulysses", "mha"), (2, 1, "ulysses", "mha"), (4, 1, "ulysses", "gqa4"),
-    (2, 1, "allgather", "split"), (4, 1, "allgather", "split_mean"), (2, 0, "allgather", "split_mean")])
+    (2, 1, "allgather", "split"), (4, 1, "allgather", "split_mean"), (2, 0, "allgather", "split_mean"),
+    (2, 2, "allgather", "mha"), (4, 2, "allgather", "mha")])   # layout 2: exchange overlapped on a comm stream
 def test_sp_prefill_equals_single_gpu_rows(world, layout, dataflow, shape):
     import multiprocessing as pymp
     import oracle as O
