@@ -349,6 +349,7 @@ class OracleModel:
         self.tau: Dict[int, np.ndarray] = {}              # rep layer -> [B]
         self.scores: Dict[int, np.ndarray] = {}           # rep layer -> [B][len] importance
         self.lse: List[Optional[np.ndarray]] = [None] * L  # last call's [B][Nh][T]
+        self.alive: List[Optional[np.ndarray]] = [None] * L  # eviction (H2O-ZDC): kept cache rows [B][len]
 
     def _rnd(self, a):
         return bf16(a) if self.faithful else a
@@ -359,6 +360,13 @@ class OracleModel:
 
     def _split(self, l):
         return self.plan.g_bp[l] < 10000
+
+    def _evict(self, l):
+        """H2O-ZDC (P:1642 DEL: "first compresses Q, K, and V using SVD and then evicts unimportant
+        tokens"), reading c26: a split group with r^u = 0 evicts its unimportant tokens from the
+        cache instead of truncating them: every query still attends (at r^i) to the prompt it is
+        computed with and to itself, but no later query sees an evicted row."""
+        return self._split(l) and self.plan.r_qk_unimp[l] == 0 and self.plan.r_vl_unimp[l] == 0
 
     def _truncate_rows(self, l, K, V, unimp):
         """Zero-fill (P:774-776 DEL): dims >= r^u of unimportant rows read back as 0.
@@ -380,8 +388,9 @@ class OracleModel:
         V = np.stack([np.stack([x[b] @ w["wv"][g] for g in range(self.dims.n_kv_heads)]) for b in range(x.shape[0])])
         return self._rnd(Q), self._rnd(K), self._rnd(V)
 
-    def _attend(self, q, Kc, Vc, q_pos, row_block=512):
-        """Eqs. 2-3 for the rows of one (b, h): s_tj = q_t.k_j / sqrt(d_h), j <= q_pos[t].
+    def _attend(self, q, Kc, Vc, q_pos, row_block=512, alive=None):
+        """Eqs. 2-3 for the rows of one (b, h): s_tj = q_t.k_j / sqrt(d_h), j <= q_pos[t]
+        (and alive[j] when rows were evicted, reading c26).
         Complete rows per query-row block (no online-softmax tiling).  Returns O [T][r_v], LSE [T]."""
         dh = self.dims.d_head
         T = q.shape[0]
@@ -393,6 +402,8 @@ class OracleModel:
             n_keys = int(np.max(q_pos[r0:r1])) + 1
             s = q[r0:r1] @ Kc[:n_keys].T / math.sqrt(dh)
             visible = np.arange(n_keys)[None, :] <= q_pos[r0:r1, None]   # j <= t_i (Eq. 3)
+            if alive is not None:
+                visible = visible & np.asarray(alive[:n_keys], dtype=bool)[None, :]
             s = np.where(visible, s, -np.inf)
             m = np.max(s, axis=1, keepdims=True)
             e = np.exp(s - m)                           # masked keys -> exactly 0
@@ -425,7 +436,8 @@ class OracleModel:
         if split and rep != l:
             if rep not in self.classes or self.classes[rep].shape[1] < S:
                 raise ValueError("layer %d: representative layer %d has not classified these tokens" % (l, rep))
-            K, V = self._truncate_rows(l, K, V, ~self.classes[rep][:, :S])
+            if not self._evict(l):   # eviction: the prompt attends in full; the cache drops rows below
+                K, V = self._truncate_rows(l, K, V, ~self.classes[rep][:, :S])
         pos = np.arange(S)
         O = np.zeros((B, dims.n_heads, S, V.shape[3]))
         lse = np.zeros((B, dims.n_heads, S))
@@ -441,7 +453,13 @@ class OracleModel:
                 sc[b] = importance(lse[b], pos, plan.importance_mode)
                 cls[b], tau[b], _ = select_important(sc[b], plan.g_bp[l])
             self.classes[l], self.tau[l], self.scores[l] = cls, tau, sc
-            K, V = self._truncate_rows(l, K, V, ~cls)
+            if not self._evict(l):
+                K, V = self._truncate_rows(l, K, V, ~cls)
+        if self._evict(l):   # the cache keeps the important rows only (evicted rows read back as 0)
+            keep = self.classes[rep][:, :S].copy()
+            K = K * keep[:, None, :, None]
+            V = V * keep[:, None, :, None]
+            self.alive[l] = keep
         self.K[l], self.V[l] = self._store(K), self._store(V)   # the prompt attended at full precision
         self.length[l] = S
         return self._output(l, O)
@@ -485,19 +503,23 @@ class OracleModel:
         Q, K, V = self._project(l, x[:, None, :])
         rep = plan.group_rep[l]
         split = self._split(l)
+        evict = self._evict(l)
         if split and rep != l:
             if self.classes[rep].shape[1] <= t:
                 raise ValueError("layer %d: representative %d has not classified position %d" % (l, rep, t))
-            K, V = self._truncate_rows(l, K, V, ~self.classes[rep][:, t:t + 1])
+            if not evict:
+                K, V = self._truncate_rows(l, K, V, ~self.classes[rep][:, t:t + 1])
         self.K[l] = np.concatenate([self.K[l], self._store(K)], axis=2)   # quantized on append (NEXT-4)
         self.V[l] = np.concatenate([self.V[l], self._store(V)], axis=2)
         self.length[l] = t + 1
+        if evict:   # the new token attends to the kept rows and to itself, then may be evicted
+            self.alive[l] = np.concatenate([self.alive[l], np.ones((B, 1), dtype=bool)], axis=1)
         O = np.zeros((B, dims.n_heads, 1, V.shape[3]))
         lse = np.zeros((B, dims.n_heads, 1))
         for b in range(B):
             for h in range(dims.n_heads):
                 O[b, h], lse[b, h] = self._attend(Q[b, h], self.K[l][b, h // G], self.V[l][b, h // G],
-                                                  np.array([t]))
+                                                  np.array([t]), alive=self.alive[l][b] if evict else None)
         self.lse[l] = lse
         if split and rep == l:
             new_cls = np.zeros((B, 1), dtype=bool)
@@ -507,9 +529,15 @@ class OracleModel:
                 new_cls[b, 0] = new_sc[b, 0] > self.tau[l][b]
             self.classes[l] = np.concatenate([self.classes[l], new_cls], axis=1)
             self.scores[l] = np.concatenate([self.scores[l], new_sc], axis=1)
-            Kt, Vt = self._truncate_rows(l, self.K[l][:, :, t:t + 1], self.V[l][:, :, t:t + 1], ~new_cls)
-            self.K[l][:, :, t:t + 1] = Kt
-            self.V[l][:, :, t:t + 1] = Vt
+            if not evict:
+                Kt, Vt = self._truncate_rows(l, self.K[l][:, :, t:t + 1], self.V[l][:, :, t:t + 1], ~new_cls)
+                self.K[l][:, :, t:t + 1] = Kt
+                self.V[l][:, :, t:t + 1] = Vt
+        if evict:   # representative: its own decision above; other layers: the representative's class
+            keep = self.classes[rep][:, t]
+            self.alive[l][:, t] = keep
+            self.K[l][:, :, t] *= keep[:, None, None]
+            self.V[l][:, :, t] *= keep[:, None, None]
         return self._output(l, O)[:, 0, :]
 
     def decode(self, x, l0=0, l1=None):

@@ -46,8 +46,8 @@ MUTANTS = [
     ("non-representative layer truncates important rows",
      "K, V = self._truncate_rows(l, K, V, ~self.classes[rep][:, :S])",
      "K, V = self._truncate_rows(l, K, V, self.classes[rep][:, :S])"),
-    ("decode attends before appending", "self.length[l] = t + 1\n        O = np.zeros",
-     "self.length[l] = t + 1\n        self.K[l], self.V[l] = self.K[l][:, :, :-1], self.V[l][:, :, :-1]\n        O = np.zeros"),
+    ("decode attends before appending", "self.length[l] = t + 1\n        if evict:",
+     "self.length[l] = t + 1\n        self.K[l], self.V[l] = self.K[l][:, :, :-1], self.V[l][:, :, :-1]\n        if evict:"),
     ("Ulysses bytes without all-to-all #2", "return (P - 1) * rows * (cols1 + cols2) * elem_bytes",
      "return (P - 1) * rows * cols1 * elem_bytes"),
     ("k-means ties to the highest index", "assign[r0:r0 + row_block] = np.argmin(d2, axis=1)",
@@ -65,6 +65,12 @@ MUTANTS = [
      "scale = np.where(amax > 0, amax / np.float32(240.0), np.float32(1.0)).astype(np.float32)"),
     ("fp8 cache not quantized on append", "self.K[l] = np.concatenate([self.K[l], self._store(K)], axis=2)",
      "self.K[l] = np.concatenate([self.K[l], K], axis=2)"),
+    ("eviction keeps evicted rows visible", "                visible = visible & np.asarray(alive[:n_keys], dtype=bool)[None, :]",
+     "                visible = visible"),
+    ("eviction truncates before the prompt attention", "            if not self._evict(l):   # eviction: the prompt attends in full; the cache drops rows below",
+     "            if True:"),
+    ("decode token does not attend itself under eviction", "            self.alive[l] = np.concatenate([self.alive[l], np.ones((B, 1), dtype=bool)], axis=1)",
+     "            self.alive[l] = np.concatenate([self.alive[l], np.zeros((B, 1), dtype=bool)], axis=1)"),
     ("SP bytes without (P-1)", "return (P - 1) * (S // P) * B * n_kv * (r_k + r_v) * elem_bytes",
      "return P * (S // P) * B * n_kv * (r_k + r_v) * elem_bytes"),
 ]

@@ -679,3 +679,45 @@ def test_fp8_cache_model_semantics():
         yd, yd8 = m.decode(x[:, t]), m8.decode(x[:, t])
         assert 0 < _rel(yd8, yd) < 0.1
     assert np.array_equal(m8.K[0][:, :, 16:], O.quantize_rows(m.K[0][:, :, 16:]))
+
+
+# ---------------------------------------------------------------- NEXT-4: eviction (H2O-ZDC)
+def test_eviction_semantics_bruteforce():
+    """Reading c26 (H2O-ZDC, P:1642 DEL): with r^u = 0 the prompt attends in full at every layer
+    (prefill rows equal the plain model's exactly), the cache keeps only the important rows, and a
+    decode token attends to the kept prompt rows plus itself -- checked against a scalar-loop
+    attention over exactly that key set (the plain model supplies the un-evicted K', V', Q')."""
+    dims = Dims(2, 32, 4, 2, 16)
+    _, folded = _fold_all(dims, 1, n_calib=128)
+    plan_e = plan_split(2, 12, 0, [[0, 1]], [4000])
+    plan_p = plan_uniform(2, 12)
+    x = Z.prompt(dims, 1, 2, 18)
+    S = 16
+    me, mp = O.OracleModel(dims, plan_e, folded), O.OracleModel(dims, plan_p, folded)
+    for l in range(2):
+        assert np.array_equal(me.prefill_layer(l, x[:, :S]), mp.prefill_layer(l, x[:, :S]))
+    keep = me.classes[0]
+    assert 0 < keep.sum() < keep.size
+    for l in range(2):
+        assert np.all(me.K[l][~np.broadcast_to(keep[:, None, :, None], me.K[l].shape)] == 0.0)
+    ye = [me.decode_layer(l, x[:, S]) for l in range(2)]
+    mp.decode_layer(0, x[:, S])
+    mp.decode_layer(1, x[:, S])
+    dh, G = dims.d_head, dims.group
+    for l in range(2):
+        w = mp.w[l]
+        for b in range(2):
+            q_all = [x[b, S] @ w["wq"][h] for h in range(dims.n_heads)]
+            y = np.zeros(dims.d_model)
+            for h in range(dims.n_heads):
+                g = h // G
+                keys = [j for j in range(S) if keep[b, j]] + [S]   # kept prompt rows + itself
+                s = [float(q_all[h] @ mp.K[l][b, g, j]) / math.sqrt(dh) for j in keys]
+                mx = max(s)
+                e = [math.exp(v - mx) for v in s]
+                o = sum(e[i] * mp.V[l][b, g, keys[i]] for i in range(len(keys))) / sum(e)
+                y += o @ w["wo"][h]
+            assert np.allclose(ye[l][b], y, rtol=0, atol=1e-12 * max(1.0, np.max(np.abs(y))))
+    # the new token's own row is evicted afterwards iff it is unimportant (strict > tau)
+    for l in range(2):
+        assert me.alive[l][:, S].tolist() == me.classes[0][:, S].tolist()
