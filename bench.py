@@ -751,6 +751,18 @@ def fp8_bench(zdc, torch, dev, stream):
                           "achieved_gbs": round((wbytes + kv) / (us / 1e6) / 1e9, 1),
                           "frac": round((wbytes + kv) / (us / 1e6) / 1e9 / peaks["hbm"], 4)}
         out[name] = rec
+    # eviction (H2O-ZDC, reading c26): a c3 group (4 layers, g = 0.5, r^i = 96) with r^u = 32 (token
+    # split) vs r^u = 0 (unimportant tokens evicted), per-key-mean importance (decode tokens ~g important)
+    dims = Z.Dims(4, 5120, 40, 40, 128)
+    rec = {"batch": 32, "prompt": 1024, "g_bp": 5000, "importance": "mean"}
+    for label, ru in (("split_r32", 32), ("evict_r0", 0)):
+        plan = Z.plan_split(4, 96, ru, [[0, 1, 2, 3]], [5000], importance_mode=1)
+        old = zdc.decode_mode("auto")
+        try:
+            rec[label] = {"us_per_layer_step": round(_decode_step_us(zdc, torch, dev, stream, dims, plan, 32, 1024), 2)}
+        finally:
+            zdc.decode_mode(old)
+    out["c3_group_eviction"] = rec
     torch.cuda.empty_cache()
     return out
 

@@ -136,11 +136,15 @@ zdc_status zdc_ctx_create(const zdc_dims* dims, const zdc_plan* plan, int32_t ma
     L.rvu = plan->r_vl_unimp[l];
     L.g_bp = plan->g_bp[l];
     L.rep = plan->group_rep[l];
-    if (L.rku < 1 || L.rku > L.rk || L.rk > d.d_head || L.rvu < 1 || L.rvu > L.rv || L.rv > d.d_head) {
+    // r_unimp = 0 (both pairs) in a split group = eviction of the unimportant tokens (H2O-ZDC, reading c26)
+    const bool evict0 = L.rku == 0 && L.rvu == 0 && plan->g_bp[l] < 10000;
+    if ((L.rku < 1 && !evict0) || L.rku > L.rk || L.rk < 1 || L.rk > d.d_head || (L.rvu < 1 && !evict0) ||
+        L.rvu > L.rv || L.rv < 1 || L.rv > d.d_head) {
       delete c;
-      return fail(ZDC_ERR_SHAPE, "layer %d: ranks must satisfy 1 <= r_unimp <= r_imp <= d_head (qk %d/%d vl %d/%d)",
-                  l, L.rk, L.rku, L.rv, L.rvu);
+      return fail(ZDC_ERR_SHAPE, "layer %d: ranks must satisfy 1 <= r_unimp <= r_imp <= d_head, or r_unimp = 0 in a "
+                  "split group (eviction) (qk %d/%d vl %d/%d)", l, L.rk, L.rku, L.rv, L.rvu);
     }
+    L.evict = evict0;
     if (L.g_bp < 0 || L.g_bp > 10000 || L.rep < 0 || L.rep > l || plan->group_rep[L.rep] != L.rep) {
       delete c;
       return fail(ZDC_ERR_INVALID_ARG, "layer %d: g_bp %d / group_rep %d invalid", l, L.g_bp, L.rep);
@@ -477,9 +481,10 @@ zdc_status zdc_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x, ui
     const LayerInfo& R = c->layers[L.rep];
     uint8_t* rep_cls = reinterpret_cast<uint8_t*>(c->cache + R.cls_off);
     g_prof_class = kProfOther;
-    if (L.split && !is_rep) {
+    if (L.split && !is_rep && !L.evict) {
       // non-representative layer: the group's classes are known; unimportant key/value rows lose
-      // dims >= r^u BEFORE attention (P:774-776 DEL; reading c13)
+      // dims >= r^u BEFORE attention (P:774-776 DEL; reading c13).  (Eviction: the prompt
+      // attends in full; the pack below keeps the important rows only, reading c26.)
       ZDC_CUDA_TRY(launch_truncate(ks, L.rk_p, L.rku, B, Nkv, S, c->max_seq, rep_cls, c->max_seq, s));
       ZDC_CUDA_TRY(launch_truncate(vs, L.rv_p, L.rvu, B, Nkv, S, c->max_seq, rep_cls, c->max_seq, s));
     }
@@ -699,8 +704,8 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
                                  reinterpret_cast<int*>(c->cache + L.ni_off), reinterpret_cast<int*>(c->cache + L.nu_off),
                                  reinterpret_cast<int*>(c->cache + L.posi_off),
                                  reinterpret_cast<int*>(c->cache + L.posu_off), c->max_seq, len_dev,
-                                 reinterpret_cast<const uint8_t*>(c->cache + R.cls_off), c->max_seq, is_rep ? 1 : 0, B,
-                                 s));
+                                 reinterpret_cast<const uint8_t*>(c->cache + R.cls_off), c->max_seq,
+                                 is_rep || L.evict ? 1 : 0, B, s));  // eviction: attend first, evict after
     }
     // a3: split-K attention over the *len_dev + 1 cached keys (two pools with a token split)
     DecodeAttnArgs a;
@@ -747,10 +752,12 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
       a.len_ptr = nullptr;
       a.n0_ptr = reinterpret_cast<const int*>(c->cache + L.ni_off);
       a.n1_ptr = reinterpret_cast<const int*>(c->cache + L.nu_off);
-      a.k1 = reinterpret_cast<const uint16_t*>(c->cache + L.ku_off);
-      a.v1 = reinterpret_cast<const uint16_t*>(c->cache + L.vu_off);
-      a.rk1 = L.rku_p;
-      a.rv1 = L.rvu_p;
+      if (!L.evict) {  // evicted rows are never attended (no pool_U)
+        a.k1 = reinterpret_cast<const uint16_t*>(c->cache + L.ku_off);
+        a.v1 = reinterpret_cast<const uint16_t*>(c->cache + L.vu_off);
+        a.rk1 = L.rku_p;
+        a.rv1 = L.rvu_p;
+      }
     }
     static const bool attn_tc_on = knob("ZDC_DEC_ATTN_TC", 1) != 0;
     cudaError_t ea = cudaErrorNotSupported;
@@ -770,6 +777,12 @@ static zdc_status enqueue_decode(zdc_ctx* c, int l0, int l1, const uint16_t* x, 
       if (ea == cudaErrorNotSupported) cudaGetLastError();
     }
     if (ea != cudaSuccess) ZDC_CUDA_TRY(launch_decode_attention(a, s));
+    if (L.evict && !is_rep) {  // the token attended itself; evict it now if its group classed it unimportant
+      g_prof_class = kProfOther;
+      ZDC_CUDA_TRY(launch_evict_last(reinterpret_cast<const uint8_t*>(c->cache + R.cls_off), c->max_seq,
+                                     reinterpret_cast<int*>(c->cache + L.ni_off), reinterpret_cast<int*>(c->cache + L.nu_off),
+                                     reinterpret_cast<int*>(c->cache + L.posu_off), c->max_seq, len_dev, c->max_seq, B, s));
+    }
     if (L.split && is_rep) {
       g_prof_class = kProfOther;
       ZDC_CUDA_TRY(launch_classify(a.lse, Nh, c->importance_mode, reinterpret_cast<const float*>(c->cache + L.tau_off),

@@ -245,6 +245,7 @@ zdc_status zdc_sp_prefill(zdc_ctx* c, int32_t l0, int32_t l1, const uint16_t* x,
     const LayerInfo& L = c->layers[l];
     if (layout == 2 && L.split)
       return fail(ZDC_ERR_UNSUPPORTED, "zdc_sp_prefill: layout 2 (overlapped exchange) with a token split (layer %d)", l);
+    if (L.evict) return fail(ZDC_ERR_UNSUPPORTED, "zdc_sp_prefill: eviction (r_unimp = 0) under SP (layer %d)", l);
     // a layer reusing classes needs its representative classified by an SP prefill of this prompt
     if (L.split && L.rep != l && L.rep < l0 && c->sp_layer[L.rep] != 1)
       return fail(ZDC_ERR_STATE, "zdc_sp_prefill: layer %d: representative %d has not classified this prompt", l, L.rep);

@@ -20,6 +20,7 @@ struct LayerInfo {
   int rk_p = 0, rv_p = 0, rku_p = 0, rvu_p = 0;
   int g_bp = 10000, rep = 0;
   bool split = false;
+  bool evict = false;  // split group with r^u = 0: unimportant tokens are evicted (H2O-ZDC, NEXT-4)
   int nq = 0, nk = 0, nv = 0, n_qkv = 0, ko_p = 0;
   int64_t w_qkv = 0, w_o = 0;                      // byte offsets in the weight region
   int64_t w_od = -1;  // W_O decode copy [Nkv][d][G*r] for the cluster decode kernel (-1: none)

@@ -295,6 +295,10 @@ cudaError_t launch_pack_weights_bf16(const uint16_t* wq, const uint16_t* wk, con
 // ---- a4 selection + class-aware packing (select.cu)
 cudaError_t launch_importance(const float* lse, int T, int Nh, int B, int t0, int mode, float* scores, int64_t ld,
                               float* out_copy, int64_t ld_copy, const int* pos_ptr, cudaStream_t s);
+// eviction (H2O-ZDC, reading c26): after a non-representative layer's decode attention, the new token
+// (the last pool_I row) leaves pool_I when its representative classed it unimportant
+cudaError_t launch_evict_last(const uint8_t* cls, int64_t ld_cls, int* n_i, int* n_u, int* pos_u, int64_t ld_pos,
+                              const int* len_ptr, int S_cap, int B, cudaStream_t s);
 cudaError_t launch_select(const float* scores, int64_t ld, int S, int g_bp, int B, uint8_t* cls, float* tau,
                           cudaStream_t s, int* nan_flag = nullptr);
 cudaError_t launch_truncate(uint16_t* kv, int width, int r_u, int B, int Nkv, int S, int S_cap, const uint8_t* cls,

@@ -360,4 +360,26 @@ cudaError_t launch_classify(const float* lse, int Nh, int mode, const float* tau
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+__global__ void evict_last_kernel(const uint8_t* __restrict__ cls, int64_t ld_cls, int* __restrict__ n_i,
+                                  int* __restrict__ n_u, int* __restrict__ pos_u, int64_t ld_pos,
+                                  const int* __restrict__ len_ptr, int S_cap) {
+  pdl_wait();
+  pdl_trigger();
+  const int b = blockIdx.x;
+  const int t = *len_ptr;
+  if (threadIdx.x != 0 || t >= S_cap || cls[b * ld_cls + t]) return;
+  const int dst = n_u[b];
+  pos_u[b * ld_pos + dst] = t;  // recorded as evicted (no row is kept)
+  n_i[b] = n_i[b] - 1;
+  n_u[b] = dst + 1;
+}
+
+cudaError_t launch_evict_last(const uint8_t* cls, int64_t ld_cls, int* n_i, int* n_u, int* pos_u, int64_t ld_pos,
+                              const int* len_ptr, int S_cap, int B, cudaStream_t s) {
+  cudaError_t e = launch_k(evict_last_kernel, dim3(B), dim3(32), 0, s, g_pdl, cls, ld_cls, n_i, n_u, pos_u, ld_pos,
+                           len_ptr, S_cap);
+  ++g_launches;
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 }  // namespace zdc
