@@ -162,14 +162,17 @@ def profile(enable: bool):
     lib().zdc_profile(1 if enable else 0)
 
 
-def trace_read(n_cta: int = 148):
-    """Fused decode kernel timeline of its last launch (ZDC_FUSED_TRACE): uint64 [n_cta][16] ns."""
+def trace_read(n_cta: int = 148, launches: int = 16):
+    """Fused decode kernel timelines (ZDC_FUSED_TRACE, diagnostic build): uint64 ns stamps
+    [launches][n_cta][32] of the last `launches` launches, oldest first (unused slots are 0)."""
     import numpy as np
-    buf = (ctypes.c_uint64 * (n_cta * 16))()
-    got = lib().zdc_trace_read(buf, n_cta * 16)
+    per = 1024 * 32
+    buf = (ctypes.c_uint64 * (16 * per))()
+    got = lib().zdc_trace_read(buf, 16 * per)
     if got <= 0:
         return None
-    return np.frombuffer(buf, dtype=np.uint64).reshape(n_cta, 16).copy()
+    a = np.frombuffer(buf, dtype=np.uint64).reshape(16, 1024, 32)[:, :n_cta].copy()
+    return a[16 - launches:]
 
 
 def profile_read():

@@ -1,6 +1,7 @@
 // decode_fused.cu — host dispatch of the fused decode layer-step (kernel: decode_fused.cuh)
 #include "kernels.h"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace zdc {
@@ -23,15 +24,28 @@ bool decode_fused_supported(int B, int RK, int G) {
          (G == 1 || G == 2 || G == 4 || G == 8);
 }
 
-unsigned long long* fused_trace_buffer() {
+// trace ring: kTraceLaunches launches x 1024 CTAs x 32 stamps; fused_trace_buffer() hands out the
+// next launch's slice (diagnostic builds only: ZDC_FUSED_TRACE)
+static constexpr int kTraceLaunches = 16;
+static unsigned long long* trace_base() {
   static unsigned long long* buf = nullptr;
   static bool init = false;
   if (!init) {
     init = true;
-    if (knob("ZDC_FUSED_TRACE", 0) && cudaMalloc(&buf, 1024 * 16 * 8) != cudaSuccess) buf = nullptr;
-    if (buf) cudaMemset(buf, 0, 1024 * 16 * 8);
+    const size_t bytes = static_cast<size_t>(kTraceLaunches) * 1024 * 32 * 8;
+    if (knob("ZDC_FUSED_TRACE", 0) && cudaMalloc(&buf, bytes) != cudaSuccess) buf = nullptr;
+    if (buf) cudaMemset(buf, 0, bytes);
   }
   return buf;
+}
+static int g_trace_next = 0;
+
+unsigned long long* fused_trace_buffer() {
+  unsigned long long* b = trace_base();
+  if (!b) return nullptr;
+  unsigned long long* r = b + static_cast<size_t>(g_trace_next % kTraceLaunches) * 1024 * 32;
+  ++g_trace_next;
+  return r;
 }
 
 cudaError_t launch_decode_fused(const DecFusedArgs& a, int RK, cudaStream_t s) {
@@ -45,11 +59,20 @@ cudaError_t launch_decode_fused(const DecFusedArgs& a, int RK, cudaStream_t s) {
 
 }  // namespace zdc
 
+// copies the trace ring: [kTraceLaunches][1024][32] ns, oldest launch first (n entries at most)
 extern "C" int zdc_trace_read(unsigned long long* out, int n) {
-  unsigned long long* b = zdc::fused_trace_buffer();
+  unsigned long long* b = zdc::trace_base();
   if (!b || !out || n <= 0) return 0;
-  if (n > 1024 * 16) n = 1024 * 16;
+  const int per = 1024 * 32, tot = zdc::kTraceLaunches * per;
+  if (n > tot) n = tot;
   if (cudaDeviceSynchronize() != cudaSuccess) return -1;
-  if (cudaMemcpy(out, b, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
-  return n;
+  const int first = zdc::g_trace_next % zdc::kTraceLaunches;  // oldest slice
+  int done = 0;
+  for (int i = 0; i < zdc::kTraceLaunches && done < n; ++i) {
+    const int sl = (first + i) % zdc::kTraceLaunches, m = std::min(per, n - done);
+    if (cudaMemcpy(out + done, b + static_cast<size_t>(sl) * per, static_cast<size_t>(m) * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+      return -1;
+    done += m;
+  }
+  return done;
 }

@@ -48,10 +48,18 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 // polls with ld.acquire until the counter reaches `target` = base + k * n for the k-th barrier of
 // this launch, where base (a multiple of n) is read after the PDL wait (every earlier launch has
 // completed, and no CTA of this launch can have passed barrier 1 yet).  No reset is needed.
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// The poll spins on relaxed loads and acquires once at the end: ld.acquire compiles to a strong
+// load + CCTL.IVALL (an L1 invalidate), which in a spin loop would run once per iteration.
 __device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned long long target) {
   asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
-  while (ld_acquire_u64(bar) < target) {
+  while (ld_relaxed_u64(bar) < target) {
   }
+  (void)ld_acquire_u64(bar);
 }
 
 __device__ __forceinline__ int atomic_add_acq_rel(int* p, int v) {
@@ -67,7 +75,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 #define ZDC_STAMP(i)                                                        \
   do {                                                                      \
-    if (a.trace) a.trace[static_cast<int64_t>(blockIdx.x) * 16 + (i)] = globaltimer(); \
+    if (a.trace) a.trace[static_cast<int64_t>(blockIdx.x) * 32 + (i)] = globaltimer(); \
   } while (0)
 
 // consumer warps per CTA (one more warp is the producer)

@@ -29,6 +29,7 @@ def main():
     p.add_argument("--ctx", type=int, default=2048)
     p.add_argument("--batch", type=int, default=1)
     p.add_argument("--steps", type=int, default=8)
+    p.add_argument("--show", type=int, default=4, help="launches to print (the last ones)")
     p.add_argument("--chain", action="store_true", help="one chained zdc_decode call per step")
     p.add_argument("--mode", default="auto", help="zdc_decode_mode: auto / fused / cluster / separate")
     args = p.parse_args()
@@ -60,20 +61,24 @@ def main():
             for l in range(L):
                 ctx.decode(xb, yb, l, l + 1)
     s.synchronize()
-    tr = zdc.trace_read(148)
+    nshow = min(args.show, args.layers * args.steps)
+    tr = zdc.trace_read(148, nshow)
     if tr is None:
         print("tracing off (set ZDC_FUSED_TRACE=1)")
         return
     tr = tr.astype(np.int64)
-    t0 = tr[:, 0][tr[:, 0] > 0].min()
-    print("%-18s %9s %9s %9s  (us after first CTA start)" % ("stamp", "min", "median", "max"))
-    for i in NAMES:
-        v = tr[:, i]
-        v = v[v > 0]
-        if len(v) == 0:
-            continue
-        v = (v - t0) / 1e3
-        print("%-18s %9.2f %9.2f %9.2f" % (NAMES[i], v.min(), np.median(v), v.max()))
+    t0 = tr[0, :, 0][tr[0, :, 0] > 0].min()
+    print("last %d launches, us after the first CTA start of the first one shown" % nshow)
+    print("%-28s %9s %9s %9s" % ("stamp", "min", "median", "max"))
+    for k in range(nshow):
+        print("-- launch %d" % k)
+        for i in NAMES:
+            v = tr[k, :, i]
+            v = v[v > 0]
+            if len(v) == 0:
+                continue
+            v = (v - t0) / 1e3
+            print("%-28s %9.2f %9.2f %9.2f" % (NAMES[i], v.min(), np.median(v), v.max()))
 
 
 if __name__ == "__main__":
