@@ -584,7 +584,14 @@ static cudaError_t launch_partial(const DecodeAttnArgs& a, int width, const uint
 static const bool g_dec_attn_v2 = knob("ZDC_DEC_ATTN_V2", 1) != 0;
 static bool v2_width(int w) { return w == 32 || w == 64 || w == 96 || w == 128; }
 
+static const bool g_dec_attn_v3 = knob("ZDC_DEC_ATTN_V3", 1) != 0;
 cudaError_t launch_decode_attention(const DecodeAttnArgs& a_in, cudaStream_t stream) {
+  // v3 (decode_attn3.cu): the byte-balanced flat split, both pools in one launch
+  if (g_dec_attn_v3 && decode3_supported(a_in)) {
+    const cudaError_t e3 = launch_decode_attention3(a_in, stream);
+    if (e3 != cudaErrorNotSupported) return e3;
+    cudaGetLastError();  // shape outside v3's shared-memory budget: v2 below
+  }
   if (g_dec_attn_v2 && v2_width(a_in.rk) && (!a_in.k1 || v2_width(a_in.rk1)) && a_in.rk == a_in.rv &&
       (!a_in.k1 || a_in.rk1 == a_in.rv1) && a_in.counters) {
     // v2 (decode_attn2.cu): 8-warp CTAs, per-warp pipelined tiles; its own split count

@@ -1,0 +1,488 @@
+// decode_attn3.cu — a3 for token generation over the compressed cache, v3: byte-balanced flat
+// split (s_tj = Q'_t . K'_j / sqrt(d_h), P = softmax(s), O'_t = sum_j P_tj V'_j,
+// P:249-260 Eqs. 2-3; with a token split, unimportant keys carry only their first r^u dims and the
+// rest read as zero, P:776 DEL / P:1442).
+//
+// Why: v2 (decode_attn2.cu) gives every (split, KV head, sequence) its own CTA.  At c3 (B = 32,
+// 40 KV heads, two pools) that is 1280 + 1280 CTAs over 296 resident slots: 4.3 waves per pool,
+// each CTA paying a pipeline ramp and a merge, and the last wave a third full.  Here the
+// work is ONE list -- for each (sequence b, KV head g) pair its pool-0 rows, then its pool-1 rows
+// -- and each of the W resident warps of the grid takes an equal share of its BYTES (row cost
+// r + r for K'+V'), so every warp streams the same amount, across pair and pool boundaries,
+// through its own ring of bulk copies without a wave tail.  A warp's share covers ~1-3 pairs; a
+// pair covered by several warps is merged by the last of them (LSE merge of the pieces).
+//
+// Per warp: a 2-stage ring of 32-row tiles {K' rows, V' rows, q of the pair}; lane 0 issues the
+// tile two ahead; lane j scores row j for the G query heads of the group; online softmax in the
+// log2 domain; P rounded to bf16 before PV, l from the unrounded P (DESIGN.md §4.3 rounding
+// points); lane owns output columns lane + 32 i.
+#include "common.cuh"
+#include "kernels.h"
+
+#include <algorithm>
+
+namespace zdc {
+
+namespace {
+
+constexpr int kW3 = 8;     // warps per CTA (one CTA per SM)
+constexpr int kTR3 = 32;   // rows per tile
+constexpr int kMaxP3 = 128;  // pieces per pair (partial slots per head)
+constexpr float kLog2e3 = 1.4426950408889634f;
+
+template <int RK, int G>
+struct DA3 {
+  static constexpr uint32_t KT = kTR3 * RK * 2;           // one K' (or V') tile of pool 0
+  static constexpr uint32_t QB = G * RK * 2;              // q of the pair's G heads (bf16)
+  static constexpr uint32_t STAGE = (2 * KT + QB + 127) / 128 * 128;
+  static constexpr int NST = 2;
+  static constexpr uint32_t WARP_BYTES = NST * STAGE;
+};
+
+__device__ __forceinline__ int64_t cdiv64(int64_t a, int64_t b) { return a <= 0 ? 0 : (a + b - 1) / b; }
+// d += A . B, m16n8k16, bf16 inputs, f32 accumulators (legacy warp MMA: this kernel is HBM-bound,
+// the tensor cores only take the dot products off the issue slots)
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+               "{%0, %1, %2, %3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
+
+// One warp's walk over its tiles: pairs p = b * Nkv + g in order; in a pair, pool-0 rows then
+// pool-1 rows; only the rows whose cost start lies in [lo, hi).
+struct Walk {
+  int64_t lo, hi;
+  int p, pool, r, r_end;  // current pair / pool / next row / end row of this pool in the range
+  bool done;
+};
+
+}  // namespace
+
+template <int RK, int G>
+__global__ void __launch_bounds__(kW3 * 32, 1) decode_attn3_kernel(const DecodeAttnArgs a, int w_launch) {
+  using C = DA3<RK, G>;
+  extern __shared__ __align__(128) uint8_t dsm[];
+  __shared__ int64_t s_pb[129];  // cost prefix over sequences (B <= 128)
+  __shared__ int s_n0[128], s_n1[128];
+  __shared__ int64_t s_weff;
+  __shared__ uint64_t bars[kW3][C::NST];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * kW3 + warp;
+  uint8_t* ring = dsm + warp * C::WARP_BYTES;
+  uint64_t* wbar = bars[warp];
+  if (lane == 0) {
+    for (int s = 0; s < C::NST; ++s) mbar_init(&wbar[s], 1);
+    fence_barrier_init();
+  }
+  pdl_trigger();
+  pdl_wait();  // the row counts (and the new rows) come from the predecessor
+
+  const int B = a.B, Nkv = a.Nkv, rk1 = a.k1 ? a.rk1 : 0;
+  const int64_t w0 = RK, w1 = rk1;  // cost of one row of each pool (K' + V' bytes / 4)
+  if (threadIdx.x < 32) {
+    // per-sequence row counts and the cost prefix (one warp; B <= 128)
+    int64_t run = 0, cmax = 0;
+    for (int b0 = 0; b0 < B; b0 += 32) {
+      const int b = b0 + lane;
+      int n0 = 0, n1 = 0;
+      if (b < B) {
+        if (a.n0_ptr) {
+          n0 = a.n0_ptr[b];
+          n1 = a.k1 ? a.n1_ptr[b] : 0;
+        } else {
+          n0 = a.len_ptr ? min(*a.len_ptr + 1, a.S_cap) : a.len;
+        }
+        s_n0[b] = n0;
+        s_n1[b] = n1;
+      }
+      const int64_t cb = static_cast<int64_t>(n0) * w0 + static_cast<int64_t>(n1) * w1;
+      int64_t x = cb;  // inclusive scan over the lanes
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+      }
+      if (b < B) s_pb[b + 1] = run + x;
+      run += __shfl_sync(0xffffffffu, x, 31);
+      int64_t m = cb;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) m = max64(m, __shfl_xor_sync(0xffffffffu, m, off));
+      cmax = max64(cmax, m);
+    }
+    if (lane == 0) {
+      s_pb[0] = 0;
+      // effective warp count: every warp range must hold a row start of each pair it crosses
+      // (rows are at most max(w0, w1) apart) and no pair may need more than kMaxP3 pieces
+      const int64_t total = run * Nkv;
+      int64_t weff = w_launch;
+      if (total > 0) {
+        weff = min64(weff, total / max64(w0, w1));
+        if (cmax > 0) weff = min64(weff, (kMaxP3 - 2) * total / cmax);
+      }
+      s_weff = max64(weff, 1);
+    }
+  }
+  __syncthreads();
+  const int64_t total = s_pb[B] * Nkv;
+  const int64_t W = s_weff;
+  if (gw >= W || total <= 0) return;
+
+  auto pair_base = [&](int p) {  // cost of the pair's first row
+    const int b = p / Nkv, g = p - b * Nkv;
+    const int64_t cb = s_pb[b + 1] - s_pb[b];
+    return s_pb[b] * Nkv + g * cb;
+  };
+  auto warp_of = [&](int64_t x) { return static_cast<int>((x * W) / total); };
+  // the walk's pool ranges for pair p (false when this warp owns no row of it)
+  auto enter_pair = [&](Walk& k) -> bool {
+    const int b = k.p / Nkv;
+    const int64_t P = pair_base(k.p);
+    const int n0 = s_n0[b], n1 = s_n1[b];
+    const int i0 = static_cast<int>(min64(n0, cdiv64(k.lo - P, w0)));
+    const int i1 = static_cast<int>(min64(n0, cdiv64(k.hi - P, w0)));
+    if (i1 > i0) {
+      k.pool = 0;
+      k.r = i0;
+      k.r_end = i1;
+      return true;
+    }
+    if (n1 > 0 && w1 > 0) {
+      const int64_t P1 = P + static_cast<int64_t>(n0) * w0;
+      const int j0 = static_cast<int>(min64(n1, cdiv64(k.lo - P1, w1)));
+      const int j1 = static_cast<int>(min64(n1, cdiv64(k.hi - P1, w1)));
+      if (j1 > j0) {
+        k.pool = 1;
+        k.r = j0;
+        k.r_end = j1;
+        return true;
+      }
+    }
+    return false;
+  };
+  auto start_walk = [&](Walk& k) {
+    k.lo = cdiv64(static_cast<int64_t>(gw) * total, W);
+    k.hi = cdiv64(static_cast<int64_t>(gw + 1) * total, W);
+    k.done = false;
+    // the pair holding cost lo: the last sequence b with prefix <= lo, then g
+    int lo_b = 0, hi_b = B - 1;
+    while (lo_b < hi_b) {
+      const int mid = (lo_b + hi_b + 1) >> 1;
+      if (s_pb[mid] * Nkv <= k.lo) lo_b = mid; else hi_b = mid - 1;
+    }
+    const int64_t cb = s_pb[lo_b + 1] - s_pb[lo_b];
+    int g = cb > 0 ? static_cast<int>((k.lo - s_pb[lo_b] * Nkv) / cb) : 0;
+    if (g >= Nkv) g = Nkv - 1;
+    k.p = lo_b * Nkv + g;
+    while (k.p < B * Nkv && pair_base(k.p) < k.hi) {
+      if (enter_pair(k)) return;
+      ++k.p;
+    }
+    k.done = true;
+  };
+  // move to the next tile's start: rest of this pool, the pool-1 rows, the next pairs
+  auto advance = [&](Walk& k, int nr) {
+    k.r += nr;
+    if (k.r < k.r_end) return;
+    const int b = k.p / Nkv;
+    if (k.pool == 0 && s_n1[b] > 0 && w1 > 0) {
+      const int64_t P1 = pair_base(k.p) + static_cast<int64_t>(s_n0[b]) * w0;
+      const int n1 = s_n1[b];
+      const int j0 = static_cast<int>(min64(n1, cdiv64(k.lo - P1, w1)));
+      const int j1 = static_cast<int>(min64(n1, cdiv64(k.hi - P1, w1)));
+      if (j1 > j0) {
+        k.pool = 1;
+        k.r = j0;
+        k.r_end = j1;
+        return;
+      }
+    }
+    for (++k.p; k.p < B * Nkv && pair_base(k.p) < k.hi; ++k.p)
+      if (enter_pair(k)) return;
+    k.done = true;
+  };
+
+  const float scl = a.scale * kLog2e3;
+  // rows per tile: 32 of pool 0; as many 32-row passes of the narrower pool 1 as fill the same
+  // bytes (c3: 96 rows of r^u = 32), so the bytes in flight per warp stay the same in both pools
+  const int tr1 = rk1 > 0 ? kTR3 * max(1, RK / rk1) : kTR3;
+  auto tile_rows = [&](const Walk& k) { return min(k.pool == 0 ? kTR3 : tr1, k.r_end - k.r); };
+  // issue side (lane 0): the tile at walk ki into stage st
+  auto issue = [&](const Walk& k, int st) {
+    const int b = k.p / Nkv, g = k.p - b * Nkv;
+    const int nr = tile_rows(k);
+    const int width = k.pool == 0 ? RK : rk1;
+    const uint16_t* kp = k.pool == 0 ? a.k : a.k1;
+    const uint16_t* vp = k.pool == 0 ? a.v : a.v1;
+    const int64_t row = (static_cast<int64_t>(b) * Nkv + g) * a.S_cap + k.r;
+    const uint32_t rb = static_cast<uint32_t>(nr) * width * 2u;
+    uint8_t* dst = ring + st * C::STAGE;
+    mbar_arrive_expect_tx(&wbar[st], 2 * rb + C::QB);
+    bulk_g2s(dst, kp + row * width, rb, &wbar[st]);
+    bulk_g2s(dst + C::KT, vp + row * width, rb, &wbar[st]);
+    bulk_g2s(dst + 2 * C::KT, a.q + b * a.ldq + static_cast<int64_t>(g) * G * a.rk, C::QB, &wbar[st]);
+  };
+
+  Walk wi, wc;  // issue-side and compute-side walks
+  start_walk(wi);
+  wc = wi;
+  if (wi.done) return;
+  if (lane == 0)
+    for (int s = 0; s < C::NST && !wi.done; ++s) {
+      issue(wi, s);
+      advance(wi, tile_rows(wi));
+    }
+
+  // ---- tensor-core formulation (mma.sync m16n8k16, bf16 in, f32 accumulate), queries on M:
+  //   S^T[16 (G heads, rest zero)][8 keys] = Q[16][16 k] . K'^T[16 k][8 keys]   per n-tile, k-step
+  //   O  [16][8 cols]               += P[16][16 keys] . V'[16 keys][8 cols]
+  // lane = 4 g + t holds row g (head g < G) of every accumulator: columns 2t, 2t+1 of each 8-wide
+  // n-tile; the S accumulators of two key n-tiles, rounded to bf16, are the P fragment of one PV
+  // k-step.  K' / V' fragments come straight from the row-major tiles with ldmatrix (V' transposed).
+  constexpr int KS = RK / 16;   // k-steps of a pool-0 row
+  constexpr int NT = RK / 8;    // output n-tiles
+  const int g = lane >> 2, tq = lane & 3;
+  float m = -INFINITY, l = 0.f;  // running max (log2 domain) / sum of row g
+  float oacc[NT][4];
+  uint32_t qa[KS][2];           // q fragments of the current piece (rows g < G; rows g + 8 are zero)
+  auto reset = [&]() {
+    m = -INFINITY;
+    l = 0.f;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
+  };
+  reset();
+  bool new_piece = true;
+  const int RVO = a.rv;
+  const uint32_t ring_s = smem_u32(ring);
+  for (int t = 0; !wc.done; ++t) {
+    const int st = t % C::NST;
+    mbar_wait(&wbar[st], (t / C::NST) & 1);
+    const int p = wc.p, pool = wc.pool, nr = tile_rows(wc);
+    const int width = pool == 0 ? RK : rk1;
+    const int ks_n = width >> 4, nt_n = width >> 3;
+    if (new_piece) {  // q of this pair (bf16 in the stage) -> A fragments
+      const uint16_t* Qt = reinterpret_cast<const uint16_t*>(ring + st * C::STAGE + 2 * C::KT);
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        qa[ks][0] = g < G ? *reinterpret_cast<const uint32_t*>(Qt + g * RK + ks * 16 + 2 * tq) : 0u;
+        qa[ks][1] = g < G ? *reinterpret_cast<const uint32_t*>(Qt + g * RK + ks * 16 + 8 + 2 * tq) : 0u;
+      }
+      new_piece = false;
+    }
+    for (int j0 = 0; j0 < nr; j0 += kTR3) {  // 32-key passes
+      const int np = min(kTR3, nr - j0);
+      const uint32_t kb = ring_s + st * C::STAGE + static_cast<uint32_t>(j0 * width * 2);
+      const uint32_t vb = kb + C::KT;
+      if (np < kTR3) {
+        // rows np.. of the stage hold stale bytes: zero those V' rows (P is 0 there, 0 * NaN is not)
+        uint16_t* Vz = reinterpret_cast<uint16_t*>(ring + st * C::STAGE + C::KT) + j0 * width;
+        for (int i = np * width + lane * 8; i < kTR3 * width; i += 256)
+          *reinterpret_cast<uint4*>(Vz + i) = make_uint4(0, 0, 0, 0);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before the stage's next bulk copy
+        __syncwarp();
+      }
+      // ---- scores: 4 n-tiles of 8 keys
+      float sacc[4][4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) sacc[j][0] = sacc[j][1] = sacc[j][2] = sacc[j][3] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        if (ks < ks_n) {
+#pragma unroll
+          for (int jp = 0; jp < 2; ++jp) {  // n-tiles 2jp, 2jp + 1
+            const int row = 8 * (2 * jp + (lane >> 4)) + (lane & 7);
+            const int col = ks * 16 + ((lane >> 3) & 1) * 8;
+            uint32_t b0, b1, b2, b3;
+            asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
+                         : "r"(kb + static_cast<uint32_t>((row * width + col) * 2)));
+            mma_bf16_16816(sacc[2 * jp], qa[ks][0], 0u, qa[ks][1], 0u, b0, b1);
+            mma_bf16_16816(sacc[2 * jp + 1], qa[ks][0], 0u, qa[ks][1], 0u, b2, b3);
+          }
+        }
+      }
+      // ---- online softmax of row g over the 32 keys (4 lanes per row), log2 domain
+      float x[4][2];
+      float tm = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int key = 8 * j + 2 * tq + e;
+          x[j][e] = key < np ? sacc[j][e] * scl : -INFINITY;
+          tm = fmaxf(tm, x[j][e]);
+        }
+      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 1));
+      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 2));
+      const float mn = fmaxf(m, tm);
+      const float alpha = exp2f(m - mn);  // 0 on the first pass of a piece
+      float ps = 0.f;
+      uint32_t pa[2][2];  // P fragments of the two 16-key k-steps (row g; rows g + 8 zero)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float p0 = exp2f(x[j][0] - mn), p1 = exp2f(x[j][1] - mn);
+        ps += p0 + p1;
+        pa[j >> 1][j & 1] = pack_bf16x2(p0, p1);  // P rounded to bf16 before PV (l from unrounded P)
+      }
+      ps += __shfl_xor_sync(0xffffffffu, ps, 1);
+      ps += __shfl_xor_sync(0xffffffffu, ps, 2);
+      l = l * alpha + ps;
+      m = mn;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        oacc[j][0] *= alpha;
+        oacc[j][1] *= alpha;
+      }
+      // ---- PV: O[.][cols] += P[.][keys] V'[keys][cols], V' fragments by transposed ldmatrix
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+#pragma unroll
+        for (int jn = 0; jn < NT; jn += 2) {  // output n-tiles jn, jn + 1 (16 columns)
+          if (jn < nt_n) {
+            const int row = kk * 16 + (lane & 15);
+            const int col = jn * 8 + (lane >> 4) * 8;
+            uint32_t b0, b1, b2, b3;
+            asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
+                         : "r"(vb + static_cast<uint32_t>((row * width + col) * 2)));
+            mma_bf16_16816(oacc[jn], pa[kk][0], 0u, pa[kk][1], 0u, b0, b1);
+            mma_bf16_16816(oacc[jn + 1], pa[kk][0], 0u, pa[kk][1], 0u, b2, b3);
+          }
+        }
+      }
+      __syncwarp();
+    }
+    // refill this stage with the tile NST ahead
+    if (lane == 0 && !wi.done) {
+      issue(wi, st);
+      advance(wi, tile_rows(wi));
+    }
+    advance(wc, nr);
+    if (!wc.done && wc.p == p) continue;  // the piece of this pair goes on
+    // ---- end of this warp's piece of pair p (row g = head g < G of the group)
+    const int b = p / Nkv, gg = p - b * Nkv;
+    const int64_t P = pair_base(p);
+    const int n0 = s_n0[b], n1 = s_n1[b];
+    const int64_t last = n1 > 0 && w1 > 0 ? P + static_cast<int64_t>(n0) * w0 + static_cast<int64_t>(n1 - 1) * w1
+                                          : P + static_cast<int64_t>(n0 - 1) * w0;
+    const int wf = warp_of(P), wl = warp_of(last);
+    const int pieces = wl - wf + 1;
+    if (pieces == 1) {  // the whole pair: O' and LSE directly
+      if (g < G) {
+        const float inv = 1.f / l;
+        uint16_t* orow = a.o + b * a.ldo + (gg * G + g) * RVO;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const int col = 8 * j + 2 * tq;
+          if (col < RVO) *reinterpret_cast<uint32_t*>(orow + col) = pack_bf16x2(oacc[j][0] * inv, oacc[j][1] * inv);
+        }
+        if (tq == 0 && a.lse) a.lse[b * a.Nh + gg * G + g] = (m + log2f(l)) / kLog2e3;
+      }
+    } else {
+      const int piece = gw - wf;
+      if (g < G) {
+        float* dst = a.part + ((static_cast<int64_t>(b) * a.Nh + gg * G + g) * kMaxP3 + piece) * (RVO + 2);
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const int col = 8 * j + 2 * tq;
+          if (col < RVO) *reinterpret_cast<float2*>(dst + col) = make_float2(oacc[j][0], oacc[j][1]);
+        }
+        if (tq == 0) {
+          dst[RVO] = m;
+          dst[RVO + 1] = l;
+        }
+      }
+      __syncwarp();
+      int lastw = 0;
+      if (lane == 0) {
+        __threadfence();
+        lastw = atomicAdd(&a.counters[p], 1) == pieces - 1;
+      }
+      lastw = __shfl_sync(0xffffffffu, lastw, 0);
+      if (lastw) {
+        __threadfence();
+        for (int gi = 0; gi < G; ++gi) {
+          const float* hp = a.part + (static_cast<int64_t>(b) * a.Nh + gg * G + gi) * kMaxP3 * (RVO + 2);
+          float M = -INFINITY;
+          for (int q = 0; q < pieces; ++q) M = fmaxf(M, __ldcg(hp + q * (RVO + 2) + RVO));
+          for (int col = lane; col < RVO; col += 32) {
+            float L = 0.f, O = 0.f;
+            for (int q = 0; q < pieces; ++q) {
+              const float ms = __ldcg(hp + q * (RVO + 2) + RVO);
+              const float f = ms == -INFINITY ? 0.f : exp2f(ms - M);
+              L = fmaf(f, __ldcg(hp + q * (RVO + 2) + RVO + 1), L);
+              O = fmaf(f, __ldcg(hp + q * (RVO + 2) + col), O);
+            }
+            a.o[b * a.ldo + (gg * G + gi) * RVO + col] = f32_to_bf16_bits(O / L);
+            if (col == 0 && a.lse) a.lse[b * a.Nh + gg * G + gi] = (M + log2f(L)) / kLog2e3;
+          }
+        }
+        if (lane == 0) a.counters[p] = 0;
+      }
+    }
+    reset();
+    new_piece = true;
+  }
+}
+
+// ------------------------------------------------------------------ host
+template <int RK, int G>
+static cudaError_t launch3_t(const DecodeAttnArgs& a, cudaStream_t stream) {
+  using C = DA3<RK, G>;
+  const size_t smem = static_cast<size_t>(kW3) * C::WARP_BYTES;
+  if (smem > 220 * 1024) return cudaErrorNotSupported;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(decode_attn3_kernel<RK, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  // as many warps as fit one per SM, but no more than 64 per (sequence, KV head) pair
+  const int pairs = a.B * a.Nkv;
+  int grid = num_sms();
+  const int64_t wmax = static_cast<int64_t>(pairs) * 64;
+  if (static_cast<int64_t>(grid) * kW3 > wmax) grid = static_cast<int>((wmax + kW3 - 1) / kW3);
+  prof_mark(stream, true, kProfAttnDecode);
+  cudaError_t e = launch_k(decode_attn3_kernel<RK, G>, dim3(grid), dim3(kW3 * 32), smem, stream, g_pdl, a, grid * kW3);
+  prof_mark(stream, false, kProfAttnDecode);
+  ++g_launches;
+  return e;
+}
+
+template <int RK>
+static cudaError_t launch3_g(const DecodeAttnArgs& a, cudaStream_t s) {
+  switch (a.Nh / a.Nkv) {
+    case 1: return launch3_t<RK, 1>(a, s);
+    case 2: return launch3_t<RK, 2>(a, s);
+    case 4: return launch3_t<RK, 4>(a, s);
+    case 8: return launch3_t<RK, 8>(a, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+bool decode3_supported(const DecodeAttnArgs& a) {
+  const int G = a.Nkv > 0 ? a.Nh / a.Nkv : 0;
+  if (a.kv_fp8 || !a.counters || !a.part || a.B < 1 || a.B > 128) return false;
+  if (G != 1 && G != 2 && G != 4 && G != 8) return false;
+  if (a.rk != a.rv || (a.rk != 32 && a.rk != 64 && a.rk != 96)) return false;  // 2 x 8 warps x 2 stages fit
+  if (a.k1 && (a.rk1 != a.rv1 || a.rk1 % 8 != 0 || a.rk1 < 8 || a.rk1 > a.rk)) return false;
+  if (a.ldq % 8 != 0) return false;
+  return true;
+}
+
+cudaError_t launch_decode_attention3(const DecodeAttnArgs& a, cudaStream_t s) {
+  if (!decode3_supported(a)) return cudaErrorNotSupported;
+  switch (a.rk) {
+    case 32: return launch3_g<32>(a, s);
+    case 64: return launch3_g<64>(a, s);
+    case 96: return launch3_g<96>(a, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+}  // namespace zdc

@@ -190,6 +190,10 @@ struct DecodeAttnArgs {
   int splits = 1;
 };
 cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t stream);
+// v3 (decode_attn3.cu): byte-balanced flat split of every (sequence, KV head) pair's pool-0 and
+// pool-1 rows over one resident warp set; partials [B][Nh][128][rv+2], counters [B][Nkv]
+bool decode3_supported(const DecodeAttnArgs& a);
+cudaError_t launch_decode_attention3(const DecodeAttnArgs& a, cudaStream_t stream);
 // tcgen05 decode attention for grouped-query layers (decode_attn_tc.cu): uniform rank r in
 // {64, 128}, G in {2, 4, 8, 16}, device-side length (len_ptr); a.splits from decode_tc_splits
 bool decode_attention_tc_supported(int rk, int rv, int G);
