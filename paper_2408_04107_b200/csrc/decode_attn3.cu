@@ -30,10 +30,10 @@ constexpr int kTR3 = 32;   // rows per tile
 constexpr int kMaxP3 = 128;  // pieces per pair (partial slots per head)
 constexpr float kLog2e3 = 1.4426950408889634f;
 
-template <int RK, int G>
+template <int RK>
 struct DA3 {
   static constexpr uint32_t KT = kTR3 * RK * 2;           // one K' (or V') tile of pool 0
-  static constexpr uint32_t QB = G * RK * 2;              // q of the pair's G heads (bf16)
+  static constexpr uint32_t QB = 8 * RK * 2;              // q of the pair's G <= 8 heads (bf16)
   static constexpr uint32_t STAGE = (2 * KT + QB + 127) / 128 * 128;
   static constexpr int NST = 2;
   static constexpr uint32_t WARP_BYTES = NST * STAGE;
@@ -52,6 +52,81 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint3
 __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 __device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
 
+// One 32-key pass of a warp over a tile of width W (a pool-0 row: RK, a pool-1 row: r^u):
+//   S^T[16 (heads g < G, rest zero)][8 keys] = Q[16][16 k] . K'^T[16 k][8 keys]  per n-tile, k-step
+//   O  [16][8 cols]                 += P[16][16 keys] . V'[16 keys][8 cols]
+// lane = 4 g + t holds row g of every accumulator (columns 2t, 2t + 1 of each 8-wide n-tile); the
+// S accumulators of two key n-tiles, rounded to bf16, are the P fragment of one PV k-step.  K' /
+// V' fragments come straight from the row-major tiles with ldmatrix (V' transposed).
+template <int W, int NT, int KSQ>
+__device__ __forceinline__ void attn3_pass(uint32_t kb, uint32_t vb, int np, int lane, const uint32_t (&qa)[KSQ][2],
+                                           float scl, float& m, float& l, float (&oacc)[NT][4]) {
+  constexpr int KS = W / 16, NTW = W / 8;
+  const int tq = lane & 3;
+  float sacc[4][4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) sacc[j][0] = sacc[j][1] = sacc[j][2] = sacc[j][3] = 0.f;
+  // lane's ldmatrix row / column offsets (bytes) of the K' fragments: n-tile 2jp + (lane >> 4)
+  const uint32_t krow = static_cast<uint32_t>((8 * (lane >> 4) + (lane & 7)) * W * 2 + ((lane >> 3) & 1) * 16);
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+#pragma unroll
+    for (int jp = 0; jp < 2; ++jp) {
+      uint32_t b0, b1, b2, b3;
+      asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
+                   : "r"(kb + krow + static_cast<uint32_t>(jp * 16 * W * 2 + ks * 32)));
+      mma_bf16_16816(sacc[2 * jp], qa[ks][0], 0u, qa[ks][1], 0u, b0, b1);
+      mma_bf16_16816(sacc[2 * jp + 1], qa[ks][0], 0u, qa[ks][1], 0u, b2, b3);
+    }
+  }
+  // online softmax of row g over the 32 keys (4 lanes per row), log2 domain
+  float x[4][2];
+  float tm = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      x[j][e] = 8 * j + 2 * tq + e < np ? sacc[j][e] * scl : -INFINITY;
+      tm = fmaxf(tm, x[j][e]);
+    }
+  tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 1));
+  tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 2));
+  const float mn = fmaxf(m, tm);
+  const float alpha = exp2f(m - mn);  // 0 on the first pass of a piece
+  float ps = 0.f;
+  uint32_t pa[2][2];  // P fragments of the two 16-key k-steps (row g; rows g + 8 zero)
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float p0 = exp2f(x[j][0] - mn), p1 = exp2f(x[j][1] - mn);
+    ps += p0 + p1;
+    pa[j >> 1][j & 1] = pack_bf16x2(p0, p1);  // P rounded to bf16 before PV (l from the unrounded P)
+  }
+  ps += __shfl_xor_sync(0xffffffffu, ps, 1);
+  ps += __shfl_xor_sync(0xffffffffu, ps, 2);
+  l = l * alpha + ps;
+  m = mn;
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    oacc[j][0] *= alpha;
+    oacc[j][1] *= alpha;
+  }
+  // PV over the first W / 8 output n-tiles (a pool-1 row adds to its first r^u dims only)
+  const uint32_t vrow = static_cast<uint32_t>((lane & 15) * W * 2 + (lane >> 4) * 16);
+#pragma unroll
+  for (int kk = 0; kk < 2; ++kk) {
+#pragma unroll
+    for (int jn = 0; jn < NTW; jn += 2) {
+      uint32_t b0, b1, b2, b3;
+      asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
+                   : "r"(vb + vrow + static_cast<uint32_t>(kk * 16 * W * 2 + jn * 16)));
+      mma_bf16_16816(oacc[jn], pa[kk][0], 0u, pa[kk][1], 0u, b0, b1);
+      mma_bf16_16816(oacc[jn + 1], pa[kk][0], 0u, pa[kk][1], 0u, b2, b3);
+    }
+  }
+}
+
 // One warp's walk over its tiles: pairs p = b * Nkv + g in order; in a pair, pool-0 rows then
 // pool-1 rows; only the rows whose cost start lies in [lo, hi).
 struct Walk {
@@ -62,9 +137,9 @@ struct Walk {
 
 }  // namespace
 
-template <int RK, int G>
+template <int RK, int RK1>
 __global__ void __launch_bounds__(kW3 * 32, 1) decode_attn3_kernel(const DecodeAttnArgs a, int w_launch) {
-  using C = DA3<RK, G>;
+  using C = DA3<RK>;
   extern __shared__ __align__(128) uint8_t dsm[];
   __shared__ int64_t s_pb[129];  // cost prefix over sequences (B <= 128)
   __shared__ int s_n0[128], s_n1[128];
@@ -81,7 +156,7 @@ __global__ void __launch_bounds__(kW3 * 32, 1) decode_attn3_kernel(const DecodeA
   pdl_trigger();
   pdl_wait();  // the row counts (and the new rows) come from the predecessor
 
-  const int B = a.B, Nkv = a.Nkv, rk1 = a.k1 ? a.rk1 : 0;
+  const int B = a.B, Nkv = a.Nkv, G = a.Nh / a.Nkv, rk1 = RK1;
   const int64_t w0 = RK, w1 = rk1;  // cost of one row of each pool (K' + V' bytes / 4)
   if (threadIdx.x < 32) {
     // per-sequence row counts and the cost prefix (one warp; B <= 128)
@@ -208,7 +283,7 @@ __global__ void __launch_bounds__(kW3 * 32, 1) decode_attn3_kernel(const DecodeA
   const float scl = a.scale * kLog2e3;
   // rows per tile: 32 of pool 0; as many 32-row passes of the narrower pool 1 as fill the same
   // bytes (c3: 96 rows of r^u = 32), so the bytes in flight per warp stay the same in both pools
-  const int tr1 = rk1 > 0 ? kTR3 * max(1, RK / rk1) : kTR3;
+  constexpr int tr1 = RK1 > 0 ? kTR3 * (RK / RK1 > 0 ? RK / RK1 : 1) : kTR3;
   auto tile_rows = [&](const Walk& k) { return min(k.pool == 0 ? kTR3 : tr1, k.r_end - k.r); };
   // issue side (lane 0): the tile at walk ki into stage st
   auto issue = [&](const Walk& k, int st) {
@@ -220,10 +295,11 @@ __global__ void __launch_bounds__(kW3 * 32, 1) decode_attn3_kernel(const DecodeA
     const int64_t row = (static_cast<int64_t>(b) * Nkv + g) * a.S_cap + k.r;
     const uint32_t rb = static_cast<uint32_t>(nr) * width * 2u;
     uint8_t* dst = ring + st * C::STAGE;
-    mbar_arrive_expect_tx(&wbar[st], 2 * rb + C::QB);
+    const uint32_t qb = static_cast<uint32_t>(G * RK * 2);
+    mbar_arrive_expect_tx(&wbar[st], 2 * rb + qb);
     bulk_g2s(dst, kp + row * width, rb, &wbar[st]);
     bulk_g2s(dst + C::KT, vp + row * width, rb, &wbar[st]);
-    bulk_g2s(dst + 2 * C::KT, a.q + b * a.ldq + static_cast<int64_t>(g) * G * a.rk, C::QB, &wbar[st]);
+    bulk_g2s(dst + 2 * C::KT, a.q + b * a.ldq + static_cast<int64_t>(g) * G * a.rk, qb, &wbar[st]);
   };
 
   Walk wi, wc;  // issue-side and compute-side walks
@@ -236,12 +312,7 @@ __global__ void __launch_bounds__(kW3 * 32, 1) decode_attn3_kernel(const DecodeA
       advance(wi, tile_rows(wi));
     }
 
-  // ---- tensor-core formulation (mma.sync m16n8k16, bf16 in, f32 accumulate), queries on M:
-  //   S^T[16 (G heads, rest zero)][8 keys] = Q[16][16 k] . K'^T[16 k][8 keys]   per n-tile, k-step
-  //   O  [16][8 cols]               += P[16][16 keys] . V'[16 keys][8 cols]
-  // lane = 4 g + t holds row g (head g < G) of every accumulator: columns 2t, 2t+1 of each 8-wide
-  // n-tile; the S accumulators of two key n-tiles, rounded to bf16, are the P fragment of one PV
-  // k-step.  K' / V' fragments come straight from the row-major tiles with ldmatrix (V' transposed).
+  // ---- tensor-core formulation (attn3_pass): mma.sync m16n8k16, bf16 in, f32 accumulate
   constexpr int KS = RK / 16;   // k-steps of a pool-0 row
   constexpr int NT = RK / 8;    // output n-tiles
   const int g = lane >> 2, tq = lane & 3;
@@ -262,8 +333,6 @@ __global__ void __launch_bounds__(kW3 * 32, 1) decode_attn3_kernel(const DecodeA
     const int st = t % C::NST;
     mbar_wait(&wbar[st], (t / C::NST) & 1);
     const int p = wc.p, pool = wc.pool, nr = tile_rows(wc);
-    const int width = pool == 0 ? RK : rk1;
-    const int ks_n = width >> 4, nt_n = width >> 3;
     if (new_piece) {  // q of this pair (bf16 in the stage) -> A fragments
       const uint16_t* Qt = reinterpret_cast<const uint16_t*>(ring + st * C::STAGE + 2 * C::KT);
 #pragma unroll
@@ -273,6 +342,7 @@ __global__ void __launch_bounds__(kW3 * 32, 1) decode_attn3_kernel(const DecodeA
       }
       new_piece = false;
     }
+    const int width = pool == 0 ? RK : RK1;
     for (int j0 = 0; j0 < nr; j0 += kTR3) {  // 32-key passes
       const int np = min(kTR3, nr - j0);
       const uint32_t kb = ring_s + st * C::STAGE + static_cast<uint32_t>(j0 * width * 2);
@@ -285,77 +355,15 @@ __global__ void __launch_bounds__(kW3 * 32, 1) decode_attn3_kernel(const DecodeA
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before the stage's next bulk copy
         __syncwarp();
       }
-      // ---- scores: 4 n-tiles of 8 keys
-      float sacc[4][4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) sacc[j][0] = sacc[j][1] = sacc[j][2] = sacc[j][3] = 0.f;
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        if (ks < ks_n) {
-#pragma unroll
-          for (int jp = 0; jp < 2; ++jp) {  // n-tiles 2jp, 2jp + 1
-            const int row = 8 * (2 * jp + (lane >> 4)) + (lane & 7);
-            const int col = ks * 16 + ((lane >> 3) & 1) * 8;
-            uint32_t b0, b1, b2, b3;
-            asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
-                         : "r"(kb + static_cast<uint32_t>((row * width + col) * 2)));
-            mma_bf16_16816(sacc[2 * jp], qa[ks][0], 0u, qa[ks][1], 0u, b0, b1);
-            mma_bf16_16816(sacc[2 * jp + 1], qa[ks][0], 0u, qa[ks][1], 0u, b2, b3);
-          }
+      if constexpr (RK1 > 0) {
+        if (pool == 1) {
+          attn3_pass<RK1, NT, KS>(kb, vb, np, lane, qa, scl, m, l, oacc);
+          continue;
         }
       }
-      // ---- online softmax of row g over the 32 keys (4 lanes per row), log2 domain
-      float x[4][2];
-      float tm = -INFINITY;
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int key = 8 * j + 2 * tq + e;
-          x[j][e] = key < np ? sacc[j][e] * scl : -INFINITY;
-          tm = fmaxf(tm, x[j][e]);
-        }
-      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 1));
-      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 2));
-      const float mn = fmaxf(m, tm);
-      const float alpha = exp2f(m - mn);  // 0 on the first pass of a piece
-      float ps = 0.f;
-      uint32_t pa[2][2];  // P fragments of the two 16-key k-steps (row g; rows g + 8 zero)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float p0 = exp2f(x[j][0] - mn), p1 = exp2f(x[j][1] - mn);
-        ps += p0 + p1;
-        pa[j >> 1][j & 1] = pack_bf16x2(p0, p1);  // P rounded to bf16 before PV (l from unrounded P)
-      }
-      ps += __shfl_xor_sync(0xffffffffu, ps, 1);
-      ps += __shfl_xor_sync(0xffffffffu, ps, 2);
-      l = l * alpha + ps;
-      m = mn;
-#pragma unroll
-      for (int j = 0; j < NT; ++j) {
-        oacc[j][0] *= alpha;
-        oacc[j][1] *= alpha;
-      }
-      // ---- PV: O[.][cols] += P[.][keys] V'[keys][cols], V' fragments by transposed ldmatrix
-#pragma unroll
-      for (int kk = 0; kk < 2; ++kk) {
-#pragma unroll
-        for (int jn = 0; jn < NT; jn += 2) {  // output n-tiles jn, jn + 1 (16 columns)
-          if (jn < nt_n) {
-            const int row = kk * 16 + (lane & 15);
-            const int col = jn * 8 + (lane >> 4) * 8;
-            uint32_t b0, b1, b2, b3;
-            asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
-                         : "r"(vb + static_cast<uint32_t>((row * width + col) * 2)));
-            mma_bf16_16816(oacc[jn], pa[kk][0], 0u, pa[kk][1], 0u, b0, b1);
-            mma_bf16_16816(oacc[jn + 1], pa[kk][0], 0u, pa[kk][1], 0u, b2, b3);
-          }
-        }
-      }
-      __syncwarp();
+      attn3_pass<RK, NT, KS>(kb, vb, np, lane, qa, scl, m, l, oacc);
     }
+    __syncwarp();
     // refill this stage with the tile NST ahead
     if (lane == 0 && !wi.done) {
       issue(wi, st);
@@ -430,14 +438,14 @@ __global__ void __launch_bounds__(kW3 * 32, 1) decode_attn3_kernel(const DecodeA
 }
 
 // ------------------------------------------------------------------ host
-template <int RK, int G>
+template <int RK, int RK1>
 static cudaError_t launch3_t(const DecodeAttnArgs& a, cudaStream_t stream) {
-  using C = DA3<RK, G>;
+  using C = DA3<RK>;
   const size_t smem = static_cast<size_t>(kW3) * C::WARP_BYTES;
-  if (smem > 220 * 1024) return cudaErrorNotSupported;
+  if (smem > 227 * 1024) return cudaErrorNotSupported;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(decode_attn3_kernel<RK, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(decode_attn3_kernel<RK, RK1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     attr = true;
@@ -448,19 +456,20 @@ static cudaError_t launch3_t(const DecodeAttnArgs& a, cudaStream_t stream) {
   const int64_t wmax = static_cast<int64_t>(pairs) * 64;
   if (static_cast<int64_t>(grid) * kW3 > wmax) grid = static_cast<int>((wmax + kW3 - 1) / kW3);
   prof_mark(stream, true, kProfAttnDecode);
-  cudaError_t e = launch_k(decode_attn3_kernel<RK, G>, dim3(grid), dim3(kW3 * 32), smem, stream, g_pdl, a, grid * kW3);
+  cudaError_t e = launch_k(decode_attn3_kernel<RK, RK1>, dim3(grid), dim3(kW3 * 32), smem, stream, g_pdl, a, grid * kW3);
   prof_mark(stream, false, kProfAttnDecode);
   ++g_launches;
   return e;
 }
 
 template <int RK>
-static cudaError_t launch3_g(const DecodeAttnArgs& a, cudaStream_t s) {
-  switch (a.Nh / a.Nkv) {
-    case 1: return launch3_t<RK, 1>(a, s);
-    case 2: return launch3_t<RK, 2>(a, s);
-    case 4: return launch3_t<RK, 4>(a, s);
-    case 8: return launch3_t<RK, 8>(a, s);
+static cudaError_t launch3_r1(const DecodeAttnArgs& a, cudaStream_t s) {
+  const int r1 = a.k1 ? a.rk1 : 0;
+  switch (r1) {
+    case 0: return launch3_t<RK, 0>(a, s);
+    case 16: return launch3_t<RK, 16>(a, s);
+    case 32: if constexpr (RK >= 32) return launch3_t<RK, 32>(a, s); else return cudaErrorNotSupported;
+    case 64: if constexpr (RK >= 64) return launch3_t<RK, 64>(a, s); else return cudaErrorNotSupported;
     default: return cudaErrorNotSupported;
   }
 }
@@ -468,9 +477,9 @@ static cudaError_t launch3_g(const DecodeAttnArgs& a, cudaStream_t s) {
 bool decode3_supported(const DecodeAttnArgs& a) {
   const int G = a.Nkv > 0 ? a.Nh / a.Nkv : 0;
   if (a.kv_fp8 || !a.counters || !a.part || a.B < 1 || a.B > 128) return false;
-  if (G != 1 && G != 2 && G != 4 && G != 8) return false;
-  if (a.rk != a.rv || (a.rk != 32 && a.rk != 64 && a.rk != 96)) return false;  // 2 x 8 warps x 2 stages fit
-  if (a.k1 && (a.rk1 != a.rv1 || a.rk1 % 8 != 0 || a.rk1 < 8 || a.rk1 > a.rk)) return false;
+  if (G < 1 || G > 8 || a.Nh % a.Nkv != 0) return false;
+  if (a.rk != a.rv || (a.rk != 32 && a.rk != 64 && a.rk != 96)) return false;
+  if (a.k1 && (a.rk1 != a.rv1 || (a.rk1 != 16 && a.rk1 != 32 && a.rk1 != 64) || a.rk1 > a.rk)) return false;
   if (a.ldq % 8 != 0) return false;
   return true;
 }
@@ -478,9 +487,9 @@ bool decode3_supported(const DecodeAttnArgs& a) {
 cudaError_t launch_decode_attention3(const DecodeAttnArgs& a, cudaStream_t s) {
   if (!decode3_supported(a)) return cudaErrorNotSupported;
   switch (a.rk) {
-    case 32: return launch3_g<32>(a, s);
-    case 64: return launch3_g<64>(a, s);
-    case 96: return launch3_g<96>(a, s);
+    case 32: return launch3_r1<32>(a, s);
+    case 64: return launch3_r1<64>(a, s);
+    case 96: return launch3_r1<96>(a, s);
     default: return cudaErrorNotSupported;
   }
 }
