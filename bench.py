@@ -917,7 +917,7 @@ def run_zdc(args):
     log("graph warm-up done")
     if world > 1:
         dist.barrier()
-    clk = ClockSampler(local)
+    clk = ClockSampler(local, period_ms=20)
     clk.start()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)

@@ -469,12 +469,12 @@ cudaError_t launch_gemm(const uint16_t* A, int64_t lda, const uint16_t* B, int64
   int BN = N > 128 ? 256 : 128;
   Epilogue ep = epi;
   ep.k_splits = 1;
-  // skinny M (decode, B > 8): BN = 128 when 256-wide tiles would be few (< 40: c4 a1 20, a5 32 tiles;
-  // 128 measured 4 % faster per c4 layer-step); ZDC_SKINNY_BN forces 128 / 256 (diagnostic builds)
+  // skinny M (decode, B > 8): BN = 128 (c4 layer-step 4 % faster than 256-wide tiles; c3 a1, 45
+  // tiles of 256, 111.6 vs 114.8 us per layer-step); ZDC_SKINNY_BN=256 forces 256 (diagnostic builds)
   static const int skinny_bn = knob("ZDC_SKINNY_BN", 0);
   static const int skinny_ar = knob("ZDC_SKINNY_AR", 0);  // 128 = load full 128-row A tiles (round 1)
   const bool skinny = epi.ws && epi.ws_cnt && M <= 128 && N % 8 == 0;
-  if (skinny && N > 128) BN = skinny_bn == 128 || (skinny_bn == 0 && (N + 255) / 256 < 40) ? 128 : 256;
+  if (skinny && N > 128) BN = skinny_bn == 256 ? 256 : 128;
   // A rows per stage: the batch rounded up to 32 / 64 (more weight stages in flight), else 128
   const int AR = !skinny || skinny_ar == 128 ? 128 : M <= 32 ? 32 : M <= 64 ? 64 : 128;
   if (skinny) {
