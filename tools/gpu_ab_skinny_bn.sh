@@ -5,4 +5,4 @@ run() { ZDC_LIB_PATH=$D timeout 900 env "$@" python bench.py --steps 1 --warmup 
 import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); o=d['other_configs']
 for k in ('c3','c4'):
   x=o[k]; print(k, 'decode us', x['decode']['us_per_layer_step'], 'frac', x['decode']['frac'])"; }
-for v in 0 256 128; do echo "== skinny_bn $v"; run ZDC_SKINNY_BN=$v; done 2>&1 | tee gpurun_out/s3/ab_skinny_bn.txt
+for v in 0 1 2 3 4; do echo "== skinny_sk $v"; run ZDC_SKINNY_SK=$v; done 2>&1 | tee gpurun_out/s3/ab_skinny_sk.txt

@@ -1,6 +1,6 @@
 """Small end-to-end run of every kernel family for compute-sanitizer (racecheck / synccheck /
 memcheck): prefill (tcgen05 GEMM, attention v4 r<=96 and v3 r=128), decode (fused layer-step at
-B=2, split-K GEMM + tcgen05 GQA attention at B=10, CUDA-core split-K attention), the token split
+B=2, split-K GEMM + tcgen05 GQA attention at B=10, decode attention v3 over one / two pools), the token split
 (select / rank / pack / append / classify), the FP8 cache, and the GPU fold (K-means + Jacobi)."""
 import os
 import sys
@@ -34,7 +34,9 @@ def run(dims, plan, B, S, T, seed):
 run(Z.Dims(1, 256, 4, 4, 64), Z.plan_uniform(1, 32), 2, 160, 3, 1)                 # v4, fused decode
 run(Z.Dims(1, 256, 8, 2, 64), Z.plan_uniform(1, 64), 10, 140, 3, 2)                # GQA: split-K GEMM + TC attn
 run(Z.Dims(1, 256, 2, 2, 128), Z.plan_uniform(1, 128), 1, 130, 2, 3)               # v3 (r = 128)
-run(Z.Dims(2, 256, 4, 4, 64), Z.plan_split(2, 32, 16, [[0, 1]], [5000]), 2, 150, 3, 4)  # token split
+run(Z.Dims(2, 256, 4, 4, 64), Z.plan_split(2, 32, 16, [[0, 1]], [5000]), 2, 150, 3, 4)  # token split (v3 32/16)
+run(Z.Dims(2, 384, 4, 4, 128), Z.plan_split(2, 96, 32, [[0, 1]], [5000]), 3, 140, 3, 6)  # token split (v3 96/32)
+run(Z.Dims(1, 256, 4, 4, 64), Z.plan_uniform(1, 64), 10, 120, 3, 7)                # B > 8 uniform (v3 64/0)
 p8 = Z.plan_uniform(1, 32)
 p8.kv_fp8 = 1
 run(Z.Dims(1, 256, 4, 4, 64), p8, 2, 150, 3, 5)                                    # FP8 cache
