@@ -133,6 +133,13 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def wait_first(self, timeout_s: float = 3.0):
+        """Block until nvidia-smi has printed its first sample (it starts ~0.5 s late), so the
+        timed region that follows is sampled from its start."""
+        t0 = time.time()
+        while self.proc and not self.lines and time.time() - t0 < timeout_s:
+            time.sleep(0.01)
+
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -919,6 +926,7 @@ def run_zdc(args):
         dist.barrier()
     clk = ClockSampler(local, period_ms=20)
     clk.start()
+    clk.wait_first()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     pre_ms, dec_ms = [], []
