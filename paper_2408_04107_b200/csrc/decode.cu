@@ -586,8 +586,11 @@ static bool v2_width(int w) { return w == 32 || w == 64 || w == 96 || w == 128; 
 
 static const bool g_dec_attn_v3 = knob("ZDC_DEC_ATTN_V3", 1) != 0;
 cudaError_t launch_decode_attention(const DecodeAttnArgs& a_in, cudaStream_t stream) {
-  // v3 (decode_attn3.cu): the byte-balanced flat split, both pools in one launch
-  if (g_dec_attn_v3 && decode3_supported(a_in)) {
+  // v3 (decode_attn3.cu): the byte-balanced flat split, both pools in one launch -- for token-split
+  // layers and for at least one (sequence, KV head) pair per SM; with fewer pairs (e.g. B = 1,
+  // 32 heads) its warps' shares are a few tiles each and v2's per-split CTAs are faster
+  // (21.2 vs 12.4 us at the c2 shape)
+  if (g_dec_attn_v3 && decode3_supported(a_in) && (a_in.k1 || a_in.B * a_in.Nkv >= num_sms())) {
     const cudaError_t e3 = launch_decode_attention3(a_in, stream);
     if (e3 != cudaErrorNotSupported) return e3;
     cudaGetLastError();  // shape outside v3's shared-memory budget: v2 below

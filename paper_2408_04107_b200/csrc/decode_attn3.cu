@@ -329,21 +329,36 @@ __global__ void __launch_bounds__(kW3 * 32, 1) decode_attn3_kernel(const DecodeA
       lastw = __shfl_sync(0xffffffffu, lastw, 0);
       if (lastw) {
         __threadfence();
+        // LSE merge of the pieces, lane-parallel over pieces: lane q holds piece q's (m, l) and
+        // weight 2^(m_q - M) (chunks of 32 pieces), broadcast by shuffle into the column sums
         for (int gi = 0; gi < G; ++gi) {
           const float* hp = a.part + (static_cast<int64_t>(b) * a.Nh + gg * G + gi) * kMaxP3 * (RVO + 2);
           float M = -INFINITY;
-          for (int q = 0; q < pieces; ++q) M = fmaxf(M, __ldcg(hp + q * (RVO + 2) + RVO));
-          for (int col = lane; col < RVO; col += 32) {
-            float L = 0.f, O = 0.f;
-            for (int q = 0; q < pieces; ++q) {
-              const float ms = __ldcg(hp + q * (RVO + 2) + RVO);
-              const float f = ms == -INFINITY ? 0.f : exp2f(ms - M);
-              L = fmaf(f, __ldcg(hp + q * (RVO + 2) + RVO + 1), L);
-              O = fmaf(f, __ldcg(hp + q * (RVO + 2) + col), O);
-            }
-            a.o[b * a.ldo + (gg * G + gi) * RVO + col] = f32_to_bf16_bits(O / L);
-            if (col == 0 && a.lse) a.lse[b * a.Nh + gg * G + gi] = (M + log2f(L)) / kLog2e3;
+          for (int q = lane; q < pieces; q += 32) M = fmaxf(M, __ldcg(hp + q * (RVO + 2) + RVO));
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+          float L = 0.f;
+          for (int q = lane; q < pieces; q += 32) {
+            const float ms = __ldcg(hp + q * (RVO + 2) + RVO);
+            L += (ms == -INFINITY ? 0.f : exp2f(ms - M)) * __ldcg(hp + q * (RVO + 2) + RVO + 1);
           }
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
+          const float inv = 1.f / L;
+          for (int col = lane; col < RVO; col += 32) {
+            float O = 0.f;
+            for (int q0 = 0; q0 < pieces; q0 += 32) {
+              const int q = q0 + lane;
+              const float ms = q < pieces ? __ldcg(hp + q * (RVO + 2) + RVO) : -INFINITY;
+              const float fq = ms == -INFINITY ? 0.f : exp2f(ms - M);  // lane q's weight
+              const int nq = min(32, pieces - q0);
+#pragma unroll 8
+              for (int u = 0; u < nq; ++u)
+                O = fmaf(__shfl_sync(0xffffffffu, fq, u), __ldcg(hp + (q0 + u) * (RVO + 2) + col), O);
+            }
+            a.o[b * a.ldo + (gg * G + gi) * RVO + col] = f32_to_bf16_bits(O * inv);
+          }
+          if (lane == 0 && a.lse) a.lse[b * a.Nh + gg * G + gi] = (M + log2f(L)) / kLog2e3;
         }
         if (lane == 0) a.counters[p] = 0;
       }

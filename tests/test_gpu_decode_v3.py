@@ -70,8 +70,8 @@ def test_v3_split_decode_parity(dims, ri, ru, B, S, T, g, mode):
 
 
 @pytest.mark.parametrize("dims,r,B,S,T", [
-    (Dims(1, 256, 4, 4, 64), 64, 12, 150, 4),     # uniform, G = 1, B > 8 (v3 64 / 0)
-    (Dims(1, 256, 4, 4, 64), 32, 10, 40, 3),      # uniform r = 32, short context (few rows per warp)
+    (Dims(1, 256, 16, 16, 64), 64, 10, 150, 4),   # uniform, G = 1, 160 pairs >= the SMs (v3 64 / 0)
+    (Dims(1, 256, 16, 16, 64), 32, 12, 40, 3),    # uniform r = 32, short context (few rows per warp)
 ])
 def test_v3_uniform_decode_parity(dims, r, B, S, T):
     plan = plan_uniform(dims.n_layers, r)
