@@ -54,7 +54,7 @@ struct Walk {
 }  // namespace
 
 template <int RK, int RK1>
-__global__ void __launch_bounds__(kW3 * 32, 1) decode_attn3_kernel(const DecodeAttnArgs a, int w_launch) {
+__global__ void __launch_bounds__(kW3 * 32, 1) decode_attn3_kernel(const DecodeAttnArgs a, int w_launch, int q_once) {
   using C = DA3<RK>;
   extern __shared__ __align__(128) uint8_t dsm[];
   __shared__ int64_t s_pb[129];  // cost prefix over sequences (B <= 128)
@@ -202,6 +202,7 @@ __global__ void __launch_bounds__(kW3 * 32, 1) decode_attn3_kernel(const DecodeA
   constexpr int tr1 = RK1 > 0 ? kTR3 * (RK / RK1 > 0 ? RK / RK1 : 1) : kTR3;
   auto tile_rows = [&](const Walk& k) { return min(k.pool == 0 ? kTR3 : tr1, k.r_end - k.r); };
   // issue side (lane 0): the tile at walk ki into stage st
+  int last_p = -1;  // issue side: pair of the previous tile (q is copied with a piece's first tile only)
   auto issue = [&](const Walk& k, int st) {
     const int b = k.p / Nkv, g = k.p - b * Nkv;
     const int nr = tile_rows(k);
@@ -211,11 +212,13 @@ __global__ void __launch_bounds__(kW3 * 32, 1) decode_attn3_kernel(const DecodeA
     const int64_t row = (static_cast<int64_t>(b) * Nkv + g) * a.S_cap + k.r;
     const uint32_t rb = static_cast<uint32_t>(nr) * width * 2u;
     uint8_t* dst = ring + st * C::STAGE;
-    const uint32_t qb = static_cast<uint32_t>(G * RK * 2);
+    const bool with_q = !q_once || k.p != last_p;
+    last_p = k.p;
+    const uint32_t qb = with_q ? static_cast<uint32_t>(G * RK * 2) : 0u;
     mbar_arrive_expect_tx(&wbar[st], 2 * rb + qb);
     bulk_g2s(dst, kp + row * width, rb, &wbar[st]);
     bulk_g2s(dst + C::KT, vp + row * width, rb, &wbar[st]);
-    bulk_g2s(dst + 2 * C::KT, a.q + b * a.ldq + static_cast<int64_t>(g) * G * a.rk, qb, &wbar[st]);
+    if (with_q) bulk_g2s(dst + 2 * C::KT, a.q + b * a.ldq + static_cast<int64_t>(g) * G * a.rk, qb, &wbar[st]);
   };
 
   Walk wi, wc;  // issue-side and compute-side walks
@@ -387,7 +390,9 @@ static cudaError_t launch3_t(const DecodeAttnArgs& a, cudaStream_t stream) {
   const int64_t wmax = static_cast<int64_t>(pairs) * 64;
   if (static_cast<int64_t>(grid) * kW3 > wmax) grid = static_cast<int>((wmax + kW3 - 1) / kW3);
   prof_mark(stream, true, kProfAttnDecode);
-  cudaError_t e = launch_k(decode_attn3_kernel<RK, RK1>, dim3(grid), dim3(kW3 * 32), smem, stream, g_pdl, a, grid * kW3);
+  static const int q_once = knob("ZDC_V3_QONCE", 1);  // q copied with a piece's first tile only
+  cudaError_t e = launch_k(decode_attn3_kernel<RK, RK1>, dim3(grid), dim3(kW3 * 32), smem, stream, g_pdl, a, grid * kW3,
+                           q_once);
   prof_mark(stream, false, kProfAttnDecode);
   ++g_launches;
   return e;
