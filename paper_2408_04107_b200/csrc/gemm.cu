@@ -478,9 +478,20 @@ cudaError_t launch_gemm(const uint16_t* A, int64_t lda, const uint16_t* B, int64
   // A rows per stage: the batch rounded up to 32 / 64 (more weight stages in flight), else 128
   const int AR = !skinny || skinny_ar == 128 ? 128 : M <= 32 ? 32 : M <= 64 ? 64 : 128;
   if (skinny) {
-    // split K so the weight stream spreads over the SMs (>= 4 stage blocks per split)
+    // split K so the weight stream spreads over the SMs (>= 4 stage blocks per split): the split
+    // count of best wave efficiency items / (rounds x SMs), items = tiles x sk, sk <= 4 (ties: fewer
+    // splits) -- c3 a1 (90 tiles of 128) 3, c3 a5 / c4 a1 (40) 3, c4 a5 (64) 2
     const int tiles = (N + BN - 1) / BN, kbs = K / 64;
-    int sk = num_sms() / tiles;
+    int sk = 1;
+    double best = 0.0;
+    for (int c = 1; c <= 4; ++c) {
+      const int items = tiles * c, rounds = (items + num_sms() - 1) / num_sms();
+      const double eff = static_cast<double>(items) / (static_cast<double>(rounds) * num_sms());
+      if (eff > best + 1e-9) {
+        best = eff;
+        sk = c;
+      }
+    }
     if (sk > kbs / 4) sk = kbs / 4;
     if (sk > 1) {
       const int kpb = (kbs + sk - 1) / sk;
